@@ -1,0 +1,106 @@
+"""Oracle network steps — TEST INFRASTRUCTURE ONLY.
+
+Composes the oracle's per-op definitions in exactly the order of the paper's
+listings on dense BTCHW arrays:
+
+* front end — Listing 1: filter -> threshold(0.01) -> code(T);
+* inference — Listing 5: conv -> fire(theta) -> pool ... -> gather;
+* training of layer L — Listing 3: forward to layer L's input,
+  conv_L -> threshold(theta_L) -> inhibit -> convwta -> fire -> conv_L.stdp;
+* R-STDP: winners routed to reward/punish configs by label.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import (conv, conv_event, dog_bank, filter_apply, fire, gabor_bank, gather, inhibit,
+               lat_to_dense, log_kernels, pool, rank_code, rstdp_route, stdp, threshold, wta)
+
+
+def filter_bank(cfg: dict) -> np.ndarray:
+    fr = cfg["front"]
+    r = fr["radius"]
+    if fr["kind"] == "dog":
+        return dog_bank(fr["pairs"], r)
+    if fr["kind"] == "log":
+        return log_kernels(fr["stds"], r)
+    if fr["kind"] == "gabor":
+        return gabor_bank(fr["params"], r)
+    raise ValueError(fr["kind"])
+
+
+def front_end(cfg: dict, imgs: np.ndarray):
+    """Listing 1: -> (filter response fp32 [B][C][H][W], latency u8 [B][C][H][W])."""
+    fr = cfg["front"]
+    y = filter_apply(imgs, filter_bank(cfg), fr["pad"])
+    lat = rank_code(y, cfg["T"], fr["thresh"], fr["sort"])
+    return y, lat
+
+
+def _conv(S, W, L, event: bool, T: int):
+    st, pd = (L["stride"],) * 2, (L["pad"],) * 2
+    if event:
+        from . import dense_to_lat
+        return conv_event(dense_to_lat(S), T, W, st, pd)
+    return conv(S, W, st, pd)
+
+
+def _pool(S, L):
+    p = L["pool"]
+    if not p:
+        return S
+    return pool(S, (p["kernel"],) * 2, (p["stride"],) * 2, (p["pad"],) * 2)
+
+
+def forward(cfg: dict, imgs: np.ndarray, weights, upto: int | None = None, event: bool = False):
+    """Dense input trains of every layer up to `upto` (exclusive end = input of layer upto).
+
+    Returns (y, lat0, inputs) where inputs[l] is the dense BTCHW train fed to layer l;
+    if upto is None the list also holds the output train of the last layer (pooled)."""
+    T = cfg["T"]
+    y, lat0 = front_end(cfg, imgs)
+    S = lat_to_dense(lat0, T)
+    inputs = [S]
+    n = len(cfg["layers"]) if upto is None else upto
+    for li in range(n):
+        L = cfg["layers"][li]
+        P = _conv(S, weights[li], L, event, T)
+        S = _pool(fire(P, L["theta"]), L)
+        inputs.append(S)
+    return y, lat0, inputs
+
+
+def train_step(cfg: dict, imgs: np.ndarray, weights, labels=None, event: bool = False):
+    """One training step of layer cfg['train_layer'] (Listing 3; R-STDP for cfg['learning']=='rstdp').
+
+    Returns a dict with every intermediate the GPU path is compared against."""
+    li = cfg["train_layer"]
+    L = cfg["layers"][li]
+    T = cfg["T"]
+    y, lat0, inputs = forward(cfg, imgs, weights, upto=li, event=event)
+    S_in = inputs[li]
+    P = _conv(S_in, weights[li], L, event, T)
+    Q = threshold(P, L["theta"])
+    Qi = inhibit(Q)
+    win, nwin = wta(Qi, L["wta"]["count"], L["wta"]["radius"])
+    if cfg["learning"] == "rstdp":
+        win = rstdp_route(win, nwin, labels, cfg["maps_per_class"])
+    cfgs = [tuple(c) for c in cfg["stdp"]]
+    W_new = stdp(weights[li], S_in, win, nwin, cfgs, (L["stride"],) * 2, (L["pad"],) * 2)
+    return dict(y=y, lat0=lat0, inputs=inputs, S_in=S_in, P=P, Q=Q, Qi=Qi, win=win, nwin=nwin,
+                W_new=W_new, spikes=fire(Qi, 0.0))
+
+
+def infer(cfg: dict, imgs: np.ndarray, weights, event: bool = False):
+    """Listing 5: forward through every layer then gather -> features [B][C][H][W]."""
+    _, _, inputs = forward(cfg, imgs, weights, event=event)
+    return gather(inputs[-1])
+
+
+def sig3(x: float) -> float:
+    if x <= 0:
+        return 0.0
+    e = math.floor(math.log10(x)) - 2
+    return round(x / 10 ** e) * 10 ** e
