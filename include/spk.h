@@ -1,0 +1,292 @@
+/*
+ * spk.h — C ABI of the B200-native Spyker SDNN hot path (libspk.so).
+ *
+ * Paper: "Spyker: High-performance Library for Spiking Deep Neural Networks"
+ * (arXiv 2301.13659).  P:Lnn cites line nn of the paper text
+ * (/root/reference/PAPER.md); DESIGN.md lists every reading taken where the
+ * paper is silent (R-*).
+ *
+ * Conventions for every call
+ *  - Pointers marked [dev] are CUDA device pointers on the current device;
+ *    [host] pointers are read during the call only.  The caller owns and
+ *    allocates every buffer (outputs and workspace); the library allocates
+ *    nothing and keeps no per-call state.
+ *  - Arrays are dense, contiguous, row-major, batch first.  Spike trains are
+ *    carried as first-spike LATENCY MAPS: u8 lat[B][C][H][W], lat = first time
+ *    step the neuron is on, lat = T for "never".  This is lossless for the
+ *    paper's cumulative trains ("when a neuron fires in time step t_i,
+ *    it will also fire at time steps t_{i+1} ... t_n") and T times smaller than
+ *    the dense BTCHW u8 array of P:L60; spk_lat_to_dense / spk_dense_to_lat
+ *    convert.  T <= 254.
+ *  - Calls are asynchronous on `stream` (NULL = legacy default stream) and
+ *    capture into CUDA graphs.  Arguments and shapes are validated on the host
+ *    BEFORE any launch; a failed validation launches nothing and writes
+ *    nothing.  Calls never abort: they return a status and set a thread-local
+ *    message readable with spk_last_error().  Data-dependent faults found on
+ *    the device are reported through device-side outputs (noted per call).
+ *  - Every output is bit-reproducible run to run (no floating-point atomics).
+ */
+#ifndef SPK_H
+#define SPK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* spk_stream; /* == cudaStream_t */
+
+#if defined(__GNUC__)
+#define SPK_API __attribute__((visibility("default")))
+#else
+#define SPK_API
+#endif
+
+typedef enum {
+    SPK_OK = 0,
+    SPK_ERR_ARG = 1,         /* null / misaligned pointer, bad scalar argument */
+    SPK_ERR_SHAPE = 2,       /* geometry violates Eq. 1-3, non-positive size, channel mismatch */
+    SPK_ERR_UNSUPPORTED = 3, /* valid request this build does not implement (e.g. T > 254) */
+    SPK_ERR_WORKSPACE = 4,   /* workspace smaller than the matching *_workspace() query */
+    SPK_ERR_CUDA = 5         /* launch failed; spk_last_error() has cudaGetErrorString */
+} spk_status;
+
+/* Thread-local text of the last non-OK status of this thread ("" if none). */
+SPK_API const char* spk_last_error(void);
+/* ABI version of this header (bumped on any signature change). */
+SPK_API int spk_abi_version(void);
+#define SPK_ABI_VERSION 1
+/* Name of the last kernel launched by this thread (diagnostics). */
+SPK_API const char* spk_last_kernel(void);
+/* Number of kernels this process launched through the library. */
+SPK_API uint64_t spk_launch_count(void);
+
+/* ========================================================================
+ * a1  Feature enhancement filters (Eq. 1)
+ * ======================================================================== */
+
+/* spk_dog — Difference-of-Gaussian filter bank, DoG(size, filters, pad)
+ * (P:L70-72); LoG(sigma) is the pair DoG(sigma*sqrt2, sigma/sqrt2),
+ * DoG(sigma/sqrt2, sigma*sqrt2) and is requested through this call.
+ *   img    [dev]  u8  [B][C][H][W] image; pixel value x = u8 / 255 (R-SCALE).
+ *   sigmas [host] double [K][2] = (sigma1, sigma2) per filter, both > 0.
+ *   radius        kernel edge 2*radius+1 (the paper's `size`, R-RADIUS), 0..7.
+ *   pad           zero padding (P_h = P_w, Eq. 1).
+ *   y      [dev]  f32 [B][C*K][Ho][Wo], channel ci*K + k (R-CHORDER),
+ *                 Ho = H + 2 pad - 2 radius (Eq. 1).
+ * Each Gaussian is normalised to unit discrete sum on [-r, r]^2 (R-DOG-NORM).
+ * Each output is an fp32 fused-multiply-add chain over the taps in row-major
+ * order skipping taps outside the image (R-FILTER-ORDER).
+ * Errors: SPK_ERR_ARG (null, K < 1, sigma <= 0), SPK_ERR_SHAPE (Ho/Wo < 1). */
+SPK_API spk_status spk_dog(const uint8_t* img, int B, int C, int H, int W, const double* sigmas, int K,
+                   int radius, int pad, float* y, spk_stream stream);
+
+/* spk_gabor — Gabor filter bank: params [host] double [K][5] =
+ * (sigma, theta, gamma, lambda, psi); g = exp(-(x'^2 + gamma^2 y'^2)/(2 sigma^2))
+ * * cos(2 pi x'/lambda + psi), x' = x cos theta + y sin theta,
+ * y' = -x sin theta + y cos theta (R-GABOR, unnormalised).  Other arguments,
+ * layout and errors as spk_dog (sigma, gamma, lambda > 0). */
+SPK_API spk_status spk_gabor(const uint8_t* img, int B, int C, int H, int W, const double* params, int K,
+                     int radius, int pad, float* y, spk_stream stream);
+
+/* ========================================================================
+ * a2  Threshold + rank-order coding (Listing 1)
+ * ======================================================================== */
+
+/* Bytes of workspace spk_rank_code needs (0 today; query it anyway). */
+SPK_API size_t spk_rank_code_workspace(int B, int N, int T, int sort);
+
+/* spk_rank_code — per sample b: values v = y[b][0..N) (one sample's C*H*W
+ * response in BTCHW flat order) are thresholded (v <= thresh -> 0, strict,
+ * R-STRICT, `threshold(data, 0.01)` P:L307) and the positives coded into T
+ * cumulative bins.
+ *   sort = 1 (the paper's default, "Spyker sorts the intensity values"): the
+ *     n positives are ranked by (value desc, flat index asc) (R-TIE) and
+ *     lat = floor(rank * T / n) ("distributed among time steps evenly",
+ *     R-BINS); ranking is per sample.
+ *   sort = 0 ("it can be disabled", R-SORTOFF): lat = min(T-1,
+ *     floor(T*(vmax - v)/((vmax - vmin) + ulp(vmax)))) in fp32, per sample.
+ *   non-positives: lat = T (never).
+ *   y   [dev] f32 [B][N];  lat [dev] u8 [B][N].  N <= 2^24.  T in 1..254.
+ * Errors: SPK_ERR_ARG, SPK_ERR_SHAPE (N < 1), SPK_ERR_UNSUPPORTED (T > 254),
+ * SPK_ERR_WORKSPACE. */
+SPK_API spk_status spk_rank_code(const float* y, int B, int N, int T, float thresh, int sort, uint8_t* lat,
+                         void* ws, size_t ws_bytes, spk_stream stream);
+
+/* ========================================================================
+ * a3  Spiking convolution (Eq. 2) + a4 IF epilogues
+ * ======================================================================== */
+
+typedef struct {
+    int B, T;            /* batch, time steps */
+    int Ci, Hi, Wi;      /* input latency map [B][Ci][Hi][Wi] */
+    int Co, Kh, Kw;      /* kernel [Co][Ci][Kh][Kw] */
+    int Sh, Sw, Ph, Pw;  /* stride, zero padding (Eq. 2) */
+} spk_conv_geom;
+
+typedef struct {
+    int Lh, Lw, Sh, Sw, Ph, Pw; /* window, stride, zero padding (Eq. 3) */
+} spk_pool_geom;
+
+typedef enum {
+    /* fp32 CUDA-core reference variant: potentials accumulated in fp32. */
+    SPK_PREC_FP32 = 0,
+    /* tcgen05 tensor-core path, exact: weights as 23-bit fixed point
+     * w = s * sum_d q_d 2^(8d-23) (three u8 digit planes, s = smallest power of
+     * two >= w_max), spikes as u8 {0,1}, kind::i8 MMAs with s32 accumulators;
+     * potentials are the exact integer sums rounded once to fp32 (error
+     * <= n_active * s * 2^-24 against the fp32-weight sum). */
+    SPK_PREC_EXACT_I8 = 1
+} spk_precision;
+
+typedef enum {
+    /* out0 = f32 potentials P[B][T][Co][Ho][Wo] ("internal potentials"). */
+    SPK_EPI_POTENTIAL = 0,
+    /* IF fire: out0 = u8 lat[B][Co][Ho][Wo] = first t with P[t] > theta
+     * (strict, R-STRICT), T if none; out1 (nullable) = f32 P*[B][Co][Ho][Wo] =
+     * potential at that step (0 if never) — the record inhibition and WTA need
+     * (Listing 3 threshold -> inhibit -> convwta). */
+    SPK_EPI_FIRE = 1
+} spk_epilogue;
+
+/* Bytes of workspace spk_conv needs for this geometry and precision. */
+SPK_API size_t spk_conv_workspace(const spk_conv_geom* g, spk_precision prec);
+
+/* spk_conv — potentials of every time step of the cumulative input train
+ *   P[b][t][o][y][x] = sum_{c,i,j} W[o][c][i][j] * [lat_in[b][c][y*Sh-Ph+i][x*Sw-Pw+j] <= t]
+ * (Eq. 2; padded taps never fire), Ho = floor((Hi + 2Ph - Kh)/Sh) + 1.
+ *   lat_in [dev] u8 [B][Ci][Hi][Wi] (values 0..T; > T treated as never).
+ *   w      [dev] f32 [Co][Ci][Kh][Kw]; PRECONDITION 0 <= w <= w_max (weights are
+ *          non-negative in the paper's bounded STDP, L = 0 — required for the
+ *          latency map to be lossless, R-NONNEG).  EXACT_I8 clamps out-of-range
+ *          weights into [0, s] and raises the device flag in the workspace
+ *          (spk_conv_status reads it).
+ *   theta  IF threshold for SPK_EPI_FIRE, >= 0.
+ *   ws     workspace of spk_conv_workspace(g, prec) bytes (weight digit planes).
+ * Errors: SPK_ERR_ARG (null, theta < 0 or not finite, w_max <= 0),
+ * SPK_ERR_SHAPE (Eq. 2 violated, sizes < 1), SPK_ERR_UNSUPPORTED (T > 254, or
+ * EXACT_I8 with T > 32, Ci*Kh*Kw > 8192 or Kh,Kw > 16), SPK_ERR_WORKSPACE, SPK_ERR_CUDA. */
+SPK_API spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
+                    spk_precision prec, spk_epilogue epi, float theta, float w_max, void* out0,
+                    void* out1, void* ws, size_t ws_bytes, spk_stream stream);
+
+/* spk_fire — IF activation on materialised potentials (Listing 3
+ * `spyker.fire(data, th)`): lat[b][c][y][x] = first t with pot[b][t][c][y][x] >
+ * theta (T if none), pstar (nullable) = pot at that step (0 if never).
+ *   pot [dev] f32 [B][T][C][H][W] (BTCHW).  Errors: SPK_ERR_ARG, SPK_ERR_SHAPE. */
+SPK_API spk_status spk_fire(const float* pot, int B, int T, int C, int H, int W, float theta, uint8_t* lat,
+                    float* pstar, spk_stream stream);
+
+/* ========================================================================
+ * a5  Max pooling (Eq. 3)
+ * ======================================================================== */
+
+/* spk_pool — per-step window max of the cumulative trains == window MIN of
+ * latencies ("selects neurons that fire earlier"); zero padding never
+ * fires.  lat [dev] u8 [B][C][H][W] -> out [dev] u8 [B][C][Ho][Wo],
+ * Ho = floor((H + 2Ph - Lh)/Sh) + 1.  Errors: SPK_ERR_ARG, SPK_ERR_SHAPE. */
+SPK_API spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, int T, const spk_pool_geom* p,
+                    uint8_t* out, spk_stream stream);
+
+/* ========================================================================
+ * a6  Lateral inhibition
+ * ======================================================================== */
+
+/* spk_inhibit — in place on the (lat, P*) record of spk_conv(FIRE): for every
+ * (b, y, x) keep the channel with the least key (lat asc, P* desc, channel
+ * asc) among channels that fire (R-INHIBIT-TIE) and set every other channel to
+ * never (lat = T, P* = 0).  Locations where nothing fires are untouched.
+ *   lat [dev] u8 [B][C][H][W], pstar [dev] f32 [B][C][H][W].
+ * Errors: SPK_ERR_ARG, SPK_ERR_SHAPE. */
+SPK_API spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int H, int W, int T,
+                       spk_stream stream);
+
+/* ========================================================================
+ * a7  k-winners-take-all (convwta(array, radius, count))
+ * ======================================================================== */
+
+typedef struct {
+    int32_t b, t, c, y, x, cfg; /* sample, firing step t_i, map, row, col, STDP config */
+} spk_winner;
+
+/* spk_wta — per sample, up to k greedy picks of the least key (lat asc, P*
+ * desc, flat (c, y, x) asc) among live neurons (lat < T, not suppressed); after
+ * each pick its whole channel and the square |dy|,|dx| <= radius in every
+ * channel are suppressed (R-WTA-FOOTPRINT).  ("WTA selects neurons that fire
+ * earlier, and if the firing time of neurons is the same, then the one that
+ * has a higher internal potential will be selected".)
+ *   win  [dev] spk_winner [B][k] (slots >= nwin[b] are written with -1),
+ *   nwin [dev] i32 [B].  cfg of every winner = 0.
+ * Errors: SPK_ERR_ARG (k < 1, radius < 0), SPK_ERR_SHAPE. */
+SPK_API spk_status spk_wta(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T, int k,
+                   int radius, spk_winner* win, int32_t* nwin, spk_stream stream);
+
+/* ========================================================================
+ * a8  STDP / R-STDP (Eq. 4-7)
+ * ======================================================================== */
+
+typedef struct {
+    float a_plus, a_minus; /* A+_k (t_j <= t_i), A-_k (t_j > t_i) */
+    float lower, upper;    /* L_k < U_k */
+    int32_t stabilize;     /* 1: dW = A (W-L)(U-W) (Eq. 4); 0: dW = A (Eq. 5) */
+} spk_stdp_config;         /* spyker.STDPConfig(positive, negative, stabilize, lower, upper) */
+
+/* Bytes of workspace spk_stdp needs. */
+SPK_API size_t spk_stdp_workspace(const spk_conv_geom* g, int k);
+
+/* spk_stdp — in-place weight update of a conv layer from its winners
+ * (Listing 3 `conv.stdp(data, winners, spikes)`): for winners in (b asc, pick
+ * order) (R-BATCH) with config k = winner.cfg, for every synapse
+ * (c, i, j): t_j = lat_in[b][c][y*Sh-Ph+i][x*Sw-Pw+j] (never if padded),
+ * A = t_j <= t_i ? A+ : A- (R-EQ4-TIE), dW = A*((W-L)*(U-W)) or A,
+ * W = min(U, max(L, W + dW)) (R-EQ6-CLAMP) — fp32, this operation order, no
+ * contraction: bit-identical to the oracle.
+ *   w [dev] f32 [Co][Ci][Kh][Kw] updated in place (exclusive access);
+ *   g: geometry of the conv layer whose input is lat_in [dev] u8 [B][Ci][Hi][Wi];
+ *   win/nwin [dev] as spk_wta (winner.t = t_i, winner.(y,x) = output position);
+ *   cfgs [host] spk_stdp_config [ncfg], 1 <= ncfg <= 8.
+ * Winners with cfg outside [0, ncfg) or coordinates outside the output are skipped.
+ * Errors: SPK_ERR_ARG (L >= U, ncfg out of range), SPK_ERR_SHAPE, SPK_ERR_WORKSPACE. */
+SPK_API spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* lat_in, const spk_winner* win,
+                    const int32_t* nwin, int k, const spk_stdp_config* cfgs, int ncfg, void* ws,
+                    size_t ws_bytes, spk_stream stream);
+
+/* spk_rstdp_route — R-STDP configuration routing (Eq. 7: "passing
+ * two configurations ... and mapping each winner neuron to a configuration
+ * based on data labels"): winner.cfg = 0 (reward) if winner.c / maps_per_class
+ * == labels[winner.b], else 1 (punish) (R-CLASSMAP).  labels [dev] i32 [B].
+ * Errors: SPK_ERR_ARG. */
+SPK_API spk_status spk_rstdp_route(spk_winner* win, const int32_t* nwin, int B, int k,
+                           const int32_t* labels, int maps_per_class, spk_stream stream);
+
+/* ========================================================================
+ * a9  gather + boundary conversions
+ * ======================================================================== */
+
+/* spk_gather — "Firing times (divided by number of time steps)" (P:L269,
+ * Listing 5 `spyker.gather`): feat[i] = (T - min(lat[i], T)) / T (R-GATHER).
+ * lat [dev] u8 [n], feat [dev] f32 [n]. */
+SPK_API spk_status spk_gather(const uint8_t* lat, size_t n, int T, float* feat, spk_stream stream);
+
+/* spk_lat_to_dense — dense cumulative train dense[b][t][i] = (lat[b][i] <= t)
+ * (P:L117), BTCHW when N = C*H*W.  lat [dev] u8 [B][N], dense [dev] u8 [B][T][N]. */
+SPK_API spk_status spk_lat_to_dense(const uint8_t* lat, int B, int T, size_t N, uint8_t* dense,
+                            spk_stream stream);
+
+/* spk_dense_to_lat — first spike of a dense train; bad_index [dev] i32 (one
+ * value) receives the smallest flat index b*N + i whose train is not cumulative
+ * (a 1 followed by a 0) or holds a value other than 0/1, or -1. */
+SPK_API spk_status spk_dense_to_lat(const uint8_t* dense, int B, int T, size_t N, uint8_t* lat,
+                            int32_t* bad_index, spk_stream stream);
+
+/* Device-side status of the last EXACT_I8 spk_conv that used `ws`:
+ * *flag_out (host) = 1 if a weight was outside [0, s] and was clamped.
+ * Synchronises `stream`. */
+SPK_API spk_status spk_conv_status(const void* ws, int* flag_out, spk_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPK_H */

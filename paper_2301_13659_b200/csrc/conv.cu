@@ -1,0 +1,70 @@
+// conv.cu — spk_conv entry point: validation (Eq. 2) and dispatch to the
+// tcgen05 exact engine (conv_tc.cu) or the fp32 CUDA-core engine (conv_fp32.cu).
+#include <cmath>
+
+#include "conv.cuh"
+
+namespace {
+
+spk_status check_geom(const spk_conv_geom* g, int& Ho, int& Wo) {
+    SPK_CHECK_PTR(g);
+    SPK_CHECK(g->B >= 1 && g->T >= 1 && g->Ci >= 1 && g->Hi >= 1 && g->Wi >= 1 && g->Co >= 1 && g->Kh >= 1 &&
+                  g->Kw >= 1,
+              SPK_ERR_SHAPE, "non-positive size in conv geometry");
+    SPK_CHECK(g->Sh >= 1 && g->Sw >= 1 && g->Ph >= 0 && g->Pw >= 0, SPK_ERR_ARG, "bad stride/padding");
+    SPK_CHECK(g->Hi + 2 * g->Ph >= g->Kh && g->Wi + 2 * g->Pw >= g->Kw, SPK_ERR_SHAPE,
+              "kernel %dx%d larger than padded input %dx%d (Eq. 2)", g->Kh, g->Kw, g->Hi + 2 * g->Ph,
+              g->Wi + 2 * g->Pw);
+    SPK_CHECK(g->T <= 254, SPK_ERR_UNSUPPORTED, "T=%d > 254 (u8 latency)", g->T);
+    Ho = (g->Hi + 2 * g->Ph - g->Kh) / g->Sh + 1;
+    Wo = (g->Wi + 2 * g->Pw - g->Kw) / g->Sw + 1;
+    SPK_CHECK((double)g->B * g->Co * Ho * Wo * g->T < 9.0e18, SPK_ERR_SHAPE, "output too large");
+    return SPK_OK;
+}
+
+}  // namespace
+
+extern "C" size_t spk_conv_workspace(const spk_conv_geom* g, spk_precision prec) {
+    if (!g || prec != SPK_PREC_EXACT_I8) return 0;
+    TcPlan p;
+    if (!tc_plan(*g, p)) return 0;
+    return p.ws_bytes;
+}
+
+extern "C" spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
+                               spk_precision prec, spk_epilogue epi, float theta, float w_max, void* out0,
+                               void* out1, void* ws, size_t ws_bytes, spk_stream stream) {
+    spk::clear_error();
+    int Ho = 0, Wo = 0;
+    spk_status st = check_geom(g, Ho, Wo);
+    if (st != SPK_OK) return st;
+    SPK_CHECK_PTR(lat_in);
+    SPK_CHECK_PTR(w);
+    SPK_CHECK_PTR(out0);
+    SPK_CHECK(epi == SPK_EPI_POTENTIAL || epi == SPK_EPI_FIRE, SPK_ERR_ARG, "unknown epilogue %d", (int)epi);
+    SPK_CHECK(std::isfinite(theta) && theta >= 0.0f, SPK_ERR_ARG, "theta must be finite and >= 0");
+    cudaStream_t s = spk::as_cuda(stream);
+    if (prec == SPK_PREC_FP32) return spk_conv_fp32(lat_in, w, g, Ho, Wo, epi, theta, out0, out1, s);
+    SPK_CHECK(prec == SPK_PREC_EXACT_I8, SPK_ERR_ARG, "unknown precision %d", (int)prec);
+    SPK_CHECK(std::isfinite(w_max) && w_max > 0.0f, SPK_ERR_ARG, "w_max must be finite and > 0");
+    TcPlan p;
+    SPK_CHECK(tc_plan(*g, p), SPK_ERR_UNSUPPORTED,
+              "EXACT_I8 needs T <= 32, Ci*Kh*Kw <= %d, Kh,Kw <= 16, Ci*Hi*Wi < 2^24", kTcMaxK);
+    SPK_CHECK(ws != nullptr && ws_bytes >= p.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
+              p.ws_bytes);
+    return spk_conv_tc(lat_in, w, *g, p, epi, theta, w_max, out0, out1, ws, s);
+}
+
+extern "C" spk_status spk_conv_status(const void* ws, int* flag_out, spk_stream stream) {
+    spk::clear_error();
+    SPK_CHECK_PTR(ws);
+    SPK_CHECK_PTR(flag_out);
+    // The flag lives in the first 16 bytes of the workspace (see conv_tc.cu).
+    int v = 0;
+    cudaStream_t s = spk::as_cuda(stream);
+    if (cudaMemcpyAsync(&v, ws, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return spk::launched("spk_conv_status");
+    *flag_out = v;
+    return SPK_OK;
+}

@@ -1,0 +1,21 @@
+// conv.cuh — internal interface between the spk_conv dispatcher and its two engines.
+#pragma once
+#include "common.cuh"
+
+// Geometry of the tcgen05 exact path (see conv_tc.cu).
+struct TcPlan {
+    int Ho, Wo, K, KS, nks, TP, PPT, Nt, n_ntiles, NB;
+    long long NP, n_mtiles, total_tiles;
+    size_t packed_bytes, ws_bytes, smem_bytes;
+};
+
+constexpr int kTcKS = 64;       // K bytes (= synapses) per pipeline stage
+constexpr int kTcStages = 4;    // smem pipeline depth
+constexpr int kTcMaxK = 8192;   // synapses per neuron supported by the tcgen05 path
+
+bool tc_plan(const spk_conv_geom& g, TcPlan& p);
+spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const TcPlan& p,
+                       spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
+                       cudaStream_t s);
+spk_status spk_conv_fp32(const uint8_t* lat_in, const float* w, const spk_conv_geom* g, int Ho, int Wo,
+                         spk_epilogue epi, float theta, void* out0, void* out1, cudaStream_t s);

@@ -1,0 +1,145 @@
+// filter.cu — a1: DoG / Gabor (LoG = DoG pairs) feature-enhancement filter banks
+// (Eq. 1).  Kernel coefficients are built on the host in double from
+// the filter descriptions (tiny, per call) and passed by value; the filtering
+// runs on the GPU.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kMaxCoef = 2048;  // K * (2r+1)^2 floats passed by value (8 KB of params)
+
+struct FilterCoef {
+    float c[kMaxCoef];
+};
+
+// Unit-sum isotropic Gaussian on the integer grid [-r, r]^2 (R-DOG-NORM).
+void unit_gaussian(double sigma, int r, std::vector<double>& g) {
+    const int e = 2 * r + 1;
+    g.assign((size_t)e * e, 0.0);
+    double sum = 0.0;
+    for (int i = 0; i < e; ++i)
+        for (int j = 0; j < e; ++j) {
+            const double dy = i - r, dx = j - r;
+            const double v = std::exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma));
+            g[(size_t)i * e + j] = v;
+            sum += v;
+        }
+    for (double& v : g) v /= sum;
+}
+
+// Filter tile: 32 x 8 outputs of one (b, ci) plane, all K kernels per output pixel.
+constexpr int TX = 32, TY = 8;
+
+__global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restrict__ img, int C, int H,
+                                                       int W, int K, int r, int pad, int Ho, int Wo,
+                                                       float* __restrict__ out, const FilterCoef coef) {
+    extern __shared__ float tile[];  // (TY + 2r) x (TX + 2r)
+    const int e = 2 * r + 1;
+    const int tw = TX + 2 * r, th = TY + 2 * r;
+    const int bc = blockIdx.z;  // b * C + ci
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const uint8_t* plane = img + (size_t)bc * H * W;
+    // stage the input tile: pixel value u8 / 255 (R-SCALE), outside the image -> 0 (never used)
+    for (int q = threadIdx.y * TX + threadIdx.x; q < tw * th; q += TX * TY) {
+        const int ty = q / tw, tx = q % tw;
+        const int iy = y0 - pad + ty, ix = x0 - pad + tx;
+        float v = 0.0f;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = __fdiv_rn((float)plane[(size_t)iy * W + ix], 255.0f);
+        tile[q] = v;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+    if (x >= Wo || y >= Ho) return;
+    const int b = bc / C, ci = bc % C;
+    for (int k = 0; k < K; ++k) {
+        const float* kc = coef.c + k * e * e;
+        float acc = 0.0f;
+        for (int i = 0; i < e; ++i) {
+            const int iy = y - pad + i;
+            if (iy < 0 || iy >= H) continue;  // taps outside the image are skipped (R-FILTER-ORDER)
+            for (int j = 0; j < e; ++j) {
+                const int ix = x - pad + j;
+                if (ix < 0 || ix >= W) continue;
+                acc = __fmaf_rn(kc[i * e + j], tile[(threadIdx.y + i) * tw + threadIdx.x + j], acc);
+            }
+        }
+        out[(((size_t)b * C * K + (size_t)ci * K + k) * Ho + y) * Wo + x] = acc;
+    }
+}
+
+spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std::vector<float>& coef,
+                      int K, int radius, int pad, float* y, spk_stream stream) {
+    const int e = 2 * radius + 1;
+    const int Ho = H + 2 * pad - e + 1, Wo = W + 2 * pad - e + 1;
+    SPK_CHECK(Ho >= 1 && Wo >= 1, SPK_ERR_SHAPE, "filter output %dx%d (Eq. 1) is empty", Ho, Wo);
+    SPK_CHECK((size_t)B * C * K * Ho * Wo < (1ull << 40), SPK_ERR_SHAPE, "output too large");
+    FilterCoef fc;
+    for (size_t q = 0; q < coef.size(); ++q) fc.c[q] = coef[q];
+    dim3 grid(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY), (unsigned)(B * C));
+    SPK_CHECK(grid.z <= 65535u * 1024u, SPK_ERR_SHAPE, "B*C too large");
+    const size_t smem = sizeof(float) * (TX + 2 * radius) * (TY + 2 * radius);
+    filter_kernel<<<grid, dim3(TX, TY), smem, spk::as_cuda(stream)>>>(img, C, H, W, K, radius, pad, Ho,
+                                                                      Wo, y, fc);
+    return spk::launched("filter_kernel");
+}
+
+spk_status check_common(const uint8_t* img, int B, int C, int H, int W, const double* p, int K,
+                        int radius, int pad, float* y) {
+    SPK_CHECK_PTR(img);
+    SPK_CHECK_PTR(p);
+    SPK_CHECK_PTR(y);
+    SPK_CHECK(B >= 1 && C >= 1 && H >= 1 && W >= 1, SPK_ERR_SHAPE, "non-positive image size");
+    SPK_CHECK(K >= 1, SPK_ERR_ARG, "K=%d < 1", K);
+    SPK_CHECK(radius >= 0 && radius <= 7, SPK_ERR_UNSUPPORTED, "radius %d outside 0..7", radius);
+    SPK_CHECK(pad >= 0, SPK_ERR_ARG, "pad < 0");
+    SPK_CHECK(K * (2 * radius + 1) * (2 * radius + 1) <= kMaxCoef, SPK_ERR_UNSUPPORTED,
+              "K*(2r+1)^2 > %d coefficients", kMaxCoef);
+    return SPK_OK;
+}
+
+}  // namespace
+
+extern "C" spk_status spk_dog(const uint8_t* img, int B, int C, int H, int W, const double* sigmas,
+                              int K, int radius, int pad, float* y, spk_stream stream) {
+    spk::clear_error();
+    spk_status st = check_common(img, B, C, H, W, sigmas, K, radius, pad, y);
+    if (st != SPK_OK) return st;
+    const int e = 2 * radius + 1;
+    std::vector<float> coef((size_t)K * e * e);
+    std::vector<double> g1, g2;
+    for (int k = 0; k < K; ++k) {
+        const double s1 = sigmas[2 * k], s2 = sigmas[2 * k + 1];
+        SPK_CHECK(s1 > 0 && s2 > 0 && std::isfinite(s1) && std::isfinite(s2), SPK_ERR_ARG,
+                  "DoG sigmas must be positive");
+        unit_gaussian(s1, radius, g1);
+        unit_gaussian(s2, radius, g2);
+        for (int q = 0; q < e * e; ++q) coef[(size_t)k * e * e + q] = (float)(g1[q] - g2[q]);
+    }
+    return run_filter(img, B, C, H, W, coef, K, radius, pad, y, stream);
+}
+
+extern "C" spk_status spk_gabor(const uint8_t* img, int B, int C, int H, int W, const double* params,
+                                int K, int radius, int pad, float* y, spk_stream stream) {
+    spk::clear_error();
+    spk_status st = check_common(img, B, C, H, W, params, K, radius, pad, y);
+    if (st != SPK_OK) return st;
+    const int e = 2 * radius + 1;
+    std::vector<float> coef((size_t)K * e * e);
+    for (int k = 0; k < K; ++k) {
+        const double* p = params + 5 * k;
+        const double sigma = p[0], theta = p[1], gamma = p[2], lambda = p[3], psi = p[4];
+        SPK_CHECK(sigma > 0 && gamma > 0 && lambda > 0, SPK_ERR_ARG, "Gabor sigma/gamma/lambda must be > 0");
+        for (int i = 0; i < e; ++i)
+            for (int j = 0; j < e; ++j) {
+                const double yy = i - radius, xx = j - radius;
+                const double xr = xx * std::cos(theta) + yy * std::sin(theta);
+                const double yr = -xx * std::sin(theta) + yy * std::cos(theta);
+                const double env = std::exp(-(xr * xr + gamma * gamma * yr * yr) / (2.0 * sigma * sigma));
+                coef[(size_t)k * e * e + i * e + j] = (float)(env * std::cos(2.0 * M_PI * xr / lambda + psi));
+            }
+    }
+    return run_filter(img, B, C, H, W, coef, K, radius, pad, y, stream);
+}

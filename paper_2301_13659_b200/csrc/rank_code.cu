@@ -1,0 +1,233 @@
+// rank_code.cu — a2: threshold + rank-order coding into T cumulative bins
+// (Listing 1 `threshold(data, .01)`, `code(data, T)`).
+//
+// One CTA per sample.  The exact rank bins are found WITHOUT sorting: every
+// positive value gets the unique 64-bit key  (float bits << 32) | ~index , so
+// "larger key" == "earlier in (value desc, index asc)" (R-TIE).  A value of
+// rank r (number of larger keys) lands in bin floor(r*T/n) (R-BINS), i.e. its
+// bin is the number of bin boundaries t = 1..T-1 with r >= R_t = ceil(t*n/T).
+// The boundary keys K_t (the key with exactly R_t larger keys) are found by a
+// multi-target MSB radix select over the 8 key bytes (histograms in shared
+// memory), after which  lat = #{t : key <= K_t}.  Deterministic, exact, one
+// read of the sample per radix pass (values staged in shared memory when they
+// fit).
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kGroup = 16;                    // boundary targets resolved per sweep
+constexpr int kStageMax = 40 * 1024;          // values staged in smem up to this many
+
+struct RankSmem {
+    unsigned int hist[kGroup][256];
+    unsigned long long prefix[kGroup];
+    unsigned long long kt[256];               // resolved boundary keys K_t, t = 1..T-1
+    unsigned int rem[kGroup];
+    int slot[kGroup];
+    unsigned long long dpre[kGroup];
+    int ndist;
+    unsigned int red[32];
+    unsigned int n, umin, umax;
+};
+
+__device__ __forceinline__ unsigned int thr_bits(float v, float thresh) {
+    // threshold (strict, R-STRICT) then keep positives; 0 marks "never fires"
+    if (!(v > thresh)) v = 0.0f;
+    return v > 0.0f ? __float_as_uint(v) : 0u;
+}
+
+__device__ __forceinline__ unsigned int block_sum(unsigned int v, unsigned int* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = (l < (int)(blockDim.x >> 5)) ? red[l] : 0u;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    v = red[0];
+    __syncthreads();
+    return v;
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __restrict__ y, int N, int T,
+                                                            float thresh, int sort,
+                                                            uint8_t* __restrict__ lat) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ RankSmem sm;
+    unsigned int* vals = reinterpret_cast<unsigned int*>(dyn);
+    const float* ys = y + (size_t)blockIdx.x * N;
+    uint8_t* out = lat + (size_t)blockIdx.x * N;
+
+    auto U = [&](int i) -> unsigned int { return STAGED ? vals[i] : thr_bits(__ldg(ys + i), thresh); };
+
+    // pass 0: threshold, count positives, min/max (positive floats order like their bits)
+    unsigned int cnt = 0, mn = 0xffffffffu, mx = 0u;
+    for (int i = threadIdx.x; i < N; i += kThreads) {
+        const unsigned int u = thr_bits(__ldg(ys + i), thresh);
+        if (STAGED) vals[i] = u;
+        if (u) {
+            ++cnt;
+            mn = min(mn, u);
+            mx = max(mx, u);
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (threadIdx.x == 0) {
+        sm.umin = 0xffffffffu;
+        sm.umax = 0u;
+    }
+    const unsigned int n = block_sum(cnt, sm.red);  // contains __syncthreads
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&sm.umin, mn);
+        atomicMax(&sm.umax, mx);
+    }
+    __syncthreads();
+
+    if (n == 0) {
+        for (int i = threadIdx.x; i < N; i += kThreads) out[i] = (uint8_t)T;
+        return;
+    }
+
+    if (!sort) {
+        // R-SORTOFF: lat = min(T-1, floor(T*(vmax - v)/((vmax - vmin) + ulp(vmax)))), fp32 in this order
+        const float vmax = __uint_as_float(sm.umax), vmin = __uint_as_float(sm.umin);
+        const float ulp = __fsub_rn(__uint_as_float(sm.umax + 1u), vmax);
+        const float den = __fadd_rn(__fsub_rn(vmax, vmin), ulp);
+        for (int i = threadIdx.x; i < N; i += kThreads) {
+            const unsigned int u = U(i);
+            int l = T;
+            if (u) {
+                const float num = __fmul_rn((float)T, __fsub_rn(vmax, __uint_as_float(u)));
+                l = (int)floorf(__fdiv_rn(num, den));
+                if (l > T - 1) l = T - 1;
+            }
+            out[i] = (uint8_t)l;
+        }
+        return;
+    }
+
+    // boundary targets t = 1..T-1 with R_t = ceil(t n / T) < n
+    const int ntgt = T - 1;
+    for (int g0 = 0; g0 < ntgt; g0 += kGroup) {
+        const int gn = min(kGroup, ntgt - g0);
+        if (threadIdx.x < gn) {
+            const int t = g0 + threadIdx.x + 1;
+            const unsigned long long R = ((unsigned long long)t * n + T - 1) / T;
+            sm.rem[threadIdx.x] = (unsigned int)R;  // >= n means "no such key"
+            sm.prefix[threadIdx.x] = 0ull;
+        }
+        for (int p = 0; p < 8; ++p) {
+            const int shift = 56 - 8 * p;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                // distinct prefixes of the live targets (targets are in key-descending order)
+                int nd = 0;
+                for (int q = 0; q < gn; ++q) {
+                    if (sm.rem[q] >= n) { sm.slot[q] = -1; continue; }
+                    const unsigned long long pre = sm.prefix[q];
+                    if (nd == 0 || sm.dpre[nd - 1] != pre) sm.dpre[nd++] = pre;
+                    sm.slot[q] = nd - 1;
+                }
+                sm.ndist = nd;
+            }
+            __syncthreads();
+            const int nd = sm.ndist;
+            if (nd == 0) break;
+            for (int q = threadIdx.x; q < nd * 256; q += kThreads) (&sm.hist[0][0])[q] = 0u;
+            __syncthreads();
+            for (int i0 = 0; i0 < N; i0 += kThreads) {
+                const int i = i0 + threadIdx.x;
+                int s = -1;
+                unsigned int dig = 0;
+                if (i < N) {
+                    const unsigned int u = U(i);
+                    if (u) {
+                        const unsigned long long key = ((unsigned long long)u << 32) | (0xffffffffu - (unsigned)i);
+                        const unsigned long long pre = p ? (key >> (shift + 8)) : 0ull;
+                        for (int q = 0; q < nd; ++q)
+                            if (sm.dpre[q] == pre) { s = q; break; }
+                        dig = (unsigned int)(key >> shift) & 255u;
+                    }
+                }
+                // warp-aggregated shared-memory histogram update
+                const unsigned int code = (s < 0) ? 0xffffffffu : ((unsigned)s << 8 | dig);
+                const unsigned int peers = __match_any_sync(0xffffffffu, code);
+                if (s >= 0 && (__ffs(peers) - 1) == (int)(threadIdx.x & 31))
+                    atomicAdd(&sm.hist[s][dig], (unsigned)__popc(peers));
+            }
+            __syncthreads();
+            if (threadIdx.x < gn && sm.slot[threadIdx.x] >= 0) {
+                const unsigned int* h = sm.hist[sm.slot[threadIdx.x]];
+                unsigned int rem = sm.rem[threadIdx.x], cum = 0;
+                int d = 255;
+                for (; d > 0; --d) {
+                    if (cum + h[d] > rem) break;
+                    cum += h[d];
+                }
+                sm.rem[threadIdx.x] = rem - cum;
+                sm.prefix[threadIdx.x] = (sm.prefix[threadIdx.x] << 8) | (unsigned)d;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < gn) {
+            const int t = g0 + threadIdx.x + 1;
+            const unsigned long long R = ((unsigned long long)t * n + T - 1) / T;
+            sm.kt[t] = (R < n) ? sm.prefix[threadIdx.x] : 0ull;  // key 0 never matches a positive
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += kThreads) {
+        const unsigned int u = U(i);
+        int l = T;
+        if (u) {
+            const unsigned long long key = ((unsigned long long)u << 32) | (0xffffffffu - (unsigned)i);
+            l = 0;
+            for (int t = 1; t < T; ++t) {
+                if (key <= sm.kt[t]) l = t;
+                else break;  // K_t is non-increasing in t
+            }
+        }
+        out[i] = (uint8_t)l;
+    }
+}
+
+}  // namespace
+
+extern "C" size_t spk_rank_code_workspace(int, int, int, int) { return 0; }
+
+extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float thresh, int sort,
+                                    uint8_t* lat, void* ws, size_t ws_bytes, spk_stream stream) {
+    spk::clear_error();
+    (void)ws;
+    (void)ws_bytes;
+    SPK_CHECK_PTR(y);
+    SPK_CHECK_PTR(lat);
+    SPK_CHECK(B >= 1 && N >= 1, SPK_ERR_SHAPE, "B=%d N=%d", B, N);
+    SPK_CHECK(N <= (1 << 24), SPK_ERR_UNSUPPORTED, "N=%d > 2^24", N);
+    SPK_CHECK(T >= 1, SPK_ERR_ARG, "T=%d < 1", T);
+    SPK_CHECK(T <= 254, SPK_ERR_UNSUPPORTED, "T=%d > 254 (u8 latency)", T);
+    SPK_CHECK(B <= 0x7fffffff, SPK_ERR_SHAPE, "B too large");
+    cudaStream_t s = spk::as_cuda(stream);
+    if (N <= kStageMax) {
+        const size_t smem = sizeof(unsigned int) * (size_t)N;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(rank_code_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(unsigned int) * kStageMax));
+            attr = true;
+        }
+        rank_code_kernel<true><<<B, kThreads, smem, s>>>(y, N, T, thresh, sort, lat);
+        return spk::launched("rank_code_kernel<staged>");
+    }
+    rank_code_kernel<false><<<B, kThreads, 0, s>>>(y, N, T, thresh, sort, lat);
+    return spk::launched("rank_code_kernel<global>");
+}

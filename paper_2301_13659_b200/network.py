@@ -1,0 +1,161 @@
+"""The paper's network steps composed from libspk calls (configs/*.json).
+
+* front end   Listing 1: DoG/LoG/Gabor filter -> threshold -> rank code
+* inference   Listing 5: [conv -> fire -> pool] * L -> gather
+* train layer Listing 3: forward to the layer's input, conv ->
+              threshold/fire record (lat, P*) -> inhibit -> convwta -> stdp
+* R-STDP      P:L180-194: winners routed to reward/punish configs by label
+
+Buffers are allocated once per (config, batch) so a step can be captured in a
+CUDA graph; every stage is a libspk kernel.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import spk
+
+
+class Network:
+    def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "exact"):
+        self.cfg = cfg
+        self.B = batch
+        self.T = cfg["T"]
+        self.dev = torch.device(device)
+        self.prec = prec
+        im, fr = cfg["image"], cfg["front"]
+        self.img = torch.zeros((batch, im["C"], im["H"], im["W"]), dtype=torch.uint8, device=self.dev)
+        self.labels = torch.zeros((batch,), dtype=torch.int32, device=self.dev)
+        if fr["kind"] == "dog":
+            self.filters = ("dog", [tuple(p) for p in fr["pairs"]])
+        elif fr["kind"] == "log":
+            self.filters = ("dog", spk.log_pairs(fr["stds"]))
+        else:
+            self.filters = ("gabor", [tuple(p) for p in fr["params"]])
+        K = len(self.filters[1])
+        e = 2 * fr["radius"] + 1
+        H, W = im["H"] + 2 * fr["pad"] - e + 1, im["W"] + 2 * fr["pad"] - e + 1
+        self.y = torch.empty((batch, im["C"] * K, H, W), dtype=torch.float32, device=self.dev)
+        self.lat0 = torch.empty((batch, im["C"] * K, H, W), dtype=torch.uint8, device=self.dev)
+        self.weights: list[torch.Tensor] = []
+        self.layers = []
+        ci, h, w = im["C"] * K, H, W
+        for L in cfg["layers"]:
+            Ho = (h + 2 * L["pad"] - L["K"]) // L["stride"] + 1
+            Wo = (w + 2 * L["pad"] - L["K"]) // L["stride"] + 1
+            geom = spk.ConvGeom(batch, self.T, ci, h, w, L["Co"], L["K"], L["K"], L["stride"], L["stride"],
+                                L["pad"], L["pad"])
+            rec = dict(
+                L=L, geom=geom, Ho=Ho, Wo=Wo,
+                lat=torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.uint8, device=self.dev),
+                pstar=torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.float32, device=self.dev),
+                ws=torch.empty(max(1, spk.conv_workspace(geom, prec)), dtype=torch.uint8, device=self.dev),
+            )
+            if L["pool"]:
+                p = L["pool"]
+                Hp = (Ho + 2 * p["pad"] - p["kernel"]) // p["stride"] + 1
+                Wp = (Wo + 2 * p["pad"] - p["kernel"]) // p["stride"] + 1
+                rec["pooled"] = torch.empty((batch, L["Co"], Hp, Wp), dtype=torch.uint8, device=self.dev)
+                h, w = Hp, Wp
+            else:
+                rec["pooled"] = None
+                h, w = Ho, Wo
+            ci = L["Co"]
+            self.layers.append(rec)
+            self.weights.append(torch.zeros((L["Co"], geom.Ci, L["K"], L["K"]), dtype=torch.float32,
+                                            device=self.dev))
+        tl = cfg.get("train_layer")
+        if tl is not None:
+            rec = self.layers[tl]
+            wk = rec["L"]["wta"]
+            self.k = wk["count"]
+            self.win = torch.empty((batch, self.k, 6), dtype=torch.int32, device=self.dev)
+            self.nwin = torch.empty((batch,), dtype=torch.int32, device=self.dev)
+            self.stdp_ws = torch.empty(spk.stdp_workspace(rec["geom"], self.k), dtype=torch.uint8, device=self.dev)
+            self.stdp_cfg = spk.stdp_configs(cfg["stdp"])
+        last = self.layers[-1]
+        src = last["pooled"] if last["pooled"] is not None else last["lat"]
+        self.features = torch.empty(src.shape, dtype=torch.float32, device=self.dev)
+        self.graph = None
+
+    # ------------------------------------------------------------ data in
+    def set_weights(self, ws):
+        for dst, src in zip(self.weights, ws):
+            dst.copy_(torch.as_tensor(src))
+
+    def input_of(self, li: int) -> torch.Tensor:
+        if li == 0:
+            return self.lat0
+        prev = self.layers[li - 1]
+        return prev["pooled"] if prev["pooled"] is not None else prev["lat"]
+
+    # ------------------------------------------------------------ stages
+    def front(self):
+        fr = self.cfg["front"]
+        kind, filt = self.filters
+        if kind == "dog":
+            spk.dog(self.img, filt, fr["radius"], fr["pad"], out=self.y)
+        else:
+            spk.gabor(self.img, filt, fr["radius"], fr["pad"], out=self.y)
+        spk.rank_code(self.y, self.T, fr["thresh"], fr["sort"], out=self.lat0)
+
+    def layer(self, li: int, pstar: bool = False):
+        rec = self.layers[li]
+        L = rec["L"]
+        spk.conv(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=self.prec, epi="fire",
+                 theta=L["theta"], w_max=1.0, out0=rec["lat"], out1=rec["pstar"] if pstar else None, ws=rec["ws"],
+                 want_pstar=pstar)
+        if rec["pooled"] is not None and not pstar:
+            p = L["pool"]
+            spk.pool(rec["lat"], self.T, p["kernel"], p["stride"], p["pad"], out=rec["pooled"])
+
+    def train_step(self):
+        """Listing 3 train_layer{l} for l = cfg['train_layer'] (R-STDP if cfg['learning'] == 'rstdp')."""
+        tl = self.cfg["train_layer"]
+        self.front()
+        for li in range(tl):
+            self.layer(li)
+        self.layer(tl, pstar=True)
+        rec = self.layers[tl]
+        L = rec["L"]
+        spk.inhibit(rec["lat"], rec["pstar"], self.T)
+        spk.wta(rec["lat"], rec["pstar"], self.T, self.k, L["wta"]["radius"], win=self.win, nwin=self.nwin)
+        if self.cfg["learning"] == "rstdp":
+            spk.rstdp_route(self.win, self.nwin, self.labels, self.cfg["maps_per_class"])
+        spk.stdp(self.weights[tl], self.input_of(tl), self.win, self.nwin, None, self.T, L["stride"], L["pad"],
+                 ws=self.stdp_ws, cfg_arr=self.stdp_cfg)
+
+    def infer(self):
+        """Listing 5: every layer conv -> fire -> pool, then gather."""
+        self.front()
+        for li in range(len(self.layers)):
+            self.layer(li)
+        last = self.layers[-1]
+        src = last["pooled"] if last["pooled"] is not None else last["lat"]
+        spk.gather(src, self.T, out=self.features)
+
+    def step(self):
+        if self.cfg["timed"] == "train":
+            self.train_step()
+        else:
+            self.infer()
+
+    # ------------------------------------------------------------ CUDA graph
+    def capture(self, warmup: int = 1):
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.step()
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        self.graph = g
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            self.step()
+        else:
+            self.graph.replay()

@@ -1,0 +1,366 @@
+"""GPU parity: every libspk stage against the CPU oracle on the same seeded inputs.
+
+Stage-wise tests are teacher-forced (the GPU stage gets the oracle's input to
+that stage); pipeline tests run end to end.  Comparison rules: tests/parity.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import pipeline as opipe
+from parity import (assert_potentials, compare_latency, lat_and_pstar, near_threshold)
+
+pytestmark = pytest.mark.gpu
+RNG = np.random.default_rng(2024)
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------------- a1 filters
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_filter_bit_identical(spk, name):
+    cfg = synth.load_config(name)
+    imgs = synth.images(cfg, 0, 3)
+    fr = cfg["front"]
+    ref = oracle.filter_apply(imgs, opipe.filter_bank(cfg), fr["pad"])
+    if fr["kind"] == "dog":
+        got = spk.dog(cu(imgs), fr["pairs"], fr["radius"], fr["pad"])
+    elif fr["kind"] == "log":
+        got = spk.dog(cu(imgs), spk.log_pairs(fr["stds"]), fr["radius"], fr["pad"])
+    else:
+        got = spk.gabor(cu(imgs), fr["params"], fr["radius"], fr["pad"])
+    np.testing.assert_array_equal(host(got), ref)
+
+
+def test_filter_odd_geometry(spk):
+    imgs = RNG.integers(0, 256, (2, 3, 37, 45), dtype=np.uint8)
+    for r, pad in [(2, 0), (3, 1), (1, 4), (0, 0)]:
+        pairs = [(0.8, 1.7), (2.2, 1.1)]
+        ref = oracle.filter_apply(imgs, oracle.dog_bank(pairs, r), pad)
+        np.testing.assert_array_equal(host(spk.dog(cu(imgs), pairs, r, pad)), ref)
+        gab = [(2.0, 0.3, 0.6, 4.0, 0.5)]
+        ref = oracle.filter_apply(imgs, oracle.gabor_bank(gab, r), pad)
+        np.testing.assert_array_equal(host(spk.gabor(cu(imgs), gab, r, pad)), ref)
+
+
+# ---------------------------------------------------------------------- a2 rank coding
+@pytest.mark.parametrize("T", [1, 4, 15, 30, 100, 254])
+@pytest.mark.parametrize("sort", [True, False])
+def test_rank_code_exact(spk, T, sort):
+    cfg = synth.load_config("c2")
+    imgs = synth.images(cfg, 0, 6)
+    y = oracle.filter_apply(imgs, opipe.filter_bank(cfg), 3)
+    y[1] = np.round(y[1] * 8) / 8          # many ties
+    y[2] = 0.0                             # nothing fires
+    y[3] = -1.0
+    y[3, 0, 5, 5] = 0.5                    # a single positive
+    y[4, :, :14] = y[4, :, 14:]            # exact duplicate halves
+    ref = oracle.rank_code(y, T, 0.01, sort)
+    got = host(spk.rank_code(cu(y), T, 0.01, sort))
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_rank_code_large_sample_global_path(spk):
+    y = RNG.normal(0, 1, (3, 50_000)).astype(np.float32)  # > staged limit -> global-memory path
+    y[0, ::7] = np.round(y[0, ::7], 1)
+    for T, sort in [(15, True), (30, True), (15, False)]:
+        np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, sort)), oracle.rank_code(y, T, 0.01, sort))
+
+
+# ------------------------------------------------------------------------- a3 conv
+CONV_CASES = [
+    # B, T, Ci, Hi, Wi, Co, K, stride, pad
+    (2, 15, 6, 28, 28, 30, 5, 1, 2),      # C2 conv1
+    (2, 15, 30, 14, 14, 250, 3, 1, 1),    # C2 conv2 (2 N tiles)
+    (3, 15, 250, 4, 4, 200, 5, 1, 2),     # C2 conv3 (K = 6250, 98 stages)
+    (1, 30, 4, 20, 23, 64, 5, 1, 2),      # C4 conv1 shape class, T = 30
+    (2, 30, 64, 9, 11, 128, 3, 1, 1),     # C4 conv2 shape class
+    (3, 7, 3, 9, 11, 20, 3, 2, 0),        # strided, ragged tiles
+    (1, 16, 5, 6, 5, 17, 4, 3, 1),        # T = TP, odd Co
+    (2, 1, 2, 5, 7, 8, 2, 1, 0),          # T = 1
+]
+
+
+def _conv_inputs(B, T, Ci, Hi, Wi, Co, K, dens=0.5):
+    lat = RNG.integers(0, T, (B, Ci, Hi, Wi)).astype(np.uint8)
+    lat[RNG.random(lat.shape) > dens] = T  # never fires
+    w = RNG.uniform(0.0, 1.0, (Co, Ci, K, K)).astype(np.float32)
+    return lat, w
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("prec", ["exact", "fp32"])
+def test_conv_potentials(spk, case, prec):
+    B, T, Ci, Hi, Wi, Co, K, s, p = case
+    lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K)
+    ref = oracle.conv_event(lat, T, w, (s, s), (p, p))
+    got = host(spk.conv(cu(lat), cu(w), T, s, p, prec=prec, epi="potential"))
+    assert_potentials(got, ref)
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("prec", ["exact", "fp32"])
+def test_conv_fire_epilogue(spk, case, prec):
+    B, T, Ci, Hi, Wi, Co, K, s, p = case
+    lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K)
+    P = oracle.conv_event(lat, T, w, (s, s), (p, p))
+    theta = float(np.percentile(P[:, -1], 60)) + 0.123  # fire for roughly 40 % of neurons
+    ref_lat, ref_ps = lat_and_pstar(P, theta)
+    glat, gps = spk.conv(cu(lat), cu(w), T, s, p, prec=prec, epi="fire", theta=theta)
+    glat, gps = host(glat), host(gps)
+    excl = near_threshold(P, theta)
+    compare_latency(glat, ref_lat, excl)
+    ok = (glat == ref_lat) & (ref_lat < T)
+    assert_potentials(gps[ok], ref_ps[ok])
+    assert (gps[glat == T] == 0).all()
+
+
+def test_conv_quantised_weights_exact_integers(spk):
+    # binary weights (Listing 4 quantize) make potentials exact integers on every path
+    lat, _ = _conv_inputs(2, 15, 30, 14, 14, 250, 3)
+    w = RNG.integers(0, 2, (250, 30, 3, 3)).astype(np.float32)
+    ref = oracle.conv_event(lat, 15, w, (1, 1), (1, 1))
+    for prec in ("exact", "fp32"):
+        np.testing.assert_array_equal(host(spk.conv(cu(lat), cu(w), 15, 1, 1, prec=prec, epi="potential")), ref)
+
+
+def test_conv_weight_scale_and_clamp_flag(spk):
+    lat, w = _conv_inputs(1, 15, 4, 8, 8, 16, 3)
+    w2 = w * 3.0  # w_max = 3 -> scale 4
+    ref = oracle.conv_event(lat, 15, w2, (1, 1), (1, 1))
+    g = spk.conv_geom(cu(lat), cu(w2), 15, 1, 1)
+    ws = torch.empty(spk.conv_workspace(g), dtype=torch.uint8, device="cuda")
+    got = spk.conv(cu(lat), cu(w2), 15, 1, 1, epi="potential", w_max=3.0, ws=ws)
+    assert_potentials(host(got), ref)
+    assert spk.conv_clamp_flag(ws) == 0
+    spk.conv(cu(lat), cu(w2), 15, 1, 1, epi="potential", w_max=1.0, ws=ws)  # weights above the scale
+    assert spk.conv_clamp_flag(ws) == 1
+
+
+def test_conv_matches_dense_definition(spk):
+    # the direct BTCHW definition of Eq. 2 (not only the event form)
+    lat, w = _conv_inputs(2, 6, 3, 7, 9, 12, 3)
+    ref = oracle.conv(oracle.lat_to_dense(lat, 6), w, (1, 1), (1, 1))
+    assert_potentials(host(spk.conv(cu(lat), cu(w), 6, 1, 1, epi="potential")), ref)
+
+
+# ------------------------------------------------------------------------- a4 fire
+def test_fire_exact(spk):
+    P = np.cumsum(RNG.uniform(0, 2, (3, 15, 5, 7, 9)), axis=1).astype(np.float32)
+    theta = 9.5
+    lat, ps = spk.fire(cu(P), theta)
+    S = oracle.fire(P.astype(np.float64), theta)
+    np.testing.assert_array_equal(host(lat), oracle.dense_to_lat(S))
+    rl, rp = lat_and_pstar(P.astype(np.float64), theta)
+    np.testing.assert_array_equal(host(ps), rp.astype(np.float32))
+
+
+# ------------------------------------------------------------------------- a5 pool
+@pytest.mark.parametrize("L,s,p", [(2, 2, 0), (3, 3, 0), (3, 2, 1), (2, 1, 1), (4, 4, 2)])
+def test_pool_exact(spk, L, s, p):
+    T = 15
+    lat = RNG.integers(0, T + 1, (2, 5, 14, 13)).astype(np.uint8)
+    ref = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(lat, T), (L, L), (s, s), (p, p)))
+    np.testing.assert_array_equal(host(spk.pool(cu(lat), T, L, s, p)), ref)
+
+
+# ----------------------------------------------------------------- a6 inhibit, a7 wta
+def _records(B, T, C, H, W, dens=0.4, ties=False):
+    P = np.cumsum(RNG.uniform(0, 1, (B, T, C, H, W)) * (RNG.random((B, 1, C, H, W)) < dens), axis=1)
+    if ties:
+        P = np.round(P * 4) / 4
+    P = P.astype(np.float32).astype(np.float64)  # values representable in fp32: no rounding ambiguity
+    Q = oracle.threshold(P, 1.2)
+    lat, ps = lat_and_pstar(P, 1.2)
+    return Q, lat, ps
+
+
+@pytest.mark.parametrize("ties", [False, True])
+def test_inhibit_exact(spk, ties):
+    T = 10
+    Q, lat, ps = _records(3, T, 6, 7, 8, 0.6, ties)
+    ref = oracle.inhibit(Q)
+    rlat, rps = lat_and_pstar(ref, 0.0)
+    glat, gps = spk.inhibit(cu(lat), cu(ps.astype(np.float32)), T)
+    np.testing.assert_array_equal(host(glat), rlat)
+    np.testing.assert_array_equal(host(gps), rps.astype(np.float32))
+
+
+@pytest.mark.parametrize("k,r", [(5, 3), (8, 1), (1, 0), (3, 10), (20, 0)])
+@pytest.mark.parametrize("ties", [False, True])
+def test_wta_exact(spk, k, r, ties):
+    T = 12
+    Q, lat, ps = _records(4, T, 7, 9, 8, 0.5, ties)
+    win, nwin = oracle.wta(Q, k, r)
+    gw, gn = spk.wta(cu(lat), cu(ps.astype(np.float32)), T, k, r)
+    gw, gn = host(gw), host(gn)
+    np.testing.assert_array_equal(gn, nwin)
+    for b in range(4):
+        np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
+        assert (gw[b, nwin[b]:] == -1).all()
+
+
+# ------------------------------------------------------------------------- a8 stdp
+@pytest.mark.parametrize("stab", [1, 0])
+def test_stdp_bit_exact(spk, stab):
+    T, B, k = 15, 6, 4
+    lat_in = RNG.integers(0, T + 1, (B, 5, 9, 8)).astype(np.uint8)
+    W0 = RNG.uniform(0.0, 1.0, (7, 5, 3, 3)).astype(np.float32)
+    W0[0, 0, 0, :] = [0.0, 1.0, 0.5]
+    win = np.full((B, k, 6), -1, np.int32)
+    nwin = RNG.integers(0, k + 1, B).astype(np.int32)
+    for b in range(B):
+        for q in range(nwin[b]):
+            win[b, q] = [b, RNG.integers(0, T), RNG.integers(0, 7), RNG.integers(0, 9), RNG.integers(0, 8),
+                         RNG.integers(0, 2)]
+    cfgs = [(0.004, -0.003, 0.0, 1.0, stab), (-0.004, 0.003, 0.0, 1.0, stab)]
+    ref = oracle.stdp(W0, oracle.lat_to_dense(lat_in, T), win, nwin, cfgs, (1, 1), (1, 1))
+    w = cu(W0)
+    spk.stdp(w, cu(lat_in), cu(win), cu(nwin), cfgs, T, 1, 1)
+    np.testing.assert_array_equal(host(w), ref)
+
+
+def test_rstdp_route_exact(spk):
+    B, k = 9, 3
+    win = np.full((B, k, 6), -1, np.int32)
+    nwin = RNG.integers(0, k + 1, B).astype(np.int32)
+    for b in range(B):
+        for q in range(nwin[b]):
+            win[b, q] = [b, 3, RNG.integers(0, 200), 1, 1, 0]
+    labels = RNG.integers(0, 10, B).astype(np.int32)
+    ref = oracle.rstdp_route(win, nwin, labels, 20)
+    gw = cu(win)
+    spk.rstdp_route(gw, cu(nwin), cu(labels), 20)
+    np.testing.assert_array_equal(host(gw), ref)
+
+
+# ---------------------------------------------------------------- a9 gather, boundary
+def test_gather_and_conversions(spk):
+    T = 15
+    lat = RNG.integers(0, T + 1, (3, 4, 5, 6)).astype(np.uint8)
+    S = oracle.lat_to_dense(lat, T)
+    np.testing.assert_array_equal(host(spk.gather(cu(lat), T)), oracle.gather(S))
+    np.testing.assert_array_equal(host(spk.lat_to_dense(cu(lat), T)), S)
+    glat, bad = spk.dense_to_lat(cu(S))
+    np.testing.assert_array_equal(host(glat), lat)
+    assert int(host(bad)[0]) == -1
+    S2 = S.copy()
+    S2[1, 7, 2, 3, 4] = 0  # break the cumulative train of neuron (1, 2, 3, 4)
+    S2[1, 8, 2, 3, 4] = 1
+    if S2[1, 6, 2, 3, 4] == 0:
+        S2[1, 6, 2, 3, 4] = 1
+    _, bad = spk.dense_to_lat(cu(S2))
+    assert int(host(bad)[0]) == 1 * 120 + 2 * 30 + 3 * 6 + 4
+
+
+# ------------------------------------------------------------------ pipelines end to end
+def _gpu_train(cfg, imgs, Ws, labels=None, prec="exact"):
+    from paper_2301_13659_b200.network import Network
+
+    net = Network(cfg, imgs.shape[0], prec=prec)
+    net.img.copy_(cu(imgs))
+    if labels is not None:
+        net.labels.copy_(cu(labels))
+    net.set_weights([cu(w) for w in Ws])
+    net.train_step()
+    torch.cuda.synchronize()
+    return net
+
+
+def _check_pipeline(cfg, n, labels=False, prec="exact"):
+    imgs = synth.images(cfg, 0, n)
+    lab = synth.labels(cfg, 0, n) if labels else None
+    Ws = synth.layer_weights(cfg)
+    ref = opipe.train_step(cfg, imgs, Ws, lab, event=True)
+    net = _gpu_train(cfg, imgs, Ws, lab, prec)
+    T = cfg["T"]
+    np.testing.assert_array_equal(host(net.lat0), ref["lat0"])
+    tl = cfg["train_layer"]
+    # layer inputs (teacher-free: whole chain on the GPU)
+    excluded_samples = np.zeros(n, bool)
+    for li in range(tl):
+        L = cfg["layers"][li]
+        P = oracle.conv_event(oracle.dense_to_lat(ref["inputs"][li]), T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
+        excl = near_threshold(P, L["theta"])
+        rec = net.layers[li]
+        glat = host(rec["lat"])
+        rlat, _ = lat_and_pstar(P, L["theta"])
+        diff = (glat != rlat) & ~excluded_samples[:, None, None, None]
+        assert not (diff & ~excl).any(), f"layer {li}: unexplained latency mismatches"
+        excluded_samples |= diff.any(axis=(1, 2, 3))
+    # trained layer: (lat, P*) after inhibition, winners, weights
+    L = cfg["layers"][tl]
+    excl = near_threshold(ref["P"], L["theta"])
+    rlat, rps = lat_and_pstar(ref["Qi"], 0.0)
+    glat = host(net.layers[tl]["lat"])
+    diff = (glat != rlat) & ~excluded_samples[:, None, None, None]
+    assert not (diff & ~excl).any(), "trained layer: unexplained mismatches after inhibition"
+    excluded_samples |= diff.any(axis=(1, 2, 3))
+    gw, gn = host(net.win), host(net.nwin)
+    for b in range(n):
+        if excluded_samples[b]:
+            continue
+        assert gn[b] == ref["nwin"][b]
+        np.testing.assert_array_equal(gw[b, :gn[b]], ref["win"][b, :gn[b]])
+    if not excluded_samples.any():
+        np.testing.assert_array_equal(host(net.weights[tl]), ref["W_new"])
+    else:
+        # teacher-forced STDP with the GPU's own winners: still bit-exact
+        S_in = oracle.lat_to_dense(host(net.input_of(tl)), T)
+        W = oracle.stdp(Ws[tl], S_in, gw, gn, [tuple(c) for c in cfg["stdp"]], (L["stride"],) * 2, (L["pad"],) * 2)
+        np.testing.assert_array_equal(host(net.weights[tl]), W)
+    return int(excluded_samples.sum())
+
+
+def test_pipeline_c1(spk):
+    assert _check_pipeline(synth.load_config("c1"), 1) == 0
+
+
+@pytest.mark.parametrize("prec", ["exact", "fp32"])
+def test_pipeline_c2_small_batch(spk, prec):
+    assert _check_pipeline(synth.load_config("c2"), 12, prec=prec) <= 1
+
+
+def test_pipeline_c3_rstdp(spk):
+    assert _check_pipeline(synth.load_config("c3"), 12, labels=True) <= 1
+
+
+def test_c2_full_batch_sampled(spk):
+    """BASELINE configs[1] at full size (batch 1024), launched exactly as bench.py does
+    (CUDA graph replay): sampled images checked against the oracle one by one, the
+    STDP update checked bit-exactly with the GPU's winners teacher-forced."""
+    from paper_2301_13659_b200.network import Network
+
+    cfg = synth.load_config("c2")
+    B, T = cfg["batch"], cfg["T"]
+    imgs = synth.images(cfg, 0, B)
+    Ws = synth.layer_weights(cfg)
+    net = Network(cfg, B)
+    net.img.copy_(cu(imgs))
+    net.set_weights([cu(w) for w in Ws])
+    net.capture(warmup=1)
+    net.set_weights([cu(w) for w in Ws])  # the capture warm-up ran one training step
+    net.replay()
+    torch.cuda.synchronize()
+    gw, gn = host(net.win), host(net.nwin)
+    lat0 = host(net.lat0)
+    for b in [0, 511, 1023]:
+        ref = opipe.train_step(cfg, imgs[b:b + 1], Ws, None, event=True)
+        np.testing.assert_array_equal(lat0[b:b + 1], ref["lat0"])
+        assert gn[b] == ref["nwin"][0]
+        got = gw[b, :gn[b]].copy()
+        got[:, 0] = 0
+        np.testing.assert_array_equal(got, ref["win"][0, :gn[b]])
+    L = cfg["layers"][2]
+    S_in = oracle.lat_to_dense(host(net.input_of(2)), T)
+    W = oracle.stdp(Ws[2], S_in, gw, gn, [tuple(c) for c in cfg["stdp"]], (1, 1), (2, 2))
+    np.testing.assert_array_equal(host(net.weights[2]), W)
