@@ -16,6 +16,10 @@ import torch
 from . import spk
 
 
+def _nomark(name: str) -> None:
+    pass
+
+
 class Network:
     def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "exact"):
         self.cfg = cfg
@@ -90,55 +94,69 @@ class Network:
         return prev["pooled"] if prev["pooled"] is not None else prev["lat"]
 
     # ------------------------------------------------------------ stages
-    def front(self):
+    def front(self, mark=_nomark):
         fr = self.cfg["front"]
         kind, filt = self.filters
         if kind == "dog":
             spk.dog(self.img, filt, fr["radius"], fr["pad"], out=self.y)
         else:
             spk.gabor(self.img, filt, fr["radius"], fr["pad"], out=self.y)
+        mark("filter")
         spk.rank_code(self.y, self.T, fr["thresh"], fr["sort"], out=self.lat0)
+        mark("rank_code")
 
-    def layer(self, li: int, pstar: bool = False):
+    def layer(self, li: int, pstar: bool = False, mark=_nomark):
         rec = self.layers[li]
         L = rec["L"]
         spk.conv(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=self.prec, epi="fire",
                  theta=L["theta"], w_max=1.0, out0=rec["lat"], out1=rec["pstar"] if pstar else None, ws=rec["ws"],
                  want_pstar=pstar)
+        mark(f"conv{li}")
         if rec["pooled"] is not None and not pstar:
             p = L["pool"]
             spk.pool(rec["lat"], self.T, p["kernel"], p["stride"], p["pad"], out=rec["pooled"])
+            mark(f"pool{li}")
 
-    def train_step(self):
+    def train_step(self, mark=_nomark):
         """Listing 3 train_layer{l} for l = cfg['train_layer'] (R-STDP if cfg['learning'] == 'rstdp')."""
         tl = self.cfg["train_layer"]
-        self.front()
+        mark("start")
+        self.front(mark)
         for li in range(tl):
-            self.layer(li)
-        self.layer(tl, pstar=True)
+            self.layer(li, mark=mark)
+        self.layer(tl, pstar=True, mark=mark)
         rec = self.layers[tl]
         L = rec["L"]
         spk.inhibit(rec["lat"], rec["pstar"], self.T)
+        mark("inhibit")
         spk.wta(rec["lat"], rec["pstar"], self.T, self.k, L["wta"]["radius"], win=self.win, nwin=self.nwin)
+        mark("wta")
         if self.cfg["learning"] == "rstdp":
             spk.rstdp_route(self.win, self.nwin, self.labels, self.cfg["maps_per_class"])
+            mark("rstdp_route")
         spk.stdp(self.weights[tl], self.input_of(tl), self.win, self.nwin, None, self.T, L["stride"], L["pad"],
                  ws=self.stdp_ws, cfg_arr=self.stdp_cfg)
+        mark("stdp")
 
-    def infer(self):
+    def infer(self, mark=_nomark):
         """Listing 5: every layer conv -> fire -> pool, then gather."""
-        self.front()
+        mark("start")
+        self.front(mark)
         for li in range(len(self.layers)):
-            self.layer(li)
+            self.layer(li, mark=mark)
         last = self.layers[-1]
         src = last["pooled"] if last["pooled"] is not None else last["lat"]
         spk.gather(src, self.T, out=self.features)
+        mark("gather")
 
     def step(self):
+        self.step_marked(_nomark)
+
+    def step_marked(self, mark):
         if self.cfg["timed"] == "train":
-            self.train_step()
+            self.train_step(mark)
         else:
-            self.infer()
+            self.infer(mark)
 
     # ------------------------------------------------------------ CUDA graph
     def capture(self, warmup: int = 1):
