@@ -5,14 +5,14 @@
 // Geometry of the tcgen05 exact path (see conv_tc.cu).
 struct TcPlan {
     int Ho, Wo, K, KS, nks, TP, PPT, Nt, n_ntiles, NB;
-    int tps, NR, band, nrb;  // M tiles per sample, staged input rows per tile, bytes per channel band, band buffers
+    int tps, NR, band, nrb, bres, stack, NS, WiP, HiP;  // M tiles per sample, staged input rows per tile, bytes per channel band, band buffers, resident B
     size_t rb_stride;
     long long NP, n_mtiles, total_tiles;
     size_t packed_bytes, ws_bytes, smem_bytes;
 };
 
-constexpr int kTcKS = 64;       // K bytes (= synapses) per pipeline stage
-constexpr int kTcStages = 4;    // smem pipeline depth
+constexpr int kTcKS = 128;      // K bytes (= synapses) per pipeline stage
+constexpr int kTcStages = 4;    // pipeline depth (A stages in TMEM, B stages in smem)
 constexpr int kTcMaxK = 8192;   // synapses per neuron supported by the tcgen05 path
 
 bool tc_plan(const spk_conv_geom& g, TcPlan& p);

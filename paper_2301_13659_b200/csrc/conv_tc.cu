@@ -8,28 +8,36 @@
 //                           are TP consecutive TMEM lanes of one warp.  An
 //                           M tile (128 rows = 128/TP pixels) never crosses a
 //                           sample.
-//   cols  N = output map o (tile Nt <= 160)
+//   cols  N = output map o (tile Nt <= 128); the 3 digit planes are stacked
+//                           along N (one MMA of N = 3 Nt) when 3 Nt <= 256
 //   depth K = synapse (c, i, j), in the kernel's [Co][Ci][Kh][Kw] order.
 //   A[(p,t), k] = [lat_in(p, k) <= t]   — the cumulative spike train, built on
-//                 the fly in shared memory from the u8 latency map (never
-//                 materialised in HBM), u8 {0,1};
+//                 the fly from the u8 latency map (never materialised in HBM)
+//                 and written straight into TENSOR MEMORY (u8 {0,1}); the MMA
+//                 reads A from TMEM, so shared-memory bandwidth is spent on B only;
 //   B[k, o]     = weight digit planes: w = s * sum_d q_d 2^(8d-23), q_d in u8
-//                 (23-bit fixed point, s = power of two >= w_max).
+//                 (23-bit fixed point, s = power of two >= w_max), in shared
+//                 memory — resident for the whole kernel when it fits, else
+//                 streamed per K stage by cp.async.bulk;
 //   D_d = A x B_d with tcgen05.mma kind::i8 (s32 accumulators in TMEM, exact);
 //   X = D_2 2^16 + D_1 2^8 + D_0 is the exact integer potential in units of
-//   s 2^-23; fire iff X > floor(theta 2^23 / s); P = X s 2^-23 rounded once.
+//   s 2^-30 (A carries the spike as 128 = 2^7); fire iff X > floor(theta 2^30 / s);
+//   P = X s 2^-30 rounded once.
 //
-// Persistent, warp-specialised CTA (one per SM), 16 warps:
+// Persistent, warp-specialised CTA (one per SM), 20 warps:
 //   warps 0-7   producers: im2col gather of latencies from the staged input
-//               band -> expand to the A tile of each K stage
-//   warps 8-11  epilogue: tcgen05.ld -> integer threshold test, warp ballot,
+//               band, expand to A rows, tcgen05.st into the TMEM A stage
+//               (warp w writes lane quadrant w%4, K half w/4); A = 128 [lat <= t]
+//   warps 8-15  epilogue (2 per TMEM lane quadrant): tcgen05.ld -> integer
+//               threshold test, warp ballot,
 //               first-crossing time (popcount: potentials are monotone in t),
-//               potential at the crossing
-//   warp  12    MMA issuer (one thread), TMEM allocator
-//   warp  13    B loader: cp.async.bulk of pre-packed digit planes
-//   warps 14-15 band loaders: copy the input rows a tile needs into smem
-// Pipelines (mbarriers): input band (1-2 buffers), smem K stages (4), TMEM
-// accumulators (1-2 buffers).
+//               potential at the crossing, staged in smem and written as one
+//               run of 128/TP pixels per output map
+//   warp  16    MMA issuer (one thread), TMEM allocator
+//   warp  17    B loader: cp.async.bulk of pre-packed digit planes
+//   warps 18-19 band loaders: copy the input rows a tile needs into smem
+// Pipelines (mbarriers): input band (1-2 buffers), K stages (8; A in TMEM,
+// B in smem), TMEM accumulators (1-2 buffers).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -37,15 +45,24 @@
 
 #include "conv.cuh"
 
+#ifndef SPK_EXP
+#define SPK_EXP 0  // timing experiments only: 1 no wait::st, 2 no gather, 4 no tcgen05.st, 8 no epilogue stores,
+                   // 16 no epilogue tcgen05.ld, 32 no MMA
+#endif
+
 namespace {
 
-constexpr int KS = kTcKS;          // synapses per stage (2 MMAs of K=32)
+constexpr int KS = kTcKS;          // synapses per stage (4 MMAs of K=32)
+static_assert(KS == 128, "tc_stage_* issue exactly 4 k-steps");
 constexpr int S = kTcStages;       // pipeline depth
-constexpr int kThreads = 512;      // 16 warps
-constexpr int kProd = 256;         // warps 0-7
-constexpr int kLoaders = 64;       // warps 14-15
+constexpr int kProdWarps = 8;      // warps 0-7: producers
+constexpr int kEpiWarps = 8;       // warps 8-15: epilogue (two per TMEM lane quadrant)
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 16: MMA issuer; 17: B loader; 18-19: band loaders
+constexpr int kLoaders = 64;
+constexpr int kThreads = (kMmaWarp + 2) * 32 + kLoaders;  // 640
 constexpr int kLoadBatch = 8;      // independent loads in flight per band-loader thread
-constexpr uint32_t kNever = 0xFFFFFFFFu;
+constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-bit column)
+constexpr int kACol0 = 512 - S * kACols;  // first TMEM column of the A stages
 
 // Optional per-role cycle accounting (SPK_CONV_PROF=1): [block][role][total, wait]
 constexpr int kProfRoles = 5;  // producer, epilogue, mma, b-loader, band-loader
@@ -57,11 +74,12 @@ struct TcArgs {
     void* out0;
     float* out1;
     spk_conv_geom g;
-    int Ho, Wo, HWo, K, nks, TP, logTP, PPT, Nt, n_ntiles, NB, tps, NR, band, nrb, rb_stride;
+    int Ho, Wo, HWo, K, nks, Nt, n_ntiles, NB, tps, NR, band, nrb, rb_stride, bres, stack, NS;
+    int WiP, HiP;  // padded input width/height: the staged region includes the zero-padding halo
     long long total_tiles;
     long long theta_q;  // fire iff X > theta_q
     float out_scale;
-    uint32_t a_off, b_off, lc_off, kt_off, rg_off, bar_off;  // smem carve-up
+    uint32_t b_off, lc_off, kt_off, rg_off, ob_off, bar_off;  // smem carve-up
     int prof;
 };
 
@@ -92,19 +110,56 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
 }
-__device__ __forceinline__ void tc_mma_i8(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accum) {
+
+// One K stage of MMAs (KS/32 = 4 k-steps) from a single asm block: digit planes
+// separate (3 accumulators, 12 MMAs) or stacked along N (one accumulator span, 4 MMAs).
+// bdesc: B descriptor of k-step 0 / digit 0; inck: descriptor increment per k-step;
+// incd: per digit plane; acc0: accumulate on the first k-step.
+__device__ __forceinline__ void tc_stage_sep(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t a0, uint64_t bdesc,
+                                             uint64_t inck, uint64_t incd, uint32_t idesc, uint32_t acc0) {
     asm volatile(
-        "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(dtmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        "{\n.reg .pred p0, p1;\n.reg .b64 x0, x1, x2;\n.reg .b32 a;\n"
+        "setp.ne.b32 p0, %8, 0;\n setp.eq.b32 p1, %8, %8;\n"
+        "mov.b64 x0, %4;\n add.s64 x1, x0, %6;\n add.s64 x2, x1, %6;\n mov.b32 a, %3;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p0;\n"
+        "add.s64 x0, x0, %5;\n add.s64 x1, x1, %5;\n add.s64 x2, x2, %5;\n add.u32 a, a, 8;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p1;\n"
+        "add.s64 x0, x0, %5;\n add.s64 x1, x1, %5;\n add.s64 x2, x2, %5;\n add.u32 a, a, 8;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p1;\n"
+        "add.s64 x0, x0, %5;\n add.s64 x1, x1, %5;\n add.s64 x2, x2, %5;\n add.u32 a, a, 8;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p1;\n"
+        "}\n" ::"r"(d0),
+        "r"(d1), "r"(d2), "r"(a0), "l"(bdesc), "l"(inck), "l"(incd), "r"(idesc), "r"(acc0)
+        : "memory");
+}
+__device__ __forceinline__ void tc_stage_stacked(uint32_t d0, uint32_t a0, uint64_t bdesc, uint64_t inck,
+                                                 uint32_t idesc, uint32_t acc0) {
+    asm volatile(
+        "{\n.reg .pred p0, p1;\n.reg .b64 x0;\n.reg .b32 a;\n"
+        "setp.ne.b32 p0, %5, 0;\n setp.eq.b32 p1, %5, %5;\n mov.b64 x0, %2;\n mov.b32 a, %1;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p0;\n"
+        "add.s64 x0, x0, %3;\n add.u32 a, a, 8;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p1;\n"
+        "add.s64 x0, x0, %3;\n add.u32 a, a, 8;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p1;\n"
+        "add.s64 x0, x0, %3;\n add.u32 a, a, 8;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p1;\n"
+        "}\n" ::"r"(d0),
+        "r"(a0), "l"(bdesc), "l"(inck), "r"(idesc), "r"(acc0)
         : "memory");
 }
 // K-major, no swizzle: 8-row x 16-byte core matrices; LBO = stride between the
@@ -120,27 +175,58 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// bytes of a: 1 where a <= t (t < 128), else 0  (SWAR, no cross-byte borrow)
-__device__ __forceinline__ uint32_t le_bytes(uint32_t a, uint32_t tt /* t * 0x01010101 | 0x80808080 */) {
-    const uint32_t hi = a & 0x80808080u;
-    const uint32_t r = tt - (a & 0x7F7F7F7Fu);
-    return ((r & ~hi) & 0x80808080u) >> 7;
+// bytes of a: 0x80 where a <= t, else 0, for byte values a, t < 128 (the staged
+// region clamps latencies to <= 0x7F): no cross-byte borrow since 0x80|t > a.
+__device__ __forceinline__ uint32_t le_bytes80(uint32_t a, uint32_t tt /* t * 0x01010101 | 0x80808080 */) {
+    return (tt - a) & 0x80808080u;
 }
 
-struct TileCoord {
-    int b, p0, r0;  // sample, first pixel of the tile (within the sample), first staged input row
+// Tile bookkeeping without divisions in the loops: a CTA owns the contiguous
+// tile range [t0, t1); tile = (b * tps + j) * n_ntiles + nt.
+struct TileIter {
+    int tile, t1, nt, j, b;
+    __device__ __forceinline__ void init(const TcArgs& a) {
+        tile = (int)((long long)blockIdx.x * a.total_tiles / gridDim.x);
+        t1 = (int)((long long)(blockIdx.x + 1) * a.total_tiles / gridDim.x);
+        const int mt = tile / a.n_ntiles;
+        nt = tile - mt * a.n_ntiles;
+        b = mt / a.tps;
+        j = mt - b * a.tps;
+    }
+    __device__ __forceinline__ bool valid() const { return tile < t1; }
+    __device__ __forceinline__ void next(const TcArgs& a) {
+        ++tile;
+        if (++nt == a.n_ntiles) {
+            nt = 0;
+            if (++j == a.tps) {
+                j = 0;
+                ++b;
+            }
+        }
+    }
+    // the next tile stages a different input region (or there is no next tile)
+    __device__ __forceinline__ bool region_ends(const TcArgs& a) const {
+        if (tile + 1 >= t1) return true;
+        if (nt + 1 < a.n_ntiles) return false;
+        return a.NR == a.HiP ? (j + 1 == a.tps) : true;
+    }
+    // first staged row of this tile, in padded-image rows (input row + Ph)
+    template <int PPT>
+    __device__ __forceinline__ int r0(const TcArgs& a) const {
+        const int lo = ((j * PPT) / a.Wo) * a.g.Sh;  // first padded row the tile's receptive fields touch
+        return max(0, min(lo, a.HiP - a.NR));
+    }
 };
-
-__device__ __forceinline__ TileCoord tile_coord(const TcArgs& a, long long mt) {
-    TileCoord tc;
-    tc.b = (int)(mt / a.tps);
-    tc.p0 = (int)(mt - (long long)tc.b * a.tps) * a.PPT;
-    const int lo = (tc.p0 / a.Wo) * a.g.Sh - a.g.Ph;  // first input row the tile's receptive fields touch
-    tc.r0 = max(0, min(lo, a.g.Hi - a.NR));
-    return tc;
-}
 
 struct RoleClock {
     long long t0 = 0, wait = 0;
@@ -157,7 +243,7 @@ struct RoleClock {
         mbar_wait(bar, parity);
         wait += clock64() - w0;
     }
-    // one lane polls, the warp then proceeds together (no smem polling storm)
+    // one lane polls, the warp then proceeds together
     __device__ __forceinline__ void wait_warp(uint32_t bar, uint32_t parity) {
         if ((threadIdx.x & 31) == 0) wait_on(bar, parity);
         __syncwarp();
@@ -170,65 +256,59 @@ struct RoleClock {
     }
 };
 
-// Contiguous range of tiles of this CTA (consecutive tiles share a sample, so
-// the staged input map is reused across them).
-__device__ __forceinline__ void tile_range(const TcArgs& a, long long& t0, long long& t1) {
-    t0 = (long long)blockIdx.x * a.total_tiles / gridDim.x;
-    t1 = (long long)(blockIdx.x + 1) * a.total_tiles / gridDim.x;
-}
-// Identity of the staged input region a tile reads: the sample when whole
-// sample maps are staged (NR == Hi), else the M tile.
-__device__ __forceinline__ long long region_key(const TcArgs& a, long long tile) {
-    const long long mt = tile / a.n_ntiles;
-    return a.NR == a.g.Hi ? mt / a.tps : mt;
-}
-
 // ------------------------------------------------------------------ the kernel
 template <int EPI, bool PSTAR, int TP>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     constexpr int LOGTP = TP == 16 ? 4 : 5;
+    constexpr int PPT = 128 / TP;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* As = smem + a.a_off;
     uint8_t* Bs = smem + a.b_off;
-    uint8_t* LC = smem + a.lc_off;  // latcol double buffer: [2][PPT][KS]
+    uint8_t* LC = smem + a.lc_off;  // per-producer-warp latcol: [8 warps][2 bufs][2 pixels][KS/2]
     const uint32_t* ktab = reinterpret_cast<const uint32_t*>(smem + a.kt_off);
     uint8_t* RG = smem + a.rg_off;  // staged input band(s): [nrb][Ci][NR][Wi]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-    // barrier map: full[S] empty[S] accf[2] acce[2] rgf[2] rge[2], then the TMEM address
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 8);
+    // barrier map: full[S] empty[S] accf[2] acce[2] rgf[2] rge[2] bres, then the TMEM address
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t accf0 = smem_u32(bars + 2 * S), acce0 = smem_u32(bars + 2 * S + 2);
     const uint32_t rgf0 = smem_u32(bars + 2 * S + 4), rge0 = smem_u32(bars + 2 * S + 6);
+    const uint32_t bresb = smem_u32(bars + 2 * S + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const spk_conv_geom& g = a.g;
 
-    {  // synapse table: (c*NR*Wi + i*Wi + j) << 8 | i << 4 | j, or kNever for padding k >= K
+    {  // synapse table: offset c*NR*WiP + i*WiP + j into the halo'd staged region;
+       // padding synapses k >= K point at the "never" sentinel block after the region
         uint32_t* kt = reinterpret_cast<uint32_t*>(smem + a.kt_off);
         const int KhKw = g.Kh * g.Kw;
         for (int k = threadIdx.x; k < a.nks * KS; k += kThreads) {
-            uint32_t e = kNever;
+            uint32_t e = (uint32_t)(g.Ci * a.band);  // sentinel (reads 0x7F there)
             if (k < a.K) {
                 const int c = k / KhKw, r = k - c * KhKw, i = r / g.Kw, j = r - i * g.Kw;
-                e = ((uint32_t)(c * a.band + i * g.Wi + j) << 8) | ((uint32_t)i << 4) | (uint32_t)j;
+                e = (uint32_t)(c * a.band + i * a.WiP + j);
             }
             kt[k] = e;
         }
     }
+    if (a.NR == a.HiP) {  // whole padded samples: the halo never changes, fill it (and all) once
+        uint32_t* r4 = reinterpret_cast<uint32_t*>(RG);
+        for (int q = threadIdx.x; q < a.nrb * a.rb_stride / 4; q += kThreads) r4[q] = 0x7F7F7F7Fu;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, kProd / 32 + 1);  // producer warps + B-loader arrive.expect_tx
-            mbar_init(empty0 + 8 * s, 1);       // tcgen05.commit
+            mbar_init(full0 + 8 * s, kProdWarps + (a.bres ? 0 : 1));  // producer warps (+ B arrive.expect_tx)
+            mbar_init(empty0 + 8 * s, 1);                             // tcgen05.commit
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(accf0 + 8 * b, 1);          // tcgen05.commit
-            mbar_init(acce0 + 8 * b, 4);               // epilogue warps
-            mbar_init(rgf0 + 8 * b, kLoaders / 32);    // band loader warps
-            mbar_init(rge0 + 8 * b, kProd / 32);       // producer warps
+            mbar_init(accf0 + 8 * b, 1);              // tcgen05.commit
+            mbar_init(acce0 + 8 * b, kEpiWarps);      // epilogue warps
+            mbar_init(rgf0 + 8 * b, kLoaders / 32);   // band loader warps
+            mbar_init(rge0 + 8 * b, kProdWarps);      // producer warps
         }
+        mbar_init(bresb, a.nks);  // resident B: one arrive.expect_tx per K stage
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 12) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -238,177 +318,240 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    if (warp < 8) {
-        // ======================= producers (warps 0-7) =======================
+    if (warp < kProdWarps) {
+        // ======================= producers =======================
         RoleClock rc(a.prof != 0);
-        // Warp w builds row groups w and w+8 of every A stage (pixels pA, pB),
-        // gathering exactly the latencies those rows need: no cross-warp barrier.
-        const int pA = (warp * 8) >> LOGTP, pB = ((warp + 8) * 8) >> LOGTP;
-        const int gsel = lane >> 4;            // gather: 0 -> pA, 1 -> pB
-        const int gk0 = (lane & 15) * 4;       // 4 synapses per lane
-        const int q = lane >> 3, rl = lane & 7;
-        uint8_t* lcw = LC + warp * 256;        // per-warp latcol: [2 bufs][2 pixels][KS]
-        long long t0, t1;
-        tile_range(a, t0, t1);
-        long long sidx = 0, prev_key = -1;
-        int rcount = 0, rb = 0;
-        for (long long tile = t0; tile < t1; ++tile) {
-            const long long key = region_key(a, tile);
-            if (key != prev_key) {
-                prev_key = key;
+        const int quad = warp & 3, half = warp >> 2;
+        const int row = quad * 32 + lane;            // A row this thread writes
+        const int t = row & (TP - 1);
+        const int pslot = (row >> LOGTP) - ((quad * 32) >> LOGTP);  // 0..PPT/4-1
+        // A = 0x80 * [lat <= t]  (bit 7 of  (0x80|t) - (lat & 0x7f), masked by ~lat's bit 7)
+        const uint32_t tt = 0x80808080u | ((uint32_t)t * 0x01010101u);
+        // gather: this warp's pixels ((quad*32)>>LOGTP ..) x its KS/2 synapses of each stage
+        constexpr int HK = KS / 2;                   // synapses per warp per stage (K half)
+        constexpr int GPIX = 32 / TP;                // pixels per warp (2 or 1)
+        constexpr int GB = HK * GPIX / 32;           // bytes gathered per lane (4 or 2)
+        const int gslot = (GPIX == 2) ? (lane >> 4) : 0;
+        const int gk = half * HK + ((GPIX == 2) ? (lane & 15) : lane) * GB;
+        const int gpix_in_tile = ((quad * 32) >> LOGTP) + gslot;
+        uint8_t* lcw = LC + warp * (4 * HK);         // [2 bufs][2 pixels][HK]
+        const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(kACol0 + half * (HK / 4));
+        TileIter ti;
+        ti.init(a);
+        int sidx = 0, rcount = 0, rb = 0;
+        bool need_region = true;
+        for (; ti.valid(); ti.next(a)) {
+            if (need_region) {
                 rb = rcount % a.nrb;
                 rc.wait_warp(rgf0 + 8 * rb, (uint32_t)((rcount / a.nrb) & 1));
                 ++rcount;
             }
-            const bool last_use = (tile + 1 >= t1) || region_key(a, tile + 1) != key;
-            const TileCoord tc = tile_coord(a, tile / a.n_ntiles);
+            const bool last_use = ti.region_ends(a);
+            need_region = last_use;
             const uint8_t* region = RG + rb * a.rb_stride;
-            const int p = tc.p0 + (gsel ? pB : pA);
+            const int p = ti.j * PPT + gpix_in_tile;
             const bool pvalid = p < a.HWo;
-            int y0 = 0, x0 = 0, pixbase = 0;
+            int pixbase = 0;  // region offset of this pixel's receptive-field origin (padded coords)
             if (pvalid) {
                 const int yo = p / a.Wo, xo = p - yo * a.Wo;
-                y0 = yo * g.Sh - g.Ph;
-                x0 = xo * g.Sw - g.Pw;
-                pixbase = (y0 - tc.r0) * g.Wi + x0;
+                pixbase = (yo * g.Sh - ti.r0<PPT>(a)) * a.WiP + xo * g.Sw;
             }
             auto gather = [&](int ks) -> uint32_t {
-                uint32_t packed = 0;
-                const uint4 te4 = *reinterpret_cast<const uint4*>(ktab + ks * KS + gk0);
-                const uint32_t te[4] = {te4.x, te4.y, te4.z, te4.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    uint32_t v = 0xFFu;
-                    if (pvalid && te[e] != kNever) {
-                        const int iy = y0 + (int)((te[e] >> 4) & 15u), ix = x0 + (int)(te[e] & 15u);
-                        if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
-                            v = region[pixbase + (int)(te[e] >> 8)];
-                    }
-                    packed |= v << (8 * e);
+#if (SPK_EXP & 2)
+                return 0x01010101u * (uint32_t)ks;
+#endif
+                if (!pvalid) return 0x7F7F7F7Fu;
+                uint32_t te[GB];
+                if (GB == 4) {
+                    const uint4 t4 = *reinterpret_cast<const uint4*>(ktab + ks * KS + gk);
+                    te[0] = t4.x;
+                    te[1] = t4.y;
+                    te[2] = t4.z;
+                    te[3] = t4.w;
+                } else {
+                    const uint2 t2 = *reinterpret_cast<const uint2*>(ktab + ks * KS + gk);
+                    te[0] = t2.x;
+                    te[1] = t2.y;
                 }
+                uint32_t packed = 0;
+#pragma unroll
+                for (int e = 0; e < GB; ++e) packed |= (uint32_t)region[pixbase + (int)te[e]] << (8 * e);
                 return packed;
             };
             uint32_t cur = gather(0);
             for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
-                const int s = (int)(sidx % S);
-                const uint32_t ph = (uint32_t)((sidx / S) & 1);
-                uint8_t* lc = lcw + (sidx & 1) * 128;
-                *reinterpret_cast<uint32_t*>(lc + gsel * KS + gk0) = cur;
+                const int s = sidx % a.NS;
+                const uint32_t ph = (uint32_t)((sidx / a.NS) & 1);
+                uint8_t* lc = lcw + (sidx & 1) * (2 * HK);
+                if (GB == 4) *reinterpret_cast<uint32_t*>(lc + gslot * HK + (gk - half * HK)) = cur;
+                else *reinterpret_cast<uint16_t*>(lc + gslot * HK + (gk - half * HK)) = (uint16_t)cur;
                 __syncwarp();
-                if (ks + 1 < a.nks) cur = gather(ks + 1);  // next stage's loads overlap this expansion
-                else if (last_use) {  // staged region no longer read by this warp
+                if (ks + 1 < a.nks) {
+                    cur = gather(ks + 1);  // next stage's loads overlap this expansion
+                } else if (last_use) {     // staged region no longer read by this warp
                     __syncwarp();
                     if (lane == 0) mbar_arrive(rge0 + 8 * rb);
                 }
-                // --- wait for the MMAs that last read this A stage, then expand
-                rc.wait_warp(empty0 + 8 * s, ph ^ 1u);
-                uint8_t* A = As + s * (128 * KS);
+                // my row of this A stage: HK synapses of K half `half`
+                uint32_t r[16];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int grp = u * 8 + warp;  // 8-row group; chunk c = q
-                    const int t = (grp * 8 + rl) & (TP - 1);
-                    const uint4 L = *reinterpret_cast<const uint4*>(lc + u * KS + q * 16);
-                    const uint32_t tt = 0x80808080u | ((uint32_t)t * 0x01010101u);
-                    uint4 o;
-                    o.x = le_bytes(L.x, tt);
-                    o.y = le_bytes(L.y, tt);
-                    o.z = le_bytes(L.z, tt);
-                    o.w = le_bytes(L.w, tt);
-                    *reinterpret_cast<uint4*>(A + q * 2048 + grp * 128 + rl * 16) = o;
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const uint4 L = *reinterpret_cast<const uint4*>(lc + pslot * HK + q4 * 16);
+                    r[4 * q4 + 0] = le_bytes80(L.x, tt);
+                    r[4 * q4 + 1] = le_bytes80(L.y, tt);
+                    r[4 * q4 + 2] = le_bytes80(L.z, tt);
+                    r[4 * q4 + 3] = le_bytes80(L.w, tt);
                 }
-                fence_async_smem();
+                // wait for the MMAs that last read this TMEM A stage, then overwrite it
+                rc.wait_warp(empty0 + 8 * s, ph ^ 1u);
+                tc_fence_after();
+#if !(SPK_EXP & 4)
+                tmem_st16(trow + (uint32_t)(s * kACols), r);
+#endif
+#if !(SPK_EXP & 1)
+                tmem_wait_st();
+#endif
+                tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(full0 + 8 * s);
             }
         }
         if (threadIdx.x == 0) rc.store(0);
-    } else if (warp < 12) {
-        // ======================= epilogue (warps 8-11) =======================
+    } else if (warp < kProdWarps + kEpiWarps) {
+        // ======================= epilogue =======================
+        // two warps per TMEM lane quadrant; warp `eh` of a quadrant takes every other 16-column chunk
         RoleClock rc(a.prof != 0);
         const int qd = warp & 3;                  // TMEM lane quadrant
+        const int eh = (warp - kProdWarps) >> 2;  // 0 or 1
         const int row = qd * 32 + lane;           // accumulator row = (pixel, t)
         const int pix = row >> LOGTP, t = row & (TP - 1);
         const int segbase = lane & ~(TP - 1);
         const uint32_t segmask = (TP == 32) ? 0xffffffffu : ((1u << TP) - 1u);
-        long long t0, t1, it = 0;
-        tile_range(a, t0, t1);
-        for (long long tile = t0; tile < t1; ++tile, ++it) {
-            const int buf = (int)(it % a.NB);
-            const long long mt = tile / a.n_ntiles;
-            const int nt = (int)(tile % a.n_ntiles);
-            const int b = (int)(mt / a.tps);
-            const int p = (int)(mt - (long long)b * a.tps) * a.PPT + pix;
-            const bool pvalid = p < a.HWo;
-            const bool rvalid = pvalid && t < g.T;
-            const bool writer = pvalid && t == 0;
+        // store ownership after a 16-column chunk: lane -> (column lane&15, pixel segment lane>>4)
+        const int own_col = lane & 15;
+        const int own_seg = (TP == 16) ? (lane >> 4) : 0;
+        const bool own_lane = (TP == 16) || lane < 16;
+        const int own_pix = ((qd * 32) >> LOGTP) + own_seg;
+        // output staging: [2 tiles][Nt][PPT] lat bytes, then [2][Nt][PPT] P* floats
+        uint8_t* ob_lat = smem + a.ob_off;
+        float* ob_ps = reinterpret_cast<float*>(smem + a.ob_off + 2 * a.Nt * PPT);
+        const int et = threadIdx.x - kProdWarps * 32;  // 0..kEpiWarps*32-1
+        TileIter ti;
+        ti.init(a);
+        for (int it = 0; ti.valid(); ti.next(a), ++it) {
+            const int buf = it % a.NB;
+            const int b = ti.b, nt = ti.nt;
+            const int p0 = ti.j * PPT;
+            const bool rvalid = p0 + pix < a.HWo && t < g.T;
             rc.wait_warp(accf0 + 8 * buf, (uint32_t)((it / a.NB) & 1));
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
-            for (int n0 = 0; n0 < a.Nt; n0 += 16) {
+            for (int n0 = eh * 16; n0 < a.Nt; n0 += 32) {
                 uint32_t d0[16], d1[16], d2[16];
+#if (SPK_EXP & 16)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) d0[q] = d1[q] = d2[q] = (uint32_t)(n0 + q + lane);
+#else
                 tmem_ld16(tbase + n0, d0);
                 tmem_ld16(tbase + a.Nt + n0, d1);
                 tmem_ld16(tbase + 2 * a.Nt + n0, d2);
                 tmem_wait_ld();
+#endif
                 const int obase = nt * a.Nt + n0;
+                if (EPI == SPK_EPI_POTENTIAL) {
 #pragma unroll
-                for (int jj = 0; jj < 16; ++jj) {
-                    const int o = obase + jj;
-                    const int L = (int)d1[jj] * 256 + (int)d0[jj];
-                    const long long X = (long long)(int)d2[jj] * 65536ll + (long long)L;
-                    if (EPI == SPK_EPI_POTENTIAL) {
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const int o = obase + jj;
+                        const long long X =
+                            (long long)(int)d2[jj] * 65536ll + ((long long)(int)d1[jj] * 256ll + (long long)(int)d0[jj]);
                         if (rvalid && o < g.Co)
-                            static_cast<float*>(a.out0)[(((size_t)b * g.T + t) * g.Co + o) * a.HWo + p] =
+                            static_cast<float*>(a.out0)[(((size_t)b * g.T + t) * g.Co + o) * a.HWo + p0 + pix] =
                                 __fmul_rn(__ll2float_rn(X), a.out_scale);
-                    } else {
+                    }
+                } else {
+                    uint32_t mine = 0;
+                    float mine_ps = 0.0f;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const long long X =
+                            (long long)(int)d2[jj] * 65536ll + ((long long)(int)d1[jj] * 256ll + (long long)(int)d0[jj]);
                         const unsigned bal = __ballot_sync(0xffffffffu, rvalid && X > a.theta_q);
-                        const unsigned bits = (bal >> segbase) & segmask;
-                        const int l = g.T - __popc(bits);  // fired steps are exactly t = lat .. T-1
-                        float ps = 0.0f;
+                        if (jj == own_col) mine = bal;
                         if (PSTAR) {
+                            const unsigned bits = (bal >> segbase) & segmask;
+                            const int l = g.T - __popc(bits);  // fired steps are exactly t = lat .. T-1
                             const long long Xs = __shfl_sync(0xffffffffu, X, segbase + min(l, TP - 1));
-                            ps = bits ? __fmul_rn(__ll2float_rn(Xs), a.out_scale) : 0.0f;
+                            if (jj == own_col) mine_ps = bits ? __fmul_rn(__ll2float_rn(Xs), a.out_scale) : 0.0f;
                         }
-                        if (writer && o < g.Co) {
-                            const size_t oi = ((size_t)b * g.Co + o) * a.HWo + p;
-                            static_cast<uint8_t*>(a.out0)[oi] = (uint8_t)l;
-                            if (PSTAR) a.out1[oi] = ps;
-                        }
+                    }
+                    if (own_lane) {  // stage (map, pixel) -> smem
+                        const unsigned bits = (mine >> (own_seg * TP)) & segmask;
+                        const int ol = (n0 + own_col) * PPT + own_pix;
+                        ob_lat[(it & 1) * a.Nt * PPT + ol] = (uint8_t)(g.T - __popc(bits));
+                        if (PSTAR) ob_ps[(it & 1) * a.Nt * PPT + ol] = mine_ps;
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acce0 + 8 * buf);
+            if (EPI != SPK_EPI_POTENTIAL) {
+                // all epilogue warps staged their pixels: write one run of PPT pixels per map
+                asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                const uint8_t* sl = ob_lat + (it & 1) * a.Nt * PPT;
+                const float* sp = ob_ps + (it & 1) * a.Nt * PPT;
+                const int npix = min(PPT, a.HWo - p0);
+                for (int ol = et; ol < a.Nt; ol += kEpiWarps * 32) {
+                    const int o = nt * a.Nt + ol;
+                    if (o >= g.Co || (SPK_EXP & 8)) continue;
+                    const size_t oi = ((size_t)b * g.Co + o) * a.HWo + p0;
+                    uint8_t* dl = static_cast<uint8_t*>(a.out0) + oi;
+                    if (npix == PPT && PPT == 8 && (reinterpret_cast<uintptr_t>(dl) & 7) == 0) {
+                        *reinterpret_cast<uint2*>(dl) = *reinterpret_cast<const uint2*>(sl + ol * PPT);
+                    } else if (npix == PPT && PPT == 4 && (reinterpret_cast<uintptr_t>(dl) & 3) == 0) {
+                        *reinterpret_cast<uint32_t*>(dl) = *reinterpret_cast<const uint32_t*>(sl + ol * PPT);
+                    } else {
+                        for (int q = 0; q < npix; ++q) dl[q] = sl[ol * PPT + q];
+                    }
+                    if (PSTAR) {
+                        float* dp = a.out1 + oi;
+                        for (int q = 0; q < npix; ++q) dp[q] = sp[ol * PPT + q];
+                    }
+                }
+            }
         }
-        if (warp == 8 && lane == 0) rc.store(1);
-    } else if (warp == 12) {
+        if (warp == kProdWarps && lane == 0) rc.store(1);
+    } else if (warp == kMmaWarp) {
         // ======================= MMA issuer =======================
         RoleClock rc(a.prof != 0);
         if (lane == 0) {
-            const uint32_t idesc = (2u << 4) | ((uint32_t)(a.Nt >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-            const uint32_t a_base = smem_u32(As), b_base = smem_u32(Bs);
-            const uint32_t bstage = 3u * a.Nt * KS, bdig = (uint32_t)a.Nt * KS, bchunk = (uint32_t)a.Nt * 16;
-            long long sidx = 0, it = 0, t0, t1;
-            tile_range(a, t0, t1);
-            for (long long tile = t0; tile < t1; ++tile, ++it) {
-                const int buf = (int)(it % a.NB);
+            const int nmma = a.stack ? 3 * a.Nt : a.Nt;  // N of one MMA
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            const uint32_t b_base = smem_u32(Bs);
+            const uint32_t bstage = 3u * a.Nt * KS, bchunk = 3u * a.Nt * 16;  // chunk stride (LBO)
+            const uint64_t d0 = smem_desc(b_base, bchunk, 128);                // descriptor template
+            const uint64_t inck = (2u * bchunk) >> 4;                          // next k-step (2 chunks)
+            const uint64_t incd = ((uint32_t)a.Nt * 16u) >> 4;                 // next digit plane (Nt rows)
+            if (a.bres) rc.wait_on(bresb, 0u);
+            TileIter ti;
+            ti.init(a);
+            int sidx = 0;
+            for (int it = 0; ti.valid(); ti.next(a), ++it) {
+                const int buf = it % a.NB;
                 rc.wait_on(acce0 + 8 * buf, (uint32_t)(((it / a.NB) & 1) ^ 1));
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(buf * 3 * a.Nt);
                 for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
-                    const int s = (int)(sidx % S);
-                    rc.wait_on(full0 + 8 * s, (uint32_t)((sidx / S) & 1));
+                    const int s = sidx % a.NS;
+                    rc.wait_on(full0 + 8 * s, (uint32_t)((sidx / a.NS) & 1));
                     tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < KS / 32; ++kk) {
-                        const uint64_t ad = smem_desc(a_base + s * (128 * KS) + kk * 2 * 2048, 2048, 128);
-#pragma unroll
-                        for (int d = 0; d < 3; ++d) {
-                            const uint64_t bd =
-                                smem_desc(b_base + s * bstage + d * bdig + kk * 2 * bchunk, bchunk, 128);
-                            tc_mma_i8(dbase + d * a.Nt, ad, bd, idesc, (ks | kk) ? 1u : 0u);
-                        }
+                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)s) * bstage) >> 4);
+                    const uint32_t at = tmem + (uint32_t)(kACol0 + s * kACols);
+                    if (SPK_EXP & 32) {
+                    } else if (a.stack) {
+                        tc_stage_stacked(dbase, at, dst, inck, idesc, ks ? 1u : 0u);
+                    } else {
+                        tc_stage_sep(dbase, dbase + a.Nt, dbase + 2 * a.Nt, at, dst, inck, incd, idesc, ks ? 1u : 0u);
                     }
                     tc_commit(empty0 + 8 * s);
                 }
@@ -417,86 +560,120 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             rc.store(2);
         }
         __syncwarp();
-    } else if (warp == 13) {
+    } else if (warp == kMmaWarp + 1) {
         // ======================= B loader =======================
         RoleClock rc(a.prof != 0);
         if (lane == 0) {
             const uint32_t bstage = 3u * a.Nt * KS;
             const uint32_t b_base = smem_u32(Bs);
-            long long sidx = 0, t0, t1;
-            tile_range(a, t0, t1);
-            for (long long tile = t0; tile < t1; ++tile) {
-                const int nt = (int)(tile % a.n_ntiles);
-                for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
-                    const int s = (int)(sidx % S);
-                    rc.wait_on(empty0 + 8 * s, (uint32_t)(((sidx / S) & 1) ^ 1));
-                    mbar_arrive_tx(full0 + 8 * s, bstage);
-                    bulk_g2s(b_base + s * bstage, a.wpk + ((size_t)nt * a.nks + ks) * bstage, bstage, full0 + 8 * s);
+            if (a.bres) {
+                // whole packed B of the (single) N tile, resident for the kernel
+                for (int ks = 0; ks < a.nks; ++ks) {
+                    mbar_arrive_tx(bresb, bstage);
+                    bulk_g2s(b_base + ks * bstage, a.wpk + (size_t)ks * bstage, bstage, bresb);
+                }
+            } else {
+                TileIter ti;
+                ti.init(a);
+                int sidx = 0;
+                for (; ti.valid(); ti.next(a)) {
+                    for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
+                        const int s = sidx % a.NS;
+                        rc.wait_on(empty0 + 8 * s, (uint32_t)(((sidx / a.NS) & 1) ^ 1));
+                        mbar_arrive_tx(full0 + 8 * s, bstage);
+                        bulk_g2s(b_base + s * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bstage,
+                                 full0 + 8 * s);
+                    }
                 }
             }
             rc.store(3);
         }
         __syncwarp();
     } else {
-        // ======================= input band loaders (warps 14-15) =======================
+        // ======================= input band loaders =======================
         RoleClock rc(a.prof != 0);
         const int lt = threadIdx.x - (kThreads - kLoaders);  // 0..63
         const size_t plane = (size_t)g.Hi * g.Wi;
-        long long t0, t1, prev_key = -1;
-        tile_range(a, t0, t1);
+        TileIter ti;
+        ti.init(a);
         int rcount = 0;
-        for (long long tile = t0; tile < t1; ++tile) {
-            const long long key = region_key(a, tile);
-            if (key == prev_key) continue;  // same staged region as the previous tile
-            prev_key = key;
-            const TileCoord tc = tile_coord(a, tile / a.n_ntiles);
+        bool need_region = true;
+        for (; ti.valid(); ti.next(a)) {
+            const bool load = need_region;
+            need_region = ti.region_ends(a);
+            if (!load) continue;  // same staged region as the previous tile
             const int rb = rcount % a.nrb;
             uint8_t* dst = RG + rb * a.rb_stride;
             rc.wait_warp(rge0 + 8 * rb, (uint32_t)(((rcount / a.nrb) & 1) ^ 1));
             ++rcount;
-            const uint8_t* src = a.lat_in + (size_t)tc.b * g.Ci * plane + (size_t)tc.r0 * g.Wi;
+            // region[c][r][x] = min(lat[b][c][pr0 + r - Ph][x - Pw], 0x7F), 0x7F (never) in the halo
+            const uint8_t* src = a.lat_in + (size_t)ti.b * g.Ci * plane;
             const int total = g.Ci * a.band;
-            if (a.NR == g.Hi && (reinterpret_cast<uintptr_t>(src) & 3) == 0) {
-                // whole sample map, 4-byte aligned: one contiguous block of Ci*Hi*Wi bytes
-                const int n4 = total >> 2;
-                const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
-                uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-                for (int q0 = 0; q0 < n4; q0 += kLoaders * kLoadBatch) {
-                    uint32_t v[kLoadBatch];
+            if (a.NR == a.HiP) {
+                // whole padded sample: the halo was filled once at kernel start; copy the
+                // interior, one contiguous block of Ci*Hi*Wi bytes, 4 bytes per load when aligned
+                const int n = g.Ci * (int)plane;
+                const float inv_plane = 1.0f / (float)plane, inv_w = 1.0f / (float)g.Wi;
+                auto put = [&](int q, uint32_t v) {  // byte v of interior index q
+                    int c = (int)((float)q * inv_plane);
+                    c -= (c * (int)plane > q);
+                    c += ((c + 1) * (int)plane <= q);
+                    const int rem = q - c * (int)plane;
+                    int iy = (int)((float)rem * inv_w);
+                    iy -= (iy * g.Wi > rem);
+                    iy += ((iy + 1) * g.Wi <= rem);
+                    const int ix = rem - iy * g.Wi;
+                    dst[c * a.band + (iy + g.Ph) * a.WiP + ix + g.Pw] = (uint8_t)min(v, 0x7Fu);
+                };
+                if ((reinterpret_cast<uintptr_t>(src) & 3) == 0) {
+                    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+                    const int n4 = n >> 2;
+                    for (int q0 = 0; q0 < n4; q0 += kLoaders * kLoadBatch) {
+                        uint32_t v[kLoadBatch];
 #pragma unroll
-                    for (int u = 0; u < kLoadBatch; ++u) {
-                        const int q = q0 + u * kLoaders + lt;
-                        v[u] = q < n4 ? __ldg(s4 + q) : 0u;
-                    }
+                        for (int u = 0; u < kLoadBatch; ++u) {
+                            const int q = q0 + u * kLoaders + lt;
+                            v[u] = q < n4 ? __ldg(s4 + q) : 0u;
+                        }
 #pragma unroll
-                    for (int u = 0; u < kLoadBatch; ++u) {
-                        const int q = q0 + u * kLoaders + lt;
-                        if (q < n4) d4[q] = v[u];
-                    }
-                }
-                for (int q = (n4 << 2) + lt; q < total; q += kLoaders) dst[q] = __ldg(src + q);
-            } else {
-                // Ci bands of NR*Wi contiguous bytes (channel planes are Hi*Wi apart)
-                int c = lt / a.band, off = lt - (lt / a.band) * a.band;  // running (channel, offset)
-                for (int q0 = 0; q0 < total; q0 += kLoaders * kLoadBatch) {
-                    uint8_t v[kLoadBatch];
-                    int d[kLoadBatch];
+                        for (int u = 0; u < kLoadBatch; ++u) {
+                            const int q = q0 + u * kLoaders + lt;
+                            if (q < n4)
 #pragma unroll
-                    for (int u = 0; u < kLoadBatch; ++u) {
-                        const bool ok = q0 + u * kLoaders + lt < total;
-                        v[u] = ok ? __ldg(src + (size_t)c * plane + off) : (uint8_t)0;
-                        d[u] = ok ? c * a.band + off : -1;
-                        off += kLoaders;
-                        while (off >= a.band) {
-                            off -= a.band;
-                            ++c;
+                                for (int e = 0; e < 4; ++e) put(4 * q + e, (v[u] >> (8 * e)) & 0xFFu);
                         }
                     }
-#pragma unroll
-                    for (int u = 0; u < kLoadBatch; ++u)
-                        if (d[u] >= 0) dst[d[u]] = v[u];
+                    for (int q = (n4 << 2) + lt; q < n; q += kLoaders) put(q, __ldg(src + q));
+                } else {
+                    for (int q = lt; q < n; q += kLoaders) put(q, __ldg(src + q));
+                }
+            } else {
+                // band of NR padded rows: one padded row (c, r) per thread per pass
+                const int pr0 = ti.r0<PPT>(a);
+                for (int row = lt; row < g.Ci * a.NR; row += kLoaders) {
+                    const int c = row / a.NR, r = row - c * a.NR;
+                    const int iy = pr0 + r - g.Ph;
+                    uint8_t* d = dst + c * a.band + r * a.WiP;
+                    if ((unsigned)iy >= (unsigned)g.Hi) {
+                        for (int x = 0; x < a.WiP; ++x) d[x] = 0x7F;
+                        continue;
+                    }
+                    const uint8_t* sr = src + (size_t)c * plane + (size_t)iy * g.Wi;
+                    for (int x = 0; x < g.Pw; ++x) d[x] = 0x7F;
+                    for (int x = 0; x < g.Pw; ++x) d[g.Pw + g.Wi + x] = 0x7F;
+                    int x = 0;
+                    for (; x + 4 <= g.Wi; x += 4) {
+                        const uint8_t v0 = __ldg(sr + x), v1 = __ldg(sr + x + 1), v2 = __ldg(sr + x + 2),
+                                      v3 = __ldg(sr + x + 3);
+                        d[g.Pw + x] = min(v0, (uint8_t)0x7F);
+                        d[g.Pw + x + 1] = min(v1, (uint8_t)0x7F);
+                        d[g.Pw + x + 2] = min(v2, (uint8_t)0x7F);
+                        d[g.Pw + x + 3] = min(v3, (uint8_t)0x7F);
+                    }
+                    for (; x < g.Wi; ++x) d[g.Pw + x] = min(__ldg(sr + x), (uint8_t)0x7F);
                 }
             }
+            if (lt < 16) dst[total + lt] = 0x7F;  // sentinel block for padding synapses
             __syncwarp();
             if (lane == 0) mbar_arrive(rgf0 + 8 * rb);
         }
@@ -506,20 +683,21 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 12) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
     }
 }
 
 // ------------------------------------------------------------------ weight packing
-// Digit planes in the exact smem image of each (n-tile, K-stage) block:
-//   block (nt, ks): [digit 0..2][chunk 0..KS/16-1][Nt/8 row groups][8 rows][16 bytes]
+// Digit planes in the exact smem image of each (n-tile, K-stage) block, digit-stacked
+// along N:  block (nt, ks): [chunk 0..KS/16-1][3*Nt/8 row groups][8 rows][16 bytes],
+// row d*Nt + n holding digit d of output map nt*Nt + n.
 __global__ void pack_weights_kernel(const float* __restrict__ w, int Co, int K, int Nt, int n_ntiles, int nks,
                                     float inv_scale23, uint8_t* __restrict__ wpk, int* __restrict__ flag) {
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // over (nt, ks, c, n, e)
-    const size_t per_block = (size_t)Nt * KS;
-    if (q >= (size_t)n_ntiles * nks * per_block) return;
-    const size_t blk = q / per_block, r = q % per_block;
+    const size_t per_plane = (size_t)Nt * KS;
+    if (q >= (size_t)n_ntiles * nks * per_plane) return;
+    const size_t blk = q / per_plane, r = q % per_plane;
     const int nt = (int)(blk / nks), ks = (int)(blk % nks);
     const int c = (int)(r / ((size_t)Nt * 16)), r2 = (int)(r % ((size_t)Nt * 16));
     const int n = r2 / 16, e = r2 % 16;
@@ -532,10 +710,12 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int Co, int K, 
         x = (x > 8388608.0f) ? 8388608.0f : 0.0f;
     }
     const uint32_t qv = (uint32_t)__float2int_rn(x);  // 0 .. 2^23
-    const size_t dst = blk * 3 * per_block + (size_t)c * Nt * 16 + (size_t)(n >> 3) * 128 + (n & 7) * 16 + e;
-    wpk[dst] = (uint8_t)(qv & 255u);
-    wpk[dst + per_block] = (uint8_t)((qv >> 8) & 255u);
-    wpk[dst + 2 * per_block] = (uint8_t)(qv >> 16);
+    uint8_t* base = wpk + blk * 3 * per_plane + (size_t)c * 3 * Nt * 16;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const int row = d * Nt + n;
+        base[(size_t)(row >> 3) * 128 + (row & 7) * 16 + e] = (uint8_t)((qv >> (8 * d)) & 255u);
+    }
 }
 
 int sm_count() {
@@ -573,22 +753,26 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     p.Wo = (g.Wi + 2 * g.Pw - g.Kw) / g.Sw + 1;
     p.K = g.Ci * g.Kh * g.Kw;
     if (g.T > 32 || p.K > kTcMaxK || g.Kh > 16 || g.Kw > 16) return false;
+    if ((long long)g.B * ((p.Ho * p.Wo + 128 / (g.T <= 16 ? 16 : 32) - 1) / (128 / (g.T <= 16 ? 16 : 32))) * 4 >= (1ll << 31))
+        return false;  // tile indices are 32-bit
     p.KS = KS;
     p.nks = (p.K + KS - 1) / KS;
     p.TP = g.T <= 16 ? 16 : 32;
     p.PPT = 128 / p.TP;
-    int nn = 1;
-    while (true) {
+    // N tiling: accumulators (3 digit planes) + the TMEM A stages share 512 columns
+    const int acc_cols = kACol0;  // 384
+    if (g.Co <= 64) {
+        p.Nt = ((g.Co + 15) / 16) * 16;
+        p.NB = 2;
+    } else {
+        const int nn = (g.Co + 127) / 128;
         const int per = (g.Co + nn - 1) / nn;
-        const int Nt = ((per + 15) / 16) * 16;
-        if (3 * Nt <= 480) {
-            p.Nt = Nt;
-            break;
-        }
-        ++nn;
+        p.Nt = ((per + 15) / 16) * 16;
+        p.NB = (6 * p.Nt <= acc_cols) ? 2 : 1;
     }
+    if (3 * p.Nt * p.NB > acc_cols) return false;
+    p.stack = (3 * p.Nt <= 256) ? 1 : 0;  // one MMA of N = 3 Nt covers the three digit planes
     p.n_ntiles = (g.Co + p.Nt - 1) / p.Nt;
-    p.NB = (6 * p.Nt <= 512) ? 2 : 1;
     const int HWo = p.Ho * p.Wo;
     p.tps = (HWo + p.PPT - 1) / p.PPT;
     // input rows one tile needs: (rows its pixels span) * Sh + Kh - Sh, at most Hi
@@ -597,19 +781,33 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
         const int y0 = (j * p.PPT) / p.Wo, y1 = (std::min(j * p.PPT + p.PPT, HWo) - 1) / p.Wo;
         span = std::max(span, (y1 - y0) * g.Sh + g.Kh);
     }
-    p.NR = std::min(g.Hi, span);
-    p.band = p.NR * g.Wi;
+    // staged region: padded rows (zero-padding halo included, as "never") of every channel
+    p.WiP = g.Wi + 2 * g.Pw;
+    p.HiP = g.Hi + 2 * g.Ph;
+    p.NR = std::min(p.HiP, span);
+    // stage whole (padded) sample maps when two fit comfortably: one load serves every tile of the sample
+    if ((size_t)g.Ci * p.HiP * p.WiP <= 24 * 1024) p.NR = p.HiP;
+    p.band = p.NR * p.WiP;
     p.NP = (long long)g.B * HWo;
     p.n_mtiles = (long long)g.B * p.tps;
     p.total_tiles = p.n_mtiles * p.n_ntiles;
     p.packed_bytes = (size_t)p.n_ntiles * p.nks * 3 * p.Nt * KS;
     p.ws_bytes = 256 + p.packed_bytes;
-    const size_t a = (size_t)S * 128 * KS, b = (size_t)S * 3 * p.Nt * KS, lc = 8 * 256,
-                 kt = 4 * (size_t)p.nks * KS;
-    const size_t region = ((size_t)g.Ci * p.band + 15) & ~(size_t)15;
-    const size_t fixed = a + b + lc + kt + 512;
+    const size_t bstage = (size_t)3 * p.Nt * KS, lc = 8 * 4 * (KS / 2), kt = 4 * (size_t)p.nks * KS;
+    const size_t ob = 2 * (size_t)p.Nt * p.PPT * 5;  // output staging (lat + P*), double-buffered
+    const size_t region = ((size_t)g.Ci * p.band + 16 + 15) & ~(size_t)15;  // + sentinel block
     const size_t cap = 227 * 1024;
-    if (fixed + region > cap || (size_t)g.Ci * p.band >= (1u << 24)) return false;
+    if ((size_t)g.Ci * p.band >= (1u << 24)) return false;
+    const size_t other = lc + kt + ob + 1024;
+    // resident B when there is one N tile and all its K stages fit next to two band buffers
+    const size_t bres_bytes = (size_t)p.nks * bstage;
+    p.bres = (p.n_ntiles == 1 && bres_bytes + other + 2 * region <= cap) ? 1 : 0;
+    // streamed B: as many stages (<= S) as fit next to one band buffer
+    p.NS = S;
+    while (!p.bres && p.NS > 2 && (size_t)p.NS * bstage + other + region > cap) --p.NS;
+    const size_t b = p.bres ? bres_bytes : (size_t)p.NS * bstage;
+    const size_t fixed = b + other;
+    if (fixed + region > cap) return false;
     p.nrb = (fixed + 2 * region <= cap) ? 2 : 1;
     p.rb_stride = region;
     p.smem_bytes = fixed + p.nrb * region;
@@ -625,7 +823,6 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     double scale = std::ldexp(1.0, ex);
     if (std::ldexp(1.0, ex - 1) >= (double)w_max) scale = std::ldexp(1.0, ex - 1);
     const float inv_scale23 = (float)(8388608.0 / scale);
-    const float out_scale = (float)(scale / 8388608.0);
 
     int* flag = static_cast<int*>(ws);
     uint8_t* wpk = static_cast<uint8_t*>(ws) + 256;
@@ -647,32 +844,36 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.HWo = p.Ho * p.Wo;
     a.K = p.K;
     a.nks = p.nks;
-    a.TP = p.TP;
-    a.logTP = p.TP == 16 ? 4 : 5;
-    a.PPT = p.PPT;
     a.Nt = p.Nt;
     a.n_ntiles = p.n_ntiles;
     a.NB = p.NB;
     a.tps = p.tps;
     a.NR = p.NR;
     a.band = p.band;
+    a.WiP = p.WiP;
+    a.HiP = p.HiP;
     a.nrb = p.nrb;
     a.rb_stride = (int)p.rb_stride;
+    a.bres = p.bres;
+    a.stack = p.stack;
+    a.NS = p.NS;
     a.total_tiles = p.total_tiles;
     // fire iff X * s 2^-23 > theta  <=>  X > floor(theta 2^23 / s)   (X integer, scaling exact)
-    a.theta_q = (long long)std::floor((double)theta * (8388608.0 / scale));
-    a.out_scale = out_scale;
+    // spikes enter the MMA as 128: X is in units of s 2^-30
+    a.theta_q = (long long)std::floor((double)theta * (1073741824.0 / scale));
+    a.out_scale = (float)(scale / 1073741824.0);
     static const int prof_env = [] {
         const char* e = std::getenv("SPK_CONV_PROF");
         return e && e[0] == '1' ? 1 : 0;
     }();
     a.prof = prof_env;
-    a.a_off = 0;
-    a.b_off = (uint32_t)(S * 128 * KS);
-    a.lc_off = a.b_off + (uint32_t)(S * 3 * p.Nt * KS);
-    a.kt_off = a.lc_off + 8u * 256u;  // per-producer-warp latcol buffers
+    const size_t bstage = (size_t)3 * p.Nt * KS;
+    a.b_off = 0;
+    a.lc_off = (uint32_t)(p.bres ? p.nks * bstage : p.NS * bstage);
+    a.kt_off = a.lc_off + 8u * 4u * (KS / 2);
     a.rg_off = (a.kt_off + (uint32_t)(4 * p.nks * KS) + 15u) & ~15u;
-    a.bar_off = (a.rg_off + (uint32_t)(p.nrb * p.rb_stride) + 15u) & ~15u;
+    a.ob_off = (a.rg_off + (uint32_t)(p.nrb * p.rb_stride) + 15u) & ~15u;
+    a.bar_off = (a.ob_off + (uint32_t)(2 * p.Nt * p.PPT * 5) + 15u) & ~15u;
     const long long grid = p.total_tiles < sm_count() ? p.total_tiles : sm_count();
     if (p.TP == 16) launch_tp<16>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
     else launch_tp<32>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);

@@ -8,11 +8,12 @@ call fails, SpkError is raised.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "libspk.so"
+_LIB_PATH = Path(os.environ.get("SPK_LIB_OVERRIDE", Path(__file__).resolve().parent / "libspk.so"))
 _lib = None
 
 SPK_PREC = {"fp32": 0, "exact": 1}
