@@ -11,8 +11,6 @@ listings on dense BTCHW arrays:
 """
 from __future__ import annotations
 
-import math
-
 import numpy as np
 
 from . import (conv, conv_event, dog_bank, filter_apply, fire, gabor_bank, gather, inhibit,
@@ -100,7 +98,5 @@ def infer(cfg: dict, imgs: np.ndarray, weights, event: bool = False):
 
 
 def sig3(x: float) -> float:
-    if x <= 0:
-        return 0.0
-    e = math.floor(math.log10(x)) - 2
-    return round(x / 10 ** e) * 10 ** e
+    """Round to 3 significant figures (calibrated thresholds, reading R-THETA-CAL)."""
+    return float(f"{x:.3g}") if x > 0 else 0.0

@@ -65,7 +65,7 @@ constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-b
 constexpr int kACol0 = 512 - S * kACols;  // first TMEM column of the A stages
 
 // Optional per-role cycle accounting (SPK_CONV_PROF=1): [block][role][total, wait]
-constexpr int kProfRoles = 5;  // producer, epilogue, mma, b-loader, band-loader
+constexpr int kProfRoles = 8;  // producer, epilogue, mma, b-loader, band-loader, mma:fence, mma:issue, mma:commit
 __device__ unsigned long long g_conv_prof[1024][kProfRoles][2];
 
 struct TcArgs {
@@ -117,51 +117,42 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                  : "memory");
 }
 
-// One K stage of MMAs (KS/32 = 4 k-steps) from a single asm block: digit planes
-// separate (3 accumulators, 12 MMAs) or stacked along N (one accumulator span, 4 MMAs).
-// bdesc: B descriptor of k-step 0 / digit 0; inck: descriptor increment per k-step;
-// incd: per digit plane; acc0: accumulate on the first k-step.
+// One K stage of MMAs (NK <= KS/32 = 4 k-steps) from a single asm block: digit
+// planes separate (3 accumulators, 3 NK MMAs) or stacked along N (one accumulator
+// span, NK MMAs).  bdesc: B descriptor of k-step 0 / digit 0; inck: descriptor
+// increment per k-step; incd: per digit plane; acc0: accumulate on the first k-step.
+// one k-step of the three digit planes (separate accumulators d0, d1, d2)
+__device__ __forceinline__ void tc_kstep3(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t a, uint64_t x0,
+                                          uint64_t incd, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\n.reg .b64 x1, x2;\n"
+        "setp.ne.b32 p, %7, 0;\n add.s64 x1, %4, %5;\n add.s64 x2, x1, %5;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %4, %6, p;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%1], [%3], x1, %6, p;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%2], [%3], x2, %6, p;\n}\n" ::"r"(d0),
+        "r"(d1), "r"(d2), "r"(a), "l"(x0), "l"(incd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+template <int NK>
 __device__ __forceinline__ void tc_stage_sep(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t a0, uint64_t bdesc,
                                              uint64_t inck, uint64_t incd, uint32_t idesc, uint32_t acc0) {
-    asm volatile(
-        "{\n.reg .pred p0, p1;\n.reg .b64 x0, x1, x2;\n.reg .b32 a;\n"
-        "setp.ne.b32 p0, %8, 0;\n setp.eq.b32 p1, %8, %8;\n"
-        "mov.b64 x0, %4;\n add.s64 x1, x0, %6;\n add.s64 x2, x1, %6;\n mov.b32 a, %3;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p0;\n"
-        "add.s64 x0, x0, %5;\n add.s64 x1, x1, %5;\n add.s64 x2, x2, %5;\n add.u32 a, a, 8;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p1;\n"
-        "add.s64 x0, x0, %5;\n add.s64 x1, x1, %5;\n add.s64 x2, x2, %5;\n add.u32 a, a, 8;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p1;\n"
-        "add.s64 x0, x0, %5;\n add.s64 x1, x1, %5;\n add.s64 x2, x2, %5;\n add.u32 a, a, 8;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %7, p1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%1], [a], x1, %7, p1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%2], [a], x2, %7, p1;\n"
-        "}\n" ::"r"(d0),
-        "r"(d1), "r"(d2), "r"(a0), "l"(bdesc), "l"(inck), "l"(incd), "r"(idesc), "r"(acc0)
-        : "memory");
+    static_assert(NK >= 1 && NK <= 4, "k-steps per stage");
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) tc_kstep3(d0, d1, d2, a0 + 8u * kk, bdesc + inck * kk, incd, idesc, kk ? 1u : acc0);
 }
+template <int NK>
 __device__ __forceinline__ void tc_stage_stacked(uint32_t d0, uint32_t a0, uint64_t bdesc, uint64_t inck,
                                                  uint32_t idesc, uint32_t acc0) {
-    asm volatile(
-        "{\n.reg .pred p0, p1;\n.reg .b64 x0;\n.reg .b32 a;\n"
-        "setp.ne.b32 p0, %5, 0;\n setp.eq.b32 p1, %5, %5;\n mov.b64 x0, %2;\n mov.b32 a, %1;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p0;\n"
-        "add.s64 x0, x0, %3;\n add.u32 a, a, 8;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p1;\n"
-        "add.s64 x0, x0, %3;\n add.u32 a, a, 8;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p1;\n"
-        "add.s64 x0, x0, %3;\n add.u32 a, a, 8;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [a], x0, %4, p1;\n"
-        "}\n" ::"r"(d0),
-        "r"(a0), "l"(bdesc), "l"(inck), "r"(idesc), "r"(acc0)
-        : "memory");
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+        asm volatile(
+            "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p; }" ::"r"(d0),
+            "r"(a0 + 8u * kk), "l"(bdesc + inck * kk), "r"(idesc), "r"(kk ? 1u : acc0)
+            : "memory");
+    }
 }
+
 // K-major, no swizzle: 8-row x 16-byte core matrices; LBO = stride between the
 // two 16-byte K chunks of one MMA, SBO = stride between 8-row groups.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -267,12 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     const uint32_t* ktab = reinterpret_cast<const uint32_t*>(smem + a.kt_off);
     uint8_t* RG = smem + a.rg_off;  // staged input band(s): [nrb][Ci][NR][Wi]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-    // barrier map: full[S] empty[S] accf[2] acce[2] rgf[2] rge[2] bres, then the TMEM address
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
+    // barrier map: full[S] empty[S] accf[4] acce[4] rgf[2] rge[2] bres, then the TMEM address
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 13);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
-    const uint32_t accf0 = smem_u32(bars + 2 * S), acce0 = smem_u32(bars + 2 * S + 2);
-    const uint32_t rgf0 = smem_u32(bars + 2 * S + 4), rge0 = smem_u32(bars + 2 * S + 6);
-    const uint32_t bresb = smem_u32(bars + 2 * S + 8);
+    const uint32_t accf0 = smem_u32(bars + 2 * S), acce0 = smem_u32(bars + 2 * S + 4);
+    const uint32_t rgf0 = smem_u32(bars + 2 * S + 8), rge0 = smem_u32(bars + 2 * S + 10);
+    const uint32_t bresb = smem_u32(bars + 2 * S + 12);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const spk_conv_geom& g = a.g;
@@ -299,9 +290,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             mbar_init(full0 + 8 * s, kProdWarps + (a.bres ? 0 : 1));  // producer warps (+ B arrive.expect_tx)
             mbar_init(empty0 + 8 * s, 1);                             // tcgen05.commit
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8 * b, 1);              // tcgen05.commit
             mbar_init(acce0 + 8 * b, kEpiWarps);      // epilogue warps
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(rgf0 + 8 * b, kLoaders / 32);   // band loader warps
             mbar_init(rge0 + 8 * b, kProdWarps);      // producer warps
         }
@@ -533,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const uint64_t inck = (2u * bchunk) >> 4;                          // next k-step (2 chunks)
             const uint64_t incd = ((uint32_t)a.Nt * 16u) >> 4;                 // next digit plane (Nt rows)
             if (a.bres) rc.wait_on(bresb, 0u);
+            long long f_fence = 0, f_issue = 0, f_commit = 0;
             TileIter ti;
             ti.init(a);
             int sidx = 0;
@@ -544,20 +538,48 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
                     const int s = sidx % a.NS;
                     rc.wait_on(full0 + 8 * s, (uint32_t)((sidx / a.NS) & 1));
+                    const long long c0 = rc.on ? clock64() : 0;
                     tc_fence_after();
+                    const long long c1 = rc.on ? clock64() : 0;
                     const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)s) * bstage) >> 4);
                     const uint32_t at = tmem + (uint32_t)(kACol0 + s * kACols);
+                    // k-steps of 32 synapses this stage holds (the last stage may be partial)
+                    const int nk = min(KS / 32, (a.K - ks * KS + 31) / 32);
+                    const uint32_t acc0 = ks ? 1u : 0u;
                     if (SPK_EXP & 32) {
                     } else if (a.stack) {
-                        tc_stage_stacked(dbase, at, dst, inck, idesc, ks ? 1u : 0u);
+                        switch (nk) {
+                            case 1: tc_stage_stacked<1>(dbase, at, dst, inck, idesc, acc0); break;
+                            case 2: tc_stage_stacked<2>(dbase, at, dst, inck, idesc, acc0); break;
+                            case 3: tc_stage_stacked<3>(dbase, at, dst, inck, idesc, acc0); break;
+                            default: tc_stage_stacked<4>(dbase, at, dst, inck, idesc, acc0); break;
+                        }
                     } else {
-                        tc_stage_sep(dbase, dbase + a.Nt, dbase + 2 * a.Nt, at, dst, inck, incd, idesc, ks ? 1u : 0u);
+                        const uint32_t e1 = dbase + a.Nt, e2 = dbase + 2 * a.Nt;
+                        switch (nk) {
+                            case 1: tc_stage_sep<1>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
+                            case 2: tc_stage_sep<2>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
+                            case 3: tc_stage_sep<3>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
+                            default: tc_stage_sep<4>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
+                        }
                     }
+                    const long long c2 = rc.on ? clock64() : 0;
                     tc_commit(empty0 + 8 * s);
+                    if (rc.on) {
+                        const long long c3 = clock64();
+                        f_fence += c1 - c0;
+                        f_issue += c2 - c1;
+                        f_commit += c3 - c2;
+                    }
                 }
                 tc_commit(accf0 + 8 * buf);
             }
             rc.store(2);
+            if (rc.on && blockIdx.x < 1024) {
+                g_conv_prof[blockIdx.x][5][0] = f_fence;
+                g_conv_prof[blockIdx.x][6][0] = f_issue;
+                g_conv_prof[blockIdx.x][7][0] = f_commit;
+            }
         }
         __syncwarp();
     } else if (warp == kMmaWarp + 1) {
@@ -763,13 +785,12 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     const int acc_cols = kACol0;  // 384
     if (g.Co <= 64) {
         p.Nt = ((g.Co + 15) / 16) * 16;
-        p.NB = 2;
     } else {
         const int nn = (g.Co + 127) / 128;
         const int per = (g.Co + nn - 1) / nn;
         p.Nt = ((per + 15) / 16) * 16;
-        p.NB = (6 * p.Nt <= acc_cols) ? 2 : 1;
     }
+    p.NB = std::min(4, acc_cols / (3 * p.Nt));  // TMEM accumulator buffers (MMA/epilogue overlap)
     if (3 * p.Nt * p.NB > acc_cols) return false;
     p.stack = (3 * p.Nt <= 256) ? 1 : 0;  // one MMA of N = 3 Nt covers the three digit planes
     p.n_ntiles = (g.Co + p.Nt - 1) / p.Nt;
@@ -881,7 +902,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
 }
 
 // Debug: copy the per-role cycle counters of the last profiled conv (SPK_CONV_PROF=1)
-// into host memory [1024][5][2] (u64).  Not part of the public ABI.
+// into host memory [1024][8][2] (u64).  Not part of the public ABI.
 extern "C" __attribute__((visibility("default"))) int spk_debug_conv_prof(void* host) {
     return (int)cudaMemcpyFromSymbol(host, g_conv_prof, sizeof(g_conv_prof));
 }

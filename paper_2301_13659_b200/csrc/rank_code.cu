@@ -15,7 +15,6 @@
 
 namespace {
 
-constexpr int kThreads = 1024;
 constexpr int kGroup = 16;                    // boundary targets resolved per sweep
 constexpr int kStageMax = 40 * 1024;          // values staged in smem up to this many
 
@@ -54,7 +53,7 @@ __device__ __forceinline__ unsigned int block_sum(unsigned int v, unsigned int* 
     return v;
 }
 
-template <bool STAGED>
+template <bool STAGED, int kThreads>
 __global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __restrict__ y, int N, int T,
                                                             float thresh, int sort,
                                                             uint8_t* __restrict__ lat) {
@@ -217,17 +216,22 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
     SPK_CHECK(T <= 254, SPK_ERR_UNSUPPORTED, "T=%d > 254 (u8 latency)", T);
     SPK_CHECK(B <= 0x7fffffff, SPK_ERR_SHAPE, "B too large");
     cudaStream_t s = spk::as_cuda(stream);
+    if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
+        const size_t smem = sizeof(unsigned int) * (size_t)N;
+        rank_code_kernel<true, 256><<<B, 256, smem, s>>>(y, N, T, thresh, sort, lat);
+        return spk::launched("rank_code_kernel<staged,256>");
+    }
     if (N <= kStageMax) {
         const size_t smem = sizeof(unsigned int) * (size_t)N;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(rank_code_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(rank_code_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned int) * kStageMax));
             attr = true;
         }
-        rank_code_kernel<true><<<B, kThreads, smem, s>>>(y, N, T, thresh, sort, lat);
-        return spk::launched("rank_code_kernel<staged>");
+        rank_code_kernel<true, 1024><<<B, 1024, smem, s>>>(y, N, T, thresh, sort, lat);
+        return spk::launched("rank_code_kernel<staged,1024>");
     }
-    rank_code_kernel<false><<<B, kThreads, 0, s>>>(y, N, T, thresh, sort, lat);
-    return spk::launched("rank_code_kernel<global>");
+    rank_code_kernel<false, 1024><<<B, 1024, 0, s>>>(y, N, T, thresh, sort, lat);
+    return spk::launched("rank_code_kernel<global,1024>");
 }

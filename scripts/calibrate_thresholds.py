@@ -4,7 +4,8 @@ Reading R-THETA-CAL: the paper and BASELINE.json give no threshold
 for these layers, so theta_l = the 80th percentile of the final-step potentials
 P[T-1] of layer l over global images 0..15 of the config's seed (earlier layers
 at their own thresholds), rounded to 3 significant figures, then written into
-configs/<name>.json.  Calls only oracle/ (the CPU oracle) and synth/.
+configs/<name>.json.  Calls only oracle/ (the CPU oracle) and synth/; images are
+processed one at a time so the fp64 potentials of big layers fit in memory.
 """
 import json
 import sys
@@ -20,18 +21,31 @@ import synth  # noqa: E402
 
 def calibrate(name: str, n_images: int = 16) -> dict:
     cfg = synth.load_config(name)
-    imgs = synth.images(cfg, 0, n_images)
     Ws = synth.layer_weights(cfg)
     T = cfg["T"]
-    _, lat0 = pipeline.front_end(cfg, imgs)
-    S = oracle.lat_to_dense(lat0, T)
-    for li, L in enumerate(cfg["layers"]):
-        P = oracle.conv_event(oracle.dense_to_lat(S), T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
-        if L["theta"] is None:
-            L["theta"] = pipeline.sig3(float(np.percentile(P[:, T - 1], 80)))
-            print(f"{name} layer {li}: theta = {L['theta']}")
-        S = oracle.pool(oracle.fire(P, L["theta"]), (L["pool"]["kernel"],) * 2,
-                        (L["pool"]["stride"],) * 2, (L["pool"]["pad"],) * 2) if L["pool"] else oracle.fire(P, L["theta"])
+    nl = len(cfg["layers"])
+    for li in range(nl):
+        L = cfg["layers"][li]
+        if L["theta"] is not None:
+            continue
+        finals = []
+        for q in range(n_images):
+            img = synth.images(cfg, q, 1)
+            _, lat = pipeline.front_end(cfg, img)
+            for lj in range(li + 1):
+                Lj = cfg["layers"][lj]
+                P = oracle.conv_event(lat, T, Ws[lj], (Lj["stride"],) * 2, (Lj["pad"],) * 2)
+                if lj == li:
+                    finals.append(P[:, T - 1].ravel())
+                    break
+                S = oracle.fire(P, Lj["theta"])
+                del P
+                if Lj["pool"]:
+                    p = Lj["pool"]
+                    S = oracle.pool(S, (p["kernel"],) * 2, (p["stride"],) * 2, (p["pad"],) * 2)
+                lat = oracle.dense_to_lat(S)
+        L["theta"] = pipeline.sig3(float(np.percentile(np.concatenate(finals), 80)))
+        print(f"{name} layer {li}: theta = {L['theta']}", flush=True)
     path = synth.CONFIG_DIR / f"{name.lower()}.json"
     raw = json.loads(path.read_text())
     for li, L in enumerate(cfg["layers"]):

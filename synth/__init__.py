@@ -104,6 +104,25 @@ def images(cfg: dict, start: int, count: int) -> np.ndarray:
     return out
 
 
+def _images_chunk(args):
+    cfg, start, count = args
+    return images(cfg, start, count)
+
+
+def images_parallel(cfg: dict, start: int, count: int, workers: int | None = None) -> np.ndarray:
+    """images() spread over host processes (bit-identical: each image depends only on its index)."""
+    import os
+    from concurrent.futures import ProcessPoolExecutor
+
+    workers = workers or min(16, os.cpu_count() or 1)
+    if count < 64 or workers <= 1:
+        return images(cfg, start, count)
+    step = (count + workers - 1) // workers
+    jobs = [(cfg, start + q, min(step, count - q)) for q in range(0, count, step)]
+    with ProcessPoolExecutor(workers) as ex:
+        return np.concatenate(list(ex.map(_images_chunk, jobs)))
+
+
 def labels(cfg: dict, start: int, count: int, classes: int = 10) -> np.ndarray:
     """Labels uniform over 0..classes-1, one draw per global index (C3)."""
     return np.array([int(_rng(cfg["seed"], 0x1AB, start + q).integers(0, classes)) for q in range(count)],

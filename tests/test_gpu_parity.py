@@ -364,3 +364,54 @@ def test_c2_full_batch_sampled(spk):
     S_in = oracle.lat_to_dense(host(net.input_of(2)), T)
     W = oracle.stdp(Ws[2], S_in, gw, gn, [tuple(c) for c in cfg["stdp"]], (1, 1), (2, 2))
     np.testing.assert_array_equal(host(net.weights[2]), W)
+
+
+def test_pipeline_c4_train_t30(spk):
+    """Caltech-shaped C4 (Gabor front end, T = 30 -> 32-row time tiles), layer-2 training step, 1 image."""
+    assert _check_pipeline(synth.load_config("c4"), 1) <= 1
+
+
+def _check_forward(cfg, n):
+    from paper_2301_13659_b200.network import Network
+
+    imgs = synth.images(cfg, 0, n)
+    Ws = synth.layer_weights(cfg)
+    T = cfg["T"]
+    net = Network(cfg, n)
+    net.img.copy_(cu(imgs))
+    net.set_weights([cu(w) for w in Ws])
+    net.infer()
+    torch.cuda.synchronize()
+    _, lat0 = opipe.front_end(cfg, imgs)
+    np.testing.assert_array_equal(host(net.lat0), lat0)
+    lat = lat0
+    excluded = np.zeros(n, bool)
+    for li, L in enumerate(cfg["layers"]):
+        P = oracle.conv_event(lat, T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
+        rlat, _ = lat_and_pstar(P, L["theta"])
+        excl = near_threshold(P, L["theta"])
+        del P
+        glat = host(net.layers[li]["lat"])
+        diff = (glat != rlat) & ~excluded[:, None, None, None]
+        assert not (diff & ~excl).any(), f"layer {li}: unexplained latency mismatches"
+        excluded |= diff.any(axis=(1, 2, 3))
+        if L["pool"]:
+            p = L["pool"]
+            lat = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(rlat, T), (p["kernel"],) * 2,
+                                                  (p["stride"],) * 2, (p["pad"],) * 2))
+            np.testing.assert_array_equal(host(net.layers[li]["pooled"])[~excluded], lat[~excluded])
+        else:
+            lat = rlat
+    feats = oracle.gather(oracle.lat_to_dense(lat, T))
+    np.testing.assert_array_equal(host(net.features)[~excluded], feats[~excluded])
+    return int(excluded.sum())
+
+
+@pytest.mark.slow
+def test_pipeline_c5_forward(spk):
+    """ImageNet-shaped C5 forward (3 conv layers of 128/256/512 maps, fp16-representable weights) + gather."""
+    assert _check_forward(synth.load_config("c5"), 1) == 0
+
+
+def test_forward_c2_all_layers(spk):
+    assert _check_forward(synth.load_config("c2"), 6) <= 1
