@@ -65,7 +65,7 @@ constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-b
 constexpr int kACol0 = 512 - S * kACols;  // first TMEM column of the A stages
 
 // Optional per-role cycle accounting (SPK_CONV_PROF=1): [block][role][total, wait]
-constexpr int kProfRoles = 8;  // producer, epilogue, mma, b-loader, band-loader, mma:fence, mma:issue, mma:commit
+constexpr int kProfRoles = 17;  // producer, epilogue, mma, b-loader, band-loader, mma:fence/issue/commit, producer sections x6
 __device__ unsigned long long g_conv_prof[1024][kProfRoles][2];
 
 struct TcArgs {
@@ -329,16 +329,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         const int gpix_in_tile = ((quad * 32) >> LOGTP) + gslot;
         uint8_t* lcw = LC + warp * (4 * HK);         // [2 bufs][2 pixels][HK]
         const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(kACol0 + half * (HK / 4));
+        long long pt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         TileIter ti;
         ti.init(a);
         int sidx = 0, rcount = 0, rb = 0;
         bool need_region = true;
+        long long tprev = rc.on ? clock64() : 0;
         for (; ti.valid(); ti.next(a)) {
+            const long long tt0 = rc.on ? clock64() : 0;
+            if (rc.on) pt[7] += tt0 - tprev;
             if (need_region) {
                 rb = rcount % a.nrb;
                 rc.wait_warp(rgf0 + 8 * rb, (uint32_t)((rcount / a.nrb) & 1));
                 ++rcount;
             }
+            const long long tt1 = rc.on ? clock64() : 0;
+            if (rc.on) pt[8] += tt1 - tt0;
             const bool last_use = ti.region_ends(a);
             need_region = last_use;
             const uint8_t* region = RG + rb * a.rb_stride;
@@ -372,19 +378,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 return packed;
             };
             uint32_t cur = gather(0);
+            if (rc.on) pt[6] += clock64() - tt1;
             for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
+                long long q0 = rc.on ? clock64() : 0;
                 const int s = sidx % a.NS;
                 const uint32_t ph = (uint32_t)((sidx / a.NS) & 1);
                 uint8_t* lc = lcw + (sidx & 1) * (2 * HK);
                 if (GB == 4) *reinterpret_cast<uint32_t*>(lc + gslot * HK + (gk - half * HK)) = cur;
                 else *reinterpret_cast<uint16_t*>(lc + gslot * HK + (gk - half * HK)) = (uint16_t)cur;
                 __syncwarp();
+                long long q1 = rc.on ? clock64() : 0;
                 if (ks + 1 < a.nks) {
                     cur = gather(ks + 1);  // next stage's loads overlap this expansion
                 } else if (last_use) {     // staged region no longer read by this warp
                     __syncwarp();
                     if (lane == 0) mbar_arrive(rge0 + 8 * rb);
                 }
+                long long q2 = rc.on ? clock64() : 0;
                 // my row of this A stage: HK synapses of K half `half`
                 uint32_t r[16];
 #pragma unroll
@@ -395,8 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     r[4 * q4 + 2] = le_bytes80(L.z, tt);
                     r[4 * q4 + 3] = le_bytes80(L.w, tt);
                 }
+                long long q3 = rc.on ? clock64() : 0;
                 // wait for the MMAs that last read this TMEM A stage, then overwrite it
                 rc.wait_warp(empty0 + 8 * s, ph ^ 1u);
+                long long q4 = rc.on ? clock64() : 0;
                 tc_fence_after();
 #if !(SPK_EXP & 4)
                 tmem_st16(trow + (uint32_t)(s * kACols), r);
@@ -405,11 +417,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 tmem_wait_st();
 #endif
                 tc_fence_before();
+                long long q5 = rc.on ? clock64() : 0;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(full0 + 8 * s);
+                if (rc.on) {
+                    const long long q6 = clock64();
+                    pt[0] += q1 - q0;  // latcol store + syncwarp
+                    pt[1] += q2 - q1;  // next gather issue
+                    pt[2] += q3 - q2;  // expansion (LDS + SWAR)
+                    pt[3] += q4 - q3;  // empty wait (incl. warp sync)
+                    pt[4] += q5 - q4;  // fence + tcgen05.st + wait::st + fence
+                    pt[5] += q6 - q5;  // sync + arrive
+                }
             }
+            tprev = rc.on ? clock64() : 0;
         }
-        if (threadIdx.x == 0) rc.store(0);
+        if (threadIdx.x == 0) {
+            rc.store(0);
+            if (rc.on && blockIdx.x < 1024)
+                for (int q = 0; q < 9; ++q) g_conv_prof[blockIdx.x][8 + q][0] = pt[q];
+        }
     } else if (warp < kProdWarps + kEpiWarps) {
         // ======================= epilogue =======================
         // two warps per TMEM lane quadrant; warp `eh` of a quadrant takes every other 16-column chunk
@@ -902,7 +929,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
 }
 
 // Debug: copy the per-role cycle counters of the last profiled conv (SPK_CONV_PROF=1)
-// into host memory [1024][8][2] (u64).  Not part of the public ABI.
+// into host memory [1024][17][2] (u64).  Not part of the public ABI.
 extern "C" __attribute__((visibility("default"))) int spk_debug_conv_prof(void* host) {
     return (int)cudaMemcpyFromSymbol(host, g_conv_prof, sizeof(g_conv_prof));
 }

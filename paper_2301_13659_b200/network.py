@@ -44,7 +44,8 @@ class Network:
         self.weights: list[torch.Tensor] = []
         self.layers = []
         ci, h, w = im["C"] * K, H, W
-        for L in cfg["layers"]:
+        tl = cfg.get("train_layer")
+        for li, L in enumerate(cfg["layers"]):
             Ho = (h + 2 * L["pad"] - L["K"]) // L["stride"] + 1
             Wo = (w + 2 * L["pad"] - L["K"]) // L["stride"] + 1
             geom = spk.ConvGeom(batch, self.T, ci, h, w, L["Co"], L["K"], L["K"], L["stride"], L["stride"],
@@ -52,7 +53,9 @@ class Network:
             rec = dict(
                 L=L, geom=geom, Ho=Ho, Wo=Wo,
                 lat=torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.uint8, device=self.dev),
-                pstar=torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.float32, device=self.dev),
+                # P* (potential at the first crossing) is only needed by the trained layer
+                pstar=(torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.float32, device=self.dev)
+                       if li == tl else None),
                 ws=torch.empty(max(1, spk.conv_workspace(geom, prec)), dtype=torch.uint8, device=self.dev),
             )
             if L["pool"]:
@@ -68,7 +71,6 @@ class Network:
             self.layers.append(rec)
             self.weights.append(torch.zeros((L["Co"], geom.Ci, L["K"], L["K"]), dtype=torch.float32,
                                             device=self.dev))
-        tl = cfg.get("train_layer")
         if tl is not None:
             rec = self.layers[tl]
             wk = rec["L"]["wta"]
