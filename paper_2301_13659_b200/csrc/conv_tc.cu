@@ -59,7 +59,9 @@ constexpr int kProdWarps = 8;      // warps 0-7: producers
 constexpr int kEpiWarps = 8;       // warps 8-15: epilogue (two per TMEM lane quadrant)
 constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 16: MMA issuer; 17: B loader; 18-19: band loaders
 constexpr int kLoaders = 64;
-constexpr int kThreads = (kMmaWarp + 2) * 32 + kLoaders;  // 640
+constexpr int kFlushWarp = kMmaWarp + 4;           // warp 20: writes staged output tiles to HBM
+constexpr int kThreads = (kFlushWarp + 1) * 32;   // 672
+constexpr int kNOB = 4;                            // output staging ring (tiles)
 constexpr int kLoadBatch = 8;      // independent loads in flight per band-loader thread
 constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-bit column)
 constexpr int kACol0 = 512 - S * kACols;  // first TMEM column of the A stages
@@ -75,6 +77,7 @@ struct TcArgs {
     float* out1;
     spk_conv_geom g;
     int Ho, Wo, HWo, K, nks, Nt, n_ntiles, NB, tps, NR, band, nrb, rb_stride, bres, stack, NS;
+    int retain;  // the A stages of an M tile stay in TMEM for all its N tiles (nks <= S)
     int WiP, HiP;  // padded input width/height: the staged region includes the zero-padding halo
     long long total_tiles;
     long long theta_q;  // fire iff X > theta_q
@@ -95,15 +98,28 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t a, uint32_t bytes) {
     asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(a), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+    return ok != 0;
+}
+// critical-path waits (producers, MMA issuer) poll
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-    uint32_t ok = 0;
-    do {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-    } while (!ok);
+    while (!mbar_try(a, parity)) {
+    }
+}
+#ifndef SPK_IDLE_NS
+#define SPK_IDLE_NS 256
+#endif
+// waits of roles with slack (epilogue, loaders, flusher) back off between polls so that
+// their spinning does not take issue slots from the producers on the same scheduler
+__device__ __forceinline__ void mbar_wait_idle(uint32_t a, uint32_t parity) {
+    while (!mbar_try(a, parity)) {
+        if (SPK_IDLE_NS > 0) __nanosleep(SPK_IDLE_NS);
+    }
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -112,9 +128,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+// the same from a converged warp: one elected lane commits
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+    asm volatile(
+        "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(bar)
+        : "memory");
 }
 
 // One K stage of MMAs (NK <= KS/32 = 4 k-steps) from a single asm block: digit
@@ -122,14 +141,18 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
 // span, NK MMAs).  bdesc: B descriptor of k-step 0 / digit 0; inck: descriptor
 // increment per k-step; incd: per digit plane; acc0: accumulate on the first k-step.
 // one k-step of the three digit planes (separate accumulators d0, d1, d2)
+// Issued by the whole (converged) MMA warp with warp-uniform operands, one elected
+// lane executing the MMAs: the operands then live in uniform registers and each
+// tcgen05.mma is a single UTCIMMA (no per-thread operand broadcast loop).
 __device__ __forceinline__ void tc_kstep3(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t a, uint64_t x0,
                                           uint64_t incd, uint32_t idesc, uint32_t acc) {
     asm volatile(
-        "{\n.reg .pred p;\n.reg .b64 x1, x2;\n"
+        "{\n.reg .pred p, e;\n.reg .b64 x1, x2;\n"
+        "elect.sync _|e, 0xffffffff;\n"
         "setp.ne.b32 p, %7, 0;\n add.s64 x1, %4, %5;\n add.s64 x2, x1, %5;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %4, %6, p;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%1], [%3], x1, %6, p;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%2], [%3], x2, %6, p;\n}\n" ::"r"(d0),
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], %4, %6, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%3], x1, %6, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%2], [%3], x2, %6, p;\n}\n" ::"r"(d0),
         "r"(d1), "r"(d2), "r"(a), "l"(x0), "l"(incd), "r"(idesc), "r"(acc)
         : "memory");
 }
@@ -146,8 +169,8 @@ __device__ __forceinline__ void tc_stage_stacked(uint32_t d0, uint32_t a0, uint6
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
         asm volatile(
-            "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p; }" ::"r"(d0),
+            "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;\n"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p; }" ::"r"(d0),
             "r"(a0 + 8u * kk), "l"(bdesc + inck * kk), "r"(idesc), "r"(kk ? 1u : acc0)
             : "memory");
     }
@@ -187,8 +210,14 @@ __device__ __forceinline__ uint32_t le_bytes80(uint32_t a, uint32_t tt /* t * 0x
 struct TileIter {
     int tile, t1, nt, j, b;
     __device__ __forceinline__ void init(const TcArgs& a) {
-        tile = (int)((long long)blockIdx.x * a.total_tiles / gridDim.x);
-        t1 = (int)((long long)(blockIdx.x + 1) * a.total_tiles / gridDim.x);
+        if (a.retain) {  // whole M tiles per CTA: A is produced once for all N tiles
+            const long long nm = a.total_tiles / a.n_ntiles;
+            tile = (int)((long long)blockIdx.x * nm / gridDim.x) * a.n_ntiles;
+            t1 = (int)((long long)(blockIdx.x + 1) * nm / gridDim.x) * a.n_ntiles;
+        } else {
+            tile = (int)((long long)blockIdx.x * a.total_tiles / gridDim.x);
+            t1 = (int)((long long)(blockIdx.x + 1) * a.total_tiles / gridDim.x);
+        }
         const int mt = tile / a.n_ntiles;
         nt = tile - mt * a.n_ntiles;
         b = mt / a.tps;
@@ -211,6 +240,11 @@ struct TileIter {
         if (nt + 1 < a.n_ntiles) return false;
         return a.NR == a.HiP ? (j + 1 == a.tps) : true;
     }
+    // same, asked at the first N tile of an M tile about the whole M tile (retained A)
+    __device__ __forceinline__ bool region_ends_m(const TcArgs& a) const {
+        if (tile + (a.n_ntiles - nt) >= t1) return true;
+        return a.NR == a.HiP ? (j + 1 == a.tps) : true;
+    }
     // first staged row of this tile, in padded-image rows (input row + Ph)
     template <int PPT>
     __device__ __forceinline__ int r0(const TcArgs& a) const {
@@ -219,6 +253,7 @@ struct TileIter {
     }
 };
 
+#ifdef SPK_CONV_PROF_BUILD
 struct RoleClock {
     long long t0 = 0, wait = 0;
     bool on;
@@ -234,9 +269,18 @@ struct RoleClock {
         mbar_wait(bar, parity);
         wait += clock64() - w0;
     }
+    __device__ __forceinline__ void wait_idle(uint32_t bar, uint32_t parity) {
+        const long long w0 = on ? clock64() : 0;
+        mbar_wait_idle(bar, parity);
+        if (on) wait += clock64() - w0;
+    }
     // one lane polls, the warp then proceeds together
     __device__ __forceinline__ void wait_warp(uint32_t bar, uint32_t parity) {
         if ((threadIdx.x & 31) == 0) wait_on(bar, parity);
+        __syncwarp();
+    }
+    __device__ __forceinline__ void wait_warp_idle(uint32_t bar, uint32_t parity) {
+        if ((threadIdx.x & 31) == 0) wait_idle(bar, parity);
         __syncwarp();
     }
     __device__ void store(int role) {
@@ -246,6 +290,24 @@ struct RoleClock {
         }
     }
 };
+#else
+// production build: no clock reads at all (the instrumented build is a debug aid)
+struct RoleClock {
+    static constexpr bool on = false;
+    __device__ RoleClock(bool) {}
+    __device__ __forceinline__ void wait_on(uint32_t bar, uint32_t parity) { mbar_wait(bar, parity); }
+    __device__ __forceinline__ void wait_idle(uint32_t bar, uint32_t parity) { mbar_wait_idle(bar, parity); }
+    __device__ __forceinline__ void wait_warp(uint32_t bar, uint32_t parity) {
+        if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+        __syncwarp();
+    }
+    __device__ __forceinline__ void wait_warp_idle(uint32_t bar, uint32_t parity) {
+        if ((threadIdx.x & 31) == 0) mbar_wait_idle(bar, parity);
+        __syncwarp();
+    }
+    __device__ void store(int) {}
+};
+#endif
 
 // ------------------------------------------------------------------ the kernel
 template <int EPI, bool PSTAR, int TP>
@@ -258,8 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     const uint32_t* ktab = reinterpret_cast<const uint32_t*>(smem + a.kt_off);
     uint8_t* RG = smem + a.rg_off;  // staged input band(s): [nrb][Ci][NR][Wi]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-    // barrier map: full[S] empty[S] accf[4] acce[4] rgf[2] rge[2] bres, then the TMEM address
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 13);
+    // barrier map: full[S] empty[S] (A stages in TMEM) accf[4] acce[4] rgf[2] rge[2] bres stg[4] fls[4]
+    // bfull[S] bempty[S] (streamed B stages in smem), then the TMEM address
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * S + 21);
+    const uint32_t bfull0 = smem_u32(bars + 2 * S + 21), bempty0 = smem_u32(bars + 3 * S + 21);
+    const uint32_t stg0 = smem_u32(bars + 2 * S + 13), fls0 = smem_u32(bars + 2 * S + 17);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t accf0 = smem_u32(bars + 2 * S), acce0 = smem_u32(bars + 2 * S + 4);
     const uint32_t rgf0 = smem_u32(bars + 2 * S + 8), rge0 = smem_u32(bars + 2 * S + 10);
@@ -287,8 +352,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, kProdWarps + (a.bres ? 0 : 1));  // producer warps (+ B arrive.expect_tx)
-            mbar_init(empty0 + 8 * s, 1);                             // tcgen05.commit
+            mbar_init(full0 + 8 * s, kProdWarps);  // producer warps
+            mbar_init(empty0 + 8 * s, 1);          // tcgen05.commit
+            mbar_init(bfull0 + 8 * s, 1);          // B loader arrive.expect_tx
+            mbar_init(bempty0 + 8 * s, 1);         // tcgen05.commit
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8 * b, 1);              // tcgen05.commit
@@ -299,6 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             mbar_init(rge0 + 8 * b, kProdWarps);      // producer warps
         }
         mbar_init(bresb, a.nks);  // resident B: one arrive.expect_tx per K stage
+        for (int b = 0; b < kNOB; ++b) {
+            mbar_init(stg0 + 8 * b, kEpiWarps);  // output tile staged by every epilogue warp
+            mbar_init(fls0 + 8 * b, 1);          // staged tile written out by the flusher
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kMmaWarp) {
@@ -332,20 +403,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         long long pt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         TileIter ti;
         ti.init(a);
-        int sidx = 0, rcount = 0, rb = 0;
+        int sidx = 0, rb = 0, rbn = 0;
+        uint32_t rgph = 0;
         bool need_region = true;
         long long tprev = rc.on ? clock64() : 0;
         for (; ti.valid(); ti.next(a)) {
+            if (a.retain && ti.nt != 0) continue;  // A of this M tile is already in TMEM
             const long long tt0 = rc.on ? clock64() : 0;
             if (rc.on) pt[7] += tt0 - tprev;
             if (need_region) {
-                rb = rcount % a.nrb;
-                rc.wait_warp(rgf0 + 8 * rb, (uint32_t)((rcount / a.nrb) & 1));
-                ++rcount;
+                rb = rbn;
+                rc.wait_warp(rgf0 + 8 * rb, rgph);
+                if (++rbn == a.nrb) rbn = 0, rgph ^= 1u;
             }
             const long long tt1 = rc.on ? clock64() : 0;
             if (rc.on) pt[8] += tt1 - tt0;
-            const bool last_use = ti.region_ends(a);
+            const bool last_use = a.retain ? ti.region_ends_m(a) : ti.region_ends(a);
             need_region = last_use;
             const uint8_t* region = RG + rb * a.rb_stride;
             const int p = ti.j * PPT + gpix_in_tile;
@@ -381,8 +454,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (rc.on) pt[6] += clock64() - tt1;
             for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
                 long long q0 = rc.on ? clock64() : 0;
-                const int s = sidx % a.NS;
-                const uint32_t ph = (uint32_t)((sidx / a.NS) & 1);
+                const int s = sidx % S;
+                const uint32_t ph = (uint32_t)((sidx / S) & 1);
                 uint8_t* lc = lcw + (sidx & 1) * (2 * HK);
                 if (GB == 4) *reinterpret_cast<uint32_t*>(lc + gslot * HK + (gk - half * HK)) = cur;
                 else *reinterpret_cast<uint16_t*>(lc + gslot * HK + (gk - half * HK)) = (uint16_t)cur;
@@ -452,18 +525,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         const int own_seg = (TP == 16) ? (lane >> 4) : 0;
         const bool own_lane = (TP == 16) || lane < 16;
         const int own_pix = ((qd * 32) >> LOGTP) + own_seg;
-        // output staging: [2 tiles][Nt][PPT] lat bytes, then [2][Nt][PPT] P* floats
+        // output staging ring: [kNOB tiles][Nt][PPT] lat bytes, then [kNOB][Nt][PPT] P* floats
         uint8_t* ob_lat = smem + a.ob_off;
-        float* ob_ps = reinterpret_cast<float*>(smem + a.ob_off + 2 * a.Nt * PPT);
-        const int et = threadIdx.x - kProdWarps * 32;  // 0..kEpiWarps*32-1
+        float* ob_ps = reinterpret_cast<float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
         TileIter ti;
         ti.init(a);
-        for (int it = 0; ti.valid(); ti.next(a), ++it) {
-            const int buf = it % a.NB;
+        int buf = 0, ob = 0;
+        uint32_t acc_ph = 0, ob_ph = 0;  // phase bits of the accumulator / staging rings
+        for (; ti.valid(); ti.next(a)) {
             const int b = ti.b, nt = ti.nt;
             const int p0 = ti.j * PPT;
             const bool rvalid = p0 + pix < a.HWo && t < g.T;
-            rc.wait_warp(accf0 + 8 * buf, (uint32_t)((it / a.NB) & 1));
+            if (EPI != SPK_EPI_POTENTIAL) rc.wait_warp_idle(fls0 + 8 * ob, ob_ph ^ 1u);
+            rc.wait_warp_idle(accf0 + 8 * buf, acc_ph);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
             for (int n0 = eh * 16; n0 < a.Nt; n0 += 32) {
@@ -507,44 +581,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     if (own_lane) {  // stage (map, pixel) -> smem
                         const unsigned bits = (mine >> (own_seg * TP)) & segmask;
                         const int ol = (n0 + own_col) * PPT + own_pix;
-                        ob_lat[(it & 1) * a.Nt * PPT + ol] = (uint8_t)(g.T - __popc(bits));
-                        if (PSTAR) ob_ps[(it & 1) * a.Nt * PPT + ol] = mine_ps;
+                        ob_lat[ob * a.Nt * PPT + ol] = (uint8_t)(g.T - __popc(bits));
+                        if (PSTAR) ob_ps[ob * a.Nt * PPT + ol] = mine_ps;
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acce0 + 8 * buf);
-            if (EPI != SPK_EPI_POTENTIAL) {
-                // all epilogue warps staged their pixels: write one run of PPT pixels per map
-                asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
-                const uint8_t* sl = ob_lat + (it & 1) * a.Nt * PPT;
-                const float* sp = ob_ps + (it & 1) * a.Nt * PPT;
-                const int npix = min(PPT, a.HWo - p0);
-                for (int ol = et; ol < a.Nt; ol += kEpiWarps * 32) {
-                    const int o = nt * a.Nt + ol;
-                    if (o >= g.Co || (SPK_EXP & 8)) continue;
-                    const size_t oi = ((size_t)b * g.Co + o) * a.HWo + p0;
-                    uint8_t* dl = static_cast<uint8_t*>(a.out0) + oi;
-                    if (npix == PPT && PPT == 8 && (reinterpret_cast<uintptr_t>(dl) & 7) == 0) {
-                        *reinterpret_cast<uint2*>(dl) = *reinterpret_cast<const uint2*>(sl + ol * PPT);
-                    } else if (npix == PPT && PPT == 4 && (reinterpret_cast<uintptr_t>(dl) & 3) == 0) {
-                        *reinterpret_cast<uint32_t*>(dl) = *reinterpret_cast<const uint32_t*>(sl + ol * PPT);
-                    } else {
-                        for (int q = 0; q < npix; ++q) dl[q] = sl[ol * PPT + q];
-                    }
-                    if (PSTAR) {
-                        float* dp = a.out1 + oi;
-                        for (int q = 0; q < npix; ++q) dp[q] = sp[ol * PPT + q];
-                    }
-                }
+            if (EPI != SPK_EPI_POTENTIAL) {  // hand the staged tile to the flusher warp
+                __syncwarp();
+                if (lane == 0) mbar_arrive(stg0 + 8 * ob);
             }
+            if (++buf == a.NB) buf = 0, acc_ph ^= 1u;
+            if (++ob == kNOB) ob = 0, ob_ph ^= 1u;
         }
         if (warp == kProdWarps && lane == 0) rc.store(1);
     } else if (warp == kMmaWarp) {
         // ======================= MMA issuer =======================
         RoleClock rc(a.prof != 0);
-        if (lane == 0) {
+        {  // the whole warp runs the loop (uniform control flow); elected lanes issue
             const int nmma = a.stack ? 3 * a.Nt : a.Nt;  // N of one MMA
             const uint32_t idesc = (2u << 4) | ((uint32_t)(nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             const uint32_t b_base = smem_u32(Bs);
@@ -552,23 +608,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const uint64_t d0 = smem_desc(b_base, bchunk, 128);                // descriptor template
             const uint64_t inck = (2u * bchunk) >> 4;                          // next k-step (2 chunks)
             const uint64_t incd = ((uint32_t)a.Nt * 16u) >> 4;                 // next digit plane (Nt rows)
-            if (a.bres) rc.wait_on(bresb, 0u);
+            if (a.bres) rc.wait_warp(bresb, 0u);
             long long f_fence = 0, f_issue = 0, f_commit = 0;
             TileIter ti;
             ti.init(a);
-            int sidx = 0;
-            for (int it = 0; ti.valid(); ti.next(a), ++it) {
-                const int buf = it % a.NB;
-                rc.wait_on(acce0 + 8 * buf, (uint32_t)(((it / a.NB) & 1) ^ 1));
+            int asidx = 0, bs = 0, buf = 0;  // A ring (TMEM, S slots), B ring (smem, NS slots), accumulators
+            uint32_t b_ph = 0, acc_ph = 0;
+            for (; ti.valid(); ti.next(a)) {
+                // a retained A is produced at the first N tile and released after the last one
+                const bool newA = !a.retain || ti.nt == 0, lastA = !a.retain || ti.nt == a.n_ntiles - 1;
+                rc.wait_warp(acce0 + 8 * buf, acc_ph ^ 1u);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(buf * 3 * a.Nt);
-                for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
-                    const int s = sidx % a.NS;
-                    rc.wait_on(full0 + 8 * s, (uint32_t)((sidx / a.NS) & 1));
+                for (int ks = 0; ks < a.nks; ++ks) {
+                    const int s = (asidx + ks) % S;
+                    if (newA) rc.wait_warp(full0 + 8 * s, (uint32_t)(((asidx + ks) / S) & 1));
+                    if (!a.bres) rc.wait_warp(bfull0 + 8 * bs, b_ph);
                     const long long c0 = rc.on ? clock64() : 0;
                     tc_fence_after();
                     const long long c1 = rc.on ? clock64() : 0;
-                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)s) * bstage) >> 4);
+                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)bs) * bstage) >> 4);
                     const uint32_t at = tmem + (uint32_t)(kACol0 + s * kACols);
                     // k-steps of 32 synapses this stage holds (the last stage may be partial)
                     const int nk = min(KS / 32, (a.K - ks * KS + 31) / 32);
@@ -591,7 +650,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                         }
                     }
                     const long long c2 = rc.on ? clock64() : 0;
-                    tc_commit(empty0 + 8 * s);
+                    if (!a.bres) {
+                        tc_commit_elect(bempty0 + 8 * bs);
+                        if (++bs == a.NS) bs = 0, b_ph ^= 1u;
+                    }
+                    if (lastA) tc_commit_elect(empty0 + 8 * s);
                     if (rc.on) {
                         const long long c3 = clock64();
                         f_fence += c1 - c0;
@@ -599,10 +662,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                         f_commit += c3 - c2;
                     }
                 }
-                tc_commit(accf0 + 8 * buf);
+                tc_commit_elect(accf0 + 8 * buf);
+                if (lastA) asidx += a.nks;
+                if (++buf == a.NB) buf = 0, acc_ph ^= 1u;
             }
-            rc.store(2);
-            if (rc.on && blockIdx.x < 1024) {
+            if (lane == 0) rc.store(2);
+            if (rc.on && lane == 0 && blockIdx.x < 1024) {
                 g_conv_prof[blockIdx.x][5][0] = f_fence;
                 g_conv_prof[blockIdx.x][6][0] = f_issue;
                 g_conv_prof[blockIdx.x][7][0] = f_commit;
@@ -624,37 +689,37 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             } else {
                 TileIter ti;
                 ti.init(a);
-                int sidx = 0;
+                int s = 0;
+                uint32_t ph = 0;
                 for (; ti.valid(); ti.next(a)) {
-                    for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
-                        const int s = sidx % a.NS;
-                        rc.wait_on(empty0 + 8 * s, (uint32_t)(((sidx / a.NS) & 1) ^ 1));
-                        mbar_arrive_tx(full0 + 8 * s, bstage);
+                    for (int ks = 0; ks < a.nks; ++ks) {
+                        rc.wait_idle(bempty0 + 8 * s, ph ^ 1u);
+                        mbar_arrive_tx(bfull0 + 8 * s, bstage);
                         bulk_g2s(b_base + s * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bstage,
-                                 full0 + 8 * s);
+                                 bfull0 + 8 * s);
+                        if (++s == a.NS) s = 0, ph ^= 1u;
                     }
                 }
             }
             rc.store(3);
         }
         __syncwarp();
-    } else {
+    } else if (warp < kFlushWarp) {
         // ======================= input band loaders =======================
         RoleClock rc(a.prof != 0);
-        const int lt = threadIdx.x - (kThreads - kLoaders);  // 0..63
+        const int lt = threadIdx.x - (kMmaWarp + 2) * 32;  // 0..63
         const size_t plane = (size_t)g.Hi * g.Wi;
         TileIter ti;
         ti.init(a);
-        int rcount = 0;
+        int rb = 0;
+        uint32_t rph = 0;
         bool need_region = true;
         for (; ti.valid(); ti.next(a)) {
             const bool load = need_region;
             need_region = ti.region_ends(a);
             if (!load) continue;  // same staged region as the previous tile
-            const int rb = rcount % a.nrb;
             uint8_t* dst = RG + rb * a.rb_stride;
-            rc.wait_warp(rge0 + 8 * rb, (uint32_t)(((rcount / a.nrb) & 1) ^ 1));
-            ++rcount;
+            rc.wait_warp_idle(rge0 + 8 * rb, rph ^ 1u);
             // region[c][r][x] = min(lat[b][c][pr0 + r - Ph][x - Pw], 0x7F), 0x7F (never) in the halo
             const uint8_t* src = a.lat_in + (size_t)ti.b * g.Ci * plane;
             const int total = g.Ci * a.band;
@@ -725,8 +790,47 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (lt < 16) dst[total + lt] = 0x7F;  // sentinel block for padding synapses
             __syncwarp();
             if (lane == 0) mbar_arrive(rgf0 + 8 * rb);
+            if (++rb == a.nrb) rb = 0, rph ^= 1u;
         }
         if (lt == 0) rc.store(4);
+    }
+
+    if (warp == kFlushWarp && EPI != SPK_EPI_POTENTIAL) {
+        // ======================= flusher: staged tile -> one run of PPT pixels per output map
+        const uint8_t* ob_lat = smem + a.ob_off;
+        const float* ob_ps = reinterpret_cast<const float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
+        TileIter ti;
+        ti.init(a);
+        int ob = 0;
+        uint32_t ph = 0;
+        for (; ti.valid(); ti.next(a)) {
+            if (lane == 0) mbar_wait_idle(stg0 + 8 * ob, ph);
+            __syncwarp();
+            const int b = ti.b, nt = ti.nt, p0 = ti.j * PPT;
+            const uint8_t* sl = ob_lat + ob * a.Nt * PPT;
+            const float* sp = ob_ps + ob * a.Nt * PPT;
+            const int npix = min(PPT, a.HWo - p0);
+            for (int ol = lane; ol < a.Nt; ol += 32) {
+                const int o = nt * a.Nt + ol;
+                if (o >= g.Co || (SPK_EXP & 8)) continue;
+                const size_t oi = ((size_t)b * g.Co + o) * a.HWo + p0;
+                uint8_t* dl = static_cast<uint8_t*>(a.out0) + oi;
+                if (npix == PPT && PPT == 8 && (reinterpret_cast<uintptr_t>(dl) & 7) == 0) {
+                    *reinterpret_cast<uint2*>(dl) = *reinterpret_cast<const uint2*>(sl + ol * PPT);
+                } else if (npix == PPT && PPT == 4 && (reinterpret_cast<uintptr_t>(dl) & 3) == 0) {
+                    *reinterpret_cast<uint32_t*>(dl) = *reinterpret_cast<const uint32_t*>(sl + ol * PPT);
+                } else {
+                    for (int q = 0; q < npix; ++q) dl[q] = sl[ol * PPT + q];
+                }
+                if (PSTAR) {
+                    float* dp = a.out1 + oi;
+                    for (int q = 0; q < npix; ++q) dp[q] = sp[ol * PPT + q];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(fls0 + 8 * ob);
+            if (++ob == kNOB) ob = 0, ph ^= 1u;
+        }
     }
 
     tc_fence_before();
@@ -810,7 +914,12 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     p.PPT = 128 / p.TP;
     // N tiling: accumulators (3 digit planes) + the TMEM A stages share 512 columns
     const int acc_cols = kACol0;  // 384
-    if (g.Co <= 64) {
+    // a reduction that fits the TMEM A ring is produced once per M tile and kept for every
+    // N tile; N tiles of 64 then give two accumulator buffers (epilogue overlaps the MMAs)
+    p.retain = (p.nks <= S && g.Co > 64) ? 1 : 0;
+    if (p.retain) {
+        p.Nt = 64;
+    } else if (g.Co <= 64) {
         p.Nt = ((g.Co + 15) / 16) * 16;
     } else {
         const int nn = (g.Co + 127) / 128;
@@ -842,7 +951,7 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     p.packed_bytes = (size_t)p.n_ntiles * p.nks * 3 * p.Nt * KS;
     p.ws_bytes = 256 + p.packed_bytes;
     const size_t bstage = (size_t)3 * p.Nt * KS, lc = 8 * 4 * (KS / 2), kt = 4 * (size_t)p.nks * KS;
-    const size_t ob = 2 * (size_t)p.Nt * p.PPT * 5;  // output staging (lat + P*), double-buffered
+    const size_t ob = (size_t)kNOB * p.Nt * p.PPT * 5;  // output staging ring (lat + P*)
     const size_t region = ((size_t)g.Ci * p.band + 16 + 15) & ~(size_t)15;  // + sentinel block
     const size_t cap = 227 * 1024;
     if ((size_t)g.Ci * p.band >= (1u << 24)) return false;
@@ -905,6 +1014,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.bres = p.bres;
     a.stack = p.stack;
     a.NS = p.NS;
+    a.retain = p.retain;
     a.total_tiles = p.total_tiles;
     // fire iff X * s 2^-23 > theta  <=>  X > floor(theta 2^23 / s)   (X integer, scaling exact)
     // spikes enter the MMA as 128: X is in units of s 2^-30
@@ -921,7 +1031,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.kt_off = a.lc_off + 8u * 4u * (KS / 2);
     a.rg_off = (a.kt_off + (uint32_t)(4 * p.nks * KS) + 15u) & ~15u;
     a.ob_off = (a.rg_off + (uint32_t)(p.nrb * p.rb_stride) + 15u) & ~15u;
-    a.bar_off = (a.ob_off + (uint32_t)(2 * p.Nt * p.PPT * 5) + 15u) & ~15u;
+    a.bar_off = (a.ob_off + (uint32_t)(kNOB * p.Nt * p.PPT * 5) + 15u) & ~15u;
     const long long grid = p.total_tiles < sm_count() ? p.total_tiles : sm_count();
     if (p.TP == 16) launch_tp<16>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
     else launch_tp<32>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
