@@ -31,42 +31,59 @@ void unit_gaussian(double sigma, int r, std::vector<double>& g) {
 }
 
 // Filter tile: 32 x 8 outputs of one (b, ci) plane, all K kernels per output pixel.
+// The (2R+1)^2 window of a pixel is read from the staged tile into registers once
+// and reused by every kernel.  Taps outside the image read a staged 0: the oracle
+// skips them, and fmaf(k, 0, acc) == acc exactly because acc starts at +0 and can
+// never become -0 (R-FILTER-ORDER), so the fmaf chain — same tap order — is
+// bit-identical.
 constexpr int TX = 32, TY = 8;
 
-__global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restrict__ img, int C, int H,
-                                                       int W, int K, int r, int pad, int Ho, int Wo,
-                                                       float* __restrict__ out, const FilterCoef coef) {
-    extern __shared__ float tile[];  // (TY + 2r) x (TX + 2r)
-    const int e = 2 * r + 1;
-    const int tw = TX + 2 * r, th = TY + 2 * r;
+template <int R>
+__global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
+                                                       int K, int pad, int Ho, int Wo, float* __restrict__ out,
+                                                       const FilterCoef coef) {
+    constexpr int E = 2 * R + 1, TW = TX + 2 * R, TH = TY + 2 * R;
+    __shared__ float tile[TH][TW];
     const int bc = blockIdx.z;  // b * C + ci
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const uint8_t* plane = img + (size_t)bc * H * W;
-    // stage the input tile: pixel value u8 / 255 (R-SCALE), outside the image -> 0 (never used)
-    for (int q = threadIdx.y * TX + threadIdx.x; q < tw * th; q += TX * TY) {
-        const int ty = q / tw, tx = q % tw;
-        const int iy = y0 - pad + ty, ix = x0 - pad + tx;
-        float v = 0.0f;
-        if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = __fdiv_rn((float)plane[(size_t)iy * W + ix], 255.0f);
-        tile[q] = v;
+    // stage the input tile: pixel value u8 / 255 (R-SCALE), outside the image -> 0
+    for (int ty = threadIdx.y; ty < TH; ty += TY) {
+        const int iy = y0 - pad + ty;
+        for (int tx = threadIdx.x; tx < TW; tx += TX) {
+            const int ix = x0 - pad + tx;
+            float v = 0.0f;
+            if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = __fdiv_rn((float)__ldg(plane + (size_t)iy * W + ix), 255.0f);
+            tile[ty][tx] = v;
+        }
     }
     __syncthreads();
     const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     if (x >= Wo || y >= Ho) return;
-    const int b = bc / C, ci = bc % C;
-    for (int k = 0; k < K; ++k) {
-        const float* kc = coef.c + k * e * e;
-        float acc = 0.0f;
-        for (int i = 0; i < e; ++i) {
-            const int iy = y - pad + i;
-            if (iy < 0 || iy >= H) continue;  // taps outside the image are skipped (R-FILTER-ORDER)
-            for (int j = 0; j < e; ++j) {
-                const int ix = x - pad + j;
-                if (ix < 0 || ix >= W) continue;
-                acc = __fmaf_rn(kc[i * e + j], tile[(threadIdx.y + i) * tw + threadIdx.x + j], acc);
-            }
+    const int b = bc / C, ci = bc - b * C;
+    float* o = out + (((size_t)b * C + ci) * K * Ho + y) * Wo + x;
+    if constexpr (E * E <= 81) {  // window in registers, reused by all K kernels
+        float v[E * E];
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[i * E + j] = tile[threadIdx.y + i][threadIdx.x + j];
+        for (int k = 0; k < K; ++k) {
+            const float* kc = coef.c + k * E * E;
+            float acc = 0.0f;
+#pragma unroll
+            for (int q = 0; q < E * E; ++q) acc = __fmaf_rn(kc[q], v[q], acc);
+            o[(size_t)k * Ho * Wo] = acc;
         }
-        out[(((size_t)b * C * K + (size_t)ci * K + k) * Ho + y) * Wo + x] = acc;
+    } else {  // large windows: read the tile per kernel
+        for (int k = 0; k < K; ++k) {
+            const float* kc = coef.c + k * E * E;
+            float acc = 0.0f;
+            for (int i = 0; i < E; ++i)
+#pragma unroll
+                for (int j = 0; j < E; ++j) acc = __fmaf_rn(kc[i * E + j], tile[threadIdx.y + i][threadIdx.x + j], acc);
+            o[(size_t)k * Ho * Wo] = acc;
+        }
     }
 }
 
@@ -79,10 +96,19 @@ spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std:
     FilterCoef fc;
     for (size_t q = 0; q < coef.size(); ++q) fc.c[q] = coef[q];
     dim3 grid(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY), (unsigned)(B * C));
-    SPK_CHECK(grid.z <= 65535u * 1024u, SPK_ERR_SHAPE, "B*C too large");
-    const size_t smem = sizeof(float) * (TX + 2 * radius) * (TY + 2 * radius);
-    filter_kernel<<<grid, dim3(TX, TY), smem, spk::as_cuda(stream)>>>(img, C, H, W, K, radius, pad, Ho,
-                                                                      Wo, y, fc);
+    SPK_CHECK(grid.z <= 65535u, SPK_ERR_SHAPE, "B*C=%d > 65535", B * C);
+    cudaStream_t s = spk::as_cuda(stream);
+    const dim3 blk(TX, TY);
+    switch (radius) {
+        case 0: filter_kernel<0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 1: filter_kernel<1><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 2: filter_kernel<2><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 3: filter_kernel<3><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 4: filter_kernel<4><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 5: filter_kernel<5><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 6: filter_kernel<6><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        default: filter_kernel<7><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+    }
     return spk::launched("filter_kernel");
 }
 

@@ -55,34 +55,38 @@ __global__ void pool_kernel(const uint8_t* __restrict__ lat, int BC, int H, int 
 }
 
 // ---------------------------------------------------------------- inhibit
-// One thread per (b, y, x): argmin over channels of (lat asc, P* desc, c asc),
-// then every other firing channel is set to never.  Channel planes are H*W
-// apart, so a warp touches 32 consecutive pixels of one plane per load.
-__global__ void inhibit_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar, int B, int C,
-                               size_t HW, int T) {
-    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= (size_t)B * HW) return;
-    const size_t b = q / HW, p = q % HW;
-    uint8_t* L = lat + b * C * HW + p;
-    float* P = pstar + b * C * HW + p;
-    int best = -1, bl = T;
-    float bp = 0.0f;
-    for (int c = 0; c < C; ++c) {
-        const int l = L[(size_t)c * HW];
+// One CTA per (sample, chunk of <= kInhPix pixels); threads stride over the
+// chunk's (channel, pixel) cells so that a sample with few pixels and many maps
+// still fills the CTA.  Pass 1: per pixel, shared-memory atomicMin of the unique
+// key (lat asc, P* desc, c asc) over firing cells; pass 2: every other firing
+// cell of the pixel is set to never.
+constexpr int kInhPix = 256;
+
+__global__ void __launch_bounds__(kT) inhibit_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar, int C,
+                                                     int HW, int T) {
+    __shared__ unsigned long long best[kInhPix];
+    const int b = blockIdx.y, p0 = blockIdx.x * kInhPix;
+    const int np = min(kInhPix, HW - p0);
+    uint8_t* L = lat + (size_t)b * C * HW + p0;
+    float* P = pstar + (size_t)b * C * HW + p0;
+    for (int q = threadIdx.x; q < np; q += kT) best[q] = ~0ull;
+    __syncthreads();
+    const int n = C * np;
+    for (int e = threadIdx.x; e < n; e += kT) {
+        const int c = e / np, pl = e - c * np;
+        const int l = L[(size_t)c * HW + pl];
         if (l >= T) continue;
-        const float ps = P[(size_t)c * HW];
-        if (best < 0 || l < bl || (l == bl && ps > bp)) {
-            best = c;
-            bl = l;
-            bp = ps;
-        }
+        const float ps = P[(size_t)c * HW + pl] + 0.0f;  // -0 -> +0: equal potentials tie on c
+        const uint32_t pd = ~spk_float_order_u32(ps);        // larger P* -> smaller key
+        atomicMin(&best[pl], ((unsigned long long)l << 56) | ((unsigned long long)pd << 24) | (unsigned)c);
     }
-    if (best < 0) return;
-    for (int c = 0; c < C; ++c) {
-        if (c == best) continue;
-        if (L[(size_t)c * HW] < T) {
-            L[(size_t)c * HW] = (uint8_t)T;
-            P[(size_t)c * HW] = 0.0f;
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += kT) {
+        const int c = e / np, pl = e - c * np;
+        const size_t o = (size_t)c * HW + pl;
+        if (L[o] < T && (unsigned)c != (unsigned)(best[pl] & 0xFFFFFFu)) {
+            L[o] = (uint8_t)T;
+            P[o] = 0.0f;
         }
     }
 }
@@ -173,8 +177,12 @@ extern "C" spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int 
     SPK_CHECK_PTR(pstar);
     SPK_CHECK(B >= 1 && C >= 1 && H >= 1 && W >= 1, SPK_ERR_SHAPE, "non-positive size");
     SPK_CHECK(T >= 1 && T <= 254, SPK_ERR_UNSUPPORTED, "T=%d outside 1..254", T);
-    const size_t HW = (size_t)H * W;
-    inhibit_kernel<<<spk::ceil_div((size_t)B * HW, kT), kT, 0, spk::as_cuda(stream)>>>(lat, pstar, B, C, HW, T);
+    SPK_CHECK(C < (1 << 24), SPK_ERR_UNSUPPORTED, "C=%d >= 2^24", C);
+    SPK_CHECK((long long)H * W < (1ll << 31) && (long long)C * kInhPix < (1ll << 31), SPK_ERR_SHAPE, "map too large");
+    SPK_CHECK(B <= 65535, SPK_ERR_SHAPE, "B=%d > 65535", B);
+    const int HW = H * W;
+    const dim3 grid(spk::ceil_div((size_t)HW, kInhPix), (unsigned)B);
+    inhibit_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
     return spk::launched("inhibit_kernel");
 }
 

@@ -199,6 +199,59 @@ __global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __rest
     }
 }
 
+// Small samples (N <= kSortMax), sort mode: the unique keys of the positive values
+// are compacted into shared memory and bitonic-sorted descending; the value at
+// sorted position r gets bin floor(r T / n) (R-BINS) — the same ranks as the
+// radix select, with far fewer passes over shared memory.
+constexpr int kSortMax = 8192, kSortThreads = 512;
+
+__global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const float* __restrict__ y, int N, int T,
+                                                                      float thresh, uint8_t* __restrict__ lat) {
+    extern __shared__ unsigned long long keys[];  // capacity: next power of two >= N
+    __shared__ unsigned int s_n;
+    const float* ys = y + (size_t)blockIdx.x * N;
+    uint8_t* out = lat + (size_t)blockIdx.x * N;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    // compaction (order irrelevant: keys are unique); non-positive values never fire
+    for (int i0 = 0; i0 < N; i0 += kSortThreads) {
+        const int i = i0 + threadIdx.x;
+        const unsigned int u = i < N ? thr_bits(__ldg(ys + i), thresh) : 0u;
+        const unsigned int m = __ballot_sync(0xffffffffu, u != 0u);
+        unsigned int base = 0;
+        if (lane == 0 && m) base = atomicAdd(&s_n, (unsigned)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (u) keys[base + __popc(m & ((1u << lane) - 1u))] = ((unsigned long long)u << 32) | (0xffffffffu - (unsigned)i);
+        else if (i < N) out[i] = (uint8_t)T;
+    }
+    __syncthreads();
+    const int n = (int)s_n;
+    if (n == 0) return;
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int q = n + threadIdx.x; q < P; q += kSortThreads) keys[q] = 0ull;  // sorts last
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < (P >> 1); t += kSortThreads) {
+                const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1)), b = a + j;
+                const unsigned long long ka = keys[a], kb = keys[b];
+                const bool desc = (a & k) == 0;
+                if ((ka < kb) == desc) {
+                    keys[a] = kb;
+                    keys[b] = ka;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int r = threadIdx.x; r < n; r += kSortThreads) {
+        const unsigned int idx = 0xffffffffu - (unsigned int)(keys[r] & 0xffffffffull);
+        out[idx] = (uint8_t)(((long long)r * T) / n);
+    }
+}
+
 }  // namespace
 
 extern "C" size_t spk_rank_code_workspace(int, int, int, int) { return 0; }
@@ -216,6 +269,19 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
     SPK_CHECK(T <= 254, SPK_ERR_UNSUPPORTED, "T=%d > 254 (u8 latency)", T);
     SPK_CHECK(B <= 0x7fffffff, SPK_ERR_SHAPE, "B too large");
     cudaStream_t s = spk::as_cuda(stream);
+    if (sort && N <= kSortMax) {
+        int cap = 1;
+        while (cap < N) cap <<= 1;
+        const size_t smem = sizeof(unsigned long long) * (size_t)cap;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(rank_code_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(unsigned long long) * kSortMax));
+            attr = true;
+        }
+        rank_code_sort_kernel<<<B, kSortThreads, smem, s>>>(y, N, T, thresh, lat);
+        return spk::launched("rank_code_sort_kernel");
+    }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
         const size_t smem = sizeof(unsigned int) * (size_t)N;
         rank_code_kernel<true, 256><<<B, 256, smem, s>>>(y, N, T, thresh, sort, lat);

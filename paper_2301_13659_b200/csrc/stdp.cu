@@ -55,38 +55,72 @@ __global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const spk_w
     if (threadIdx.x == kBucketThreads - 1) cnt[o] = min(scan[kBucketThreads - 1], cap);
 }
 
-__global__ void stdp_update_kernel(float* __restrict__ w, spk_conv_geom g, const uint8_t* __restrict__ lat_in,
-                                   const spk_winner* __restrict__ win, const int32_t* __restrict__ list,
-                                   const int32_t* __restrict__ cnt, int cap, const Cfgs cfgs) {
+// Grid (K chunks of kUpdThreads, Co): the winners of map o are staged in shared
+// memory (decoded once per CTA), then each thread walks them in order for its
+// weight, with the pre-synaptic latencies of a group of winners loaded ahead.
+constexpr int kUpdThreads = 256, kWinChunk = 256, kAhead = 4;
+
+__global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restrict__ w, spk_conv_geom g,
+                                                                  const uint8_t* __restrict__ lat_in,
+                                                                  const spk_winner* __restrict__ win,
+                                                                  const int32_t* __restrict__ list,
+                                                                  const int32_t* __restrict__ cnt, int cap,
+                                                                  const Cfgs cfgs) {
+    __shared__ long long s_base[kWinChunk];  // lat_in offset of channel 0 of the winner's sample
+    __shared__ int s_y0[kWinChunk], s_x0[kWinChunk], s_t[kWinChunk], s_cfg[kWinChunk];
     const int K = g.Ci * g.Kh * g.Kw;
-    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= (size_t)g.Co * K) return;
-    const int o = (int)(q / K), kk = (int)(q % K);
-    const int c = kk / (g.Kh * g.Kw), r = kk % (g.Kh * g.Kw), i = r / g.Kw, j = r % g.Kw;
-    const size_t HW = (size_t)g.Hi * g.Wi;
-    float W = w[q];
+    const int o = blockIdx.y;
+    const int kk = blockIdx.x * kUpdThreads + threadIdx.x;
+    const bool valid = kk < K;
+    const int KhKw = g.Kh * g.Kw;
+    const int c = kk / KhKw, r = kk - c * KhKw, i = r / g.Kw, j = r - i * g.Kw;
+    const long long HW = (long long)g.Hi * g.Wi;
+    float W = valid ? w[(size_t)o * K + kk] : 0.0f;
     const int n = cnt[o];
-    for (int e = 0; e < n; ++e) {
-        const spk_winner wn = win[list[(size_t)o * cap + e]];
-        const int iy = wn.y * g.Sh - g.Ph + i, ix = wn.x * g.Sw - g.Pw + j;
-        int tj = 0x7fffffff;  // padded input: never fires (R-NEVER)
-        if (iy >= 0 && iy < g.Hi && ix >= 0 && ix < g.Wi)
-            tj = __ldg(lat_in + ((size_t)wn.b * g.Ci + c) * HW + (size_t)iy * g.Wi + ix);  // == T: never
-        const spk_stdp_config cf = cfgs.c[wn.cfg];
-        const float A = (tj <= wn.t) ? cf.a_plus : cf.a_minus;  // R-EQ4-TIE
-        float d;
-        if (cf.stabilize) {
-            const float s = __fmul_rn(__fsub_rn(W, cf.lower), __fsub_rn(cf.upper, W));  // (W-L)(U-W), Eq. 4
-            d = __fmul_rn(A, s);
-        } else {
-            d = A;  // Eq. 5
+    for (int e0 = 0; e0 < n; e0 += kWinChunk) {
+        const int m = min(kWinChunk, n - e0);
+        __syncthreads();
+        if (threadIdx.x < m) {
+            const spk_winner wn = win[list[(size_t)o * cap + e0 + threadIdx.x]];
+            s_base[threadIdx.x] = (long long)wn.b * g.Ci * HW;
+            s_y0[threadIdx.x] = wn.y * g.Sh - g.Ph;
+            s_x0[threadIdx.x] = wn.x * g.Sw - g.Pw;
+            s_t[threadIdx.x] = wn.t;
+            s_cfg[threadIdx.x] = wn.cfg;
         }
-        float nw = __fadd_rn(W, d);
-        if (nw > cf.upper) nw = cf.upper;  // Eq. 6 on W + dW (R-EQ6-CLAMP)
-        if (nw < cf.lower) nw = cf.lower;
-        W = nw;
+        __syncthreads();
+        if (!valid) continue;
+        for (int e = 0; e < m; e += kAhead) {
+            int tj[kAhead];
+#pragma unroll
+            for (int u = 0; u < kAhead; ++u) {  // loads first: independent of W
+                tj[u] = 0x7fffffff;               // padded input: never fires (R-NEVER)
+                if (e + u < m) {
+                    const int iy = s_y0[e + u] + i, ix = s_x0[e + u] + j;
+                    if (iy >= 0 && iy < g.Hi && ix >= 0 && ix < g.Wi)
+                        tj[u] = __ldg(lat_in + s_base[e + u] + c * HW + (long long)iy * g.Wi + ix);  // T: never
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kAhead; ++u) {
+                if (e + u >= m) break;
+                const spk_stdp_config cf = cfgs.c[s_cfg[e + u]];
+                const float A = (tj[u] <= s_t[e + u]) ? cf.a_plus : cf.a_minus;  // R-EQ4-TIE
+                float d;
+                if (cf.stabilize) {
+                    const float sw = __fmul_rn(__fsub_rn(W, cf.lower), __fsub_rn(cf.upper, W));  // (W-L)(U-W), Eq. 4
+                    d = __fmul_rn(A, sw);
+                } else {
+                    d = A;  // Eq. 5
+                }
+                float nw = __fadd_rn(W, d);
+                if (nw > cf.upper) nw = cf.upper;  // Eq. 6 on W + dW (R-EQ6-CLAMP)
+                if (nw < cf.lower) nw = cf.lower;
+                W = nw;
+            }
+        }
     }
-    w[q] = W;
+    if (valid) w[(size_t)o * K + kk] = W;
 }
 
 }  // namespace
@@ -128,7 +162,9 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     stdp_bucket_kernel<<<g->Co, kBucketThreads, 0, s>>>(win, nwin, g->B, k, ncfg, Ho, Wo, cap, list, cnt);
     spk_status st = spk::launched("stdp_bucket_kernel");
     if (st != SPK_OK) return st;
-    const size_t n = (size_t)g->Co * g->Ci * g->Kh * g->Kw;
-    stdp_update_kernel<<<spk::ceil_div(n, 256), 256, 0, s>>>(w, *g, lat_in, win, list, cnt, cap, cc);
+    const size_t K = (size_t)g->Ci * g->Kh * g->Kw;
+    SPK_CHECK(g->Co <= 65535, SPK_ERR_SHAPE, "Co=%d > 65535", g->Co);
+    const dim3 grid(spk::ceil_div(K, kUpdThreads), (unsigned)g->Co);
+    stdp_update_kernel<<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, cnt, cap, cc);
     return spk::launched("stdp_update_kernel");
 }
