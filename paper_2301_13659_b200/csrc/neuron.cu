@@ -2,6 +2,8 @@
 //   a4 spk_fire (IF on materialised potentials), a5 spk_pool (Eq. 3,
 //   P:L140-149), a6 spk_inhibit, a8 spk_rstdp_route (Eq. 7),
 //   a9 spk_gather and the dense <-> latency boundary conversions.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace {
@@ -33,25 +35,23 @@ __global__ void fire_kernel(const float* __restrict__ pot, int B, int T, size_t 
 
 // ---------------------------------------------------------------- pool
 // Per-step window max of cumulative trains == window min of latencies; padded
-// cells never fire.
-__global__ void pool_kernel(const uint8_t* __restrict__ lat, int BC, int H, int W, int T,
-                            spk_pool_geom g, int Ho, int Wo, uint8_t* __restrict__ out) {
-    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= (size_t)BC * Ho * Wo) return;
-    const int x = (int)(q % Wo), y = (int)((q / Wo) % Ho);
-    const size_t bc = q / ((size_t)Ho * Wo);
-    const uint8_t* p = lat + bc * H * W;
+// cells never fire.  Grid: x = chunks of one output plane, (y, z) = plane index
+// (32-bit index math inside a plane).
+__global__ void __launch_bounds__(kT) pool_kernel(const uint8_t* __restrict__ lat, long long BC, int ppy, int H, int W,
+                                                  int T, spk_pool_geom g, int Ho, int Wo, uint8_t* __restrict__ out) {
+    // blockIdx.y selects a slice of ppy planes; inside it all index math is 32-bit
+    const int plane_out = Ho * Wo;
+    const int q = blockIdx.x * kT + threadIdx.x;  // < ppy * plane_out <= 2^30
+    const long long bc = (long long)blockIdx.y * ppy + q / plane_out;
+    if (bc >= BC || q >= ppy * plane_out) return;
+    const int r = q % plane_out, y = r / Wo, x = r - y * Wo;
+    const int y0 = y * g.Sh - g.Ph, x0 = x * g.Sw - g.Pw;
+    const int i0 = max(0, -y0), i1 = min(g.Lh, H - y0), j0 = max(0, -x0), j1 = min(g.Lw, W - x0);
+    const uint8_t* p = lat + (size_t)bc * H * W + (long long)y0 * W + x0;
     int m = T;
-    for (int i = 0; i < g.Lh; ++i) {
-        const int iy = y * g.Sh - g.Ph + i;
-        if (iy < 0 || iy >= H) continue;
-        for (int j = 0; j < g.Lw; ++j) {
-            const int ix = x * g.Sw - g.Pw + j;
-            if (ix < 0 || ix >= W) continue;
-            m = min(m, (int)__ldg(p + (size_t)iy * W + ix));
-        }
-    }
-    out[q] = (uint8_t)min(m, T);
+    for (int i = i0; i < i1; ++i)
+        for (int j = j0; j < j1; ++j) m = min(m, (int)__ldg(p + (size_t)i * W + j));
+    out[(size_t)bc * plane_out + r] = (uint8_t)min(m, T);
 }
 
 // ---------------------------------------------------------------- inhibit
@@ -165,8 +165,15 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
     const int Ho = (H + 2 * p->Ph - p->Lh) / p->Sh + 1, Wo = (W + 2 * p->Pw - p->Lw) / p->Sw + 1;
     SPK_CHECK(H + 2 * p->Ph >= p->Lh && W + 2 * p->Pw >= p->Lw && Ho >= 1 && Wo >= 1, SPK_ERR_SHAPE,
               "pool window larger than padded input (Eq. 3)");
-    const size_t n = (size_t)B * C * Ho * Wo;
-    pool_kernel<<<spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream)>>>(lat, B * C, H, W, T, *p, Ho, Wo, out);
+    SPK_CHECK((long long)H * W < (1ll << 31), SPK_ERR_SHAPE, "input plane too large");
+    SPK_CHECK((long long)Ho * Wo <= (1 << 30), SPK_ERR_SHAPE, "output plane too large");
+    const long long BC = (long long)B * C;
+    const int plane_out = Ho * Wo;
+    const long long ppy = std::min<long long>(BC, std::max(1, (1 << 30) / plane_out));
+    const long long gy = (BC + ppy - 1) / ppy;
+    SPK_CHECK(gy <= 65535, SPK_ERR_SHAPE, "B*C too large");
+    const dim3 grid(spk::ceil_div((size_t)ppy * plane_out, kT), (unsigned)gy);
+    pool_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, *p, Ho, Wo, out);
     return spk::launched("pool_kernel");
 }
 

@@ -18,109 +18,165 @@ struct Cfgs {
     spk_stdp_config c[kMaxCfg];
 };
 
-constexpr int kBucketThreads = 256;
-
-// list[o][0..cnt[o]) = winner slot indices (b*k + q) of map o, in slot order.
-__global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const spk_winner* __restrict__ win,
-                                                                    const int32_t* __restrict__ nwin,
-                                                                    int B, int k, int ncfg, int Ho,
-                                                                    int Wo, int cap,
-                                                                    int32_t* __restrict__ list,
-                                                                    int32_t* __restrict__ cnt) {
-    __shared__ int scan[kBucketThreads];
-    const int o = blockIdx.x;
-    const int S = B * k;
-    const int chunk = (S + kBucketThreads - 1) / kBucketThreads;
-    const int s0 = threadIdx.x * chunk, s1 = min(S, s0 + chunk);
-    auto take = [&](int s) -> bool {
-        const int b = s / k, q = s % k;
-        if (q >= nwin[b]) return false;
-        const spk_winner w = win[s];
-        return w.c == o && w.cfg >= 0 && w.cfg < ncfg && w.y >= 0 && w.y < Ho && w.x >= 0 && w.x < Wo &&
-               w.b >= 0 && w.b < B;
-    };
-    int mine = 0;
-    for (int s = s0; s < s1; ++s) mine += take(s);
-    scan[threadIdx.x] = mine;
-    __syncthreads();
-    for (int off = 1; off < kBucketThreads; off <<= 1) {  // inclusive Hillis-Steele scan
-        const int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
-        __syncthreads();
-        scan[threadIdx.x] += v;
-        __syncthreads();
-    }
-    int pos = scan[threadIdx.x] - mine;
-    for (int s = s0; s < s1; ++s)
-        if (take(s) && pos < cap) list[(size_t)o * cap + pos++] = s;
-    if (threadIdx.x == kBucketThreads - 1) cnt[o] = min(scan[kBucketThreads - 1], cap);
+// Bucketing: slotmap[s] = map of winner slot s (b*k + q) if it is a valid winner,
+// else -1; then one CTA per map collects its slots in slot order with a single
+// block-wide exclusive scan per pass (each thread owns a contiguous run of slots).
+__device__ __forceinline__ bool winner_valid(const spk_winner& w, int B, int ncfg, int Ho, int Wo, int Co) {
+    return w.c >= 0 && w.c < Co && w.cfg >= 0 && w.cfg < ncfg && w.y >= 0 && w.y < Ho && w.x >= 0 && w.x < Wo &&
+           w.b >= 0 && w.b < B;
 }
 
-// Grid (K chunks of kUpdThreads, Co): the winners of map o are staged in shared
-// memory (decoded once per CTA), then each thread walks them in order for its
-// weight, with the pre-synaptic latencies of a group of winners loaded ahead.
-constexpr int kUpdThreads = 256, kWinChunk = 256, kAhead = 4;
+__global__ void stdp_slotmap_kernel(const spk_winner* __restrict__ win, const int32_t* __restrict__ nwin, int B,
+                                    int k, int ncfg, int Ho, int Wo, int Co, int32_t* __restrict__ slotmap) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= B * k) return;
+    const int b = s / k, q = s - b * k;
+    int m = -1;
+    if (q < nwin[b]) {
+        const spk_winner w = win[s];
+        if (winner_valid(w, B, ncfg, Ho, Wo, Co)) m = w.c;
+    }
+    slotmap[s] = m;
+}
+
+constexpr int kBucketThreads = 1024, kBucketRun = 16;  // slots per thread per pass
+
+__global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const int32_t* __restrict__ slotmap, int S,
+                                                                    int cap, int32_t* __restrict__ list,
+                                                                    int32_t* __restrict__ start,
+                                                                    int32_t* __restrict__ cnt) {
+    constexpr int kWarps = kBucketThreads / 32;
+    __shared__ int wsum[kWarps];
+    const int o = blockIdx.x;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    int total = 0;
+    for (int p0 = 0; p0 < S; p0 += kBucketThreads * kBucketRun) {
+        const int s0 = p0 + threadIdx.x * kBucketRun;
+        int v[kBucketRun];
+        int mine = 0;
+#pragma unroll
+        for (int u = 0; u < kBucketRun; ++u) {
+            v[u] = (s0 + u < S) ? slotmap[s0 + u] : -1;
+            mine += (v[u] == o);
+        }
+        // block exclusive scan of `mine`
+        int incl = mine;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) wsum[wp] = incl;
+        __syncthreads();
+        int before = 0, chunk = 0;
+        for (int q = 0; q < kWarps; ++q) {
+            const int x = wsum[q];
+            before += (q < wp) ? x : 0;
+            chunk += x;
+        }
+        int pos = total + before + incl - mine;
+#pragma unroll
+        for (int u = 0; u < kBucketRun; ++u)
+            if (v[u] == o) {
+                if (pos < cap) list[(size_t)o * cap + pos] = s0 + u;
+                ++pos;
+            }
+        total += chunk;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        cnt[o] = min(total, cap);
+        start[o] = o * cap;
+    }
+}
+
+// Grid (K chunks of kUpdW weights, Co).  Per chunk of up to kWinChunk winners of
+// map o (in order): phase 1 — all threads, one (winner, weight) pair each —
+// gathers the pre-synaptic latency and stores the Eq. 4 case (t_j <= t_i) as a
+// byte; phase 2 — one thread per weight — runs the sequential fp32 chain of
+// Eq. 4-6 from shared memory only.  The gathers are thus fully parallel and the
+// order-dependent part is a few dependent flops per winner.
+constexpr int kUpdW = 64, kUpdThreads = 256, kWinChunk = 256;
 
 __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restrict__ w, spk_conv_geom g,
                                                                   const uint8_t* __restrict__ lat_in,
                                                                   const spk_winner* __restrict__ win,
                                                                   const int32_t* __restrict__ list,
-                                                                  const int32_t* __restrict__ cnt, int cap,
-                                                                  const Cfgs cfgs) {
-    __shared__ long long s_base[kWinChunk];  // lat_in offset of channel 0 of the winner's sample
-    __shared__ int s_y0[kWinChunk], s_x0[kWinChunk], s_t[kWinChunk], s_cfg[kWinChunk];
-    const int K = g.Ci * g.Kh * g.Kw;
+                                                                  const int32_t* __restrict__ start,
+                                                                  const int32_t* __restrict__ cnt,
+                                                                  const Cfgs cfgs, int ncfg) {
+    __shared__ long long s_ofs[kWinChunk];  // lat_in offset of (b, channel 0, y0, x0)
+    __shared__ int s_y0[kWinChunk], s_x0[kWinChunk], s_t[kWinChunk];
+    __shared__ float s_ap[kWinChunk], s_am[kWinChunk], s_lo[kWinChunk], s_hi[kWinChunk];  // winner's config
+    __shared__ uint8_t s_st[kWinChunk];
+    __shared__ uint8_t s_le[kWinChunk][kUpdW];  // [winner][weight]: t_j <= t_i
+    __shared__ spk_stdp_config s_cf[kMaxCfg];
     const int o = blockIdx.y;
-    const int kk = blockIdx.x * kUpdThreads + threadIdx.x;
-    const bool valid = kk < K;
-    const int KhKw = g.Kh * g.Kw;
-    const int c = kk / KhKw, r = kk - c * KhKw, i = r / g.Kw, j = r - i * g.Kw;
-    const long long HW = (long long)g.Hi * g.Wi;
-    float W = valid ? w[(size_t)o * K + kk] : 0.0f;
     const int n = cnt[o];
+    if (n == 0) return;
+    const int K = g.Ci * g.Kh * g.Kw;
+    const int KhKw = g.Kh * g.Kw;
+    const long long HW = (long long)g.Hi * g.Wi;
+    const int k0 = blockIdx.x * kUpdW;
+    // phase-1 role: weight lane wl of this CTA's chunk (fixed per thread)
+    const int wl = threadIdx.x & (kUpdW - 1), e_lane = threadIdx.x / kUpdW;
+    const int kk1 = k0 + wl;
+    const bool valid1 = kk1 < K;
+    const int c1 = kk1 / KhKw, r1 = kk1 - c1 * KhKw, i1 = r1 / g.Kw, j1 = r1 - i1 * g.Kw;
+    const long long own1 = c1 * HW + (long long)i1 * g.Wi + j1;
+#pragma unroll
+    for (int q = 0; q < kMaxCfg; ++q)  // static indices: the parameter block stays in constant space
+        if (threadIdx.x == q && q < ncfg) s_cf[q] = cfgs.c[q];
+    // phase-2 role (threads < kUpdW): the weight kk2 = k0 + threadIdx.x
+    const int kk2 = k0 + threadIdx.x;
+    const bool valid2 = threadIdx.x < kUpdW && kk2 < K;
+    float W = valid2 ? w[(size_t)o * K + kk2] : 0.0f;
     for (int e0 = 0; e0 < n; e0 += kWinChunk) {
         const int m = min(kWinChunk, n - e0);
         __syncthreads();
-        if (threadIdx.x < m) {
-            const spk_winner wn = win[list[(size_t)o * cap + e0 + threadIdx.x]];
-            s_base[threadIdx.x] = (long long)wn.b * g.Ci * HW;
-            s_y0[threadIdx.x] = wn.y * g.Sh - g.Ph;
-            s_x0[threadIdx.x] = wn.x * g.Sw - g.Pw;
-            s_t[threadIdx.x] = wn.t;
-            s_cfg[threadIdx.x] = wn.cfg;
+        for (int q = threadIdx.x; q < m; q += kUpdThreads) {
+            const spk_winner wn = win[list[(size_t)start[o] + e0 + q]];
+            const int y0 = wn.y * g.Sh - g.Ph, x0 = wn.x * g.Sw - g.Pw;
+            s_ofs[q] = (long long)wn.b * g.Ci * HW + (long long)y0 * g.Wi + x0;
+            s_y0[q] = y0;
+            s_x0[q] = x0;
+            s_t[q] = wn.t;
+            const spk_stdp_config cf = s_cf[wn.cfg];
+            s_ap[q] = cf.a_plus;
+            s_am[q] = cf.a_minus;
+            s_lo[q] = cf.lower;
+            s_hi[q] = cf.upper;
+            s_st[q] = cf.stabilize != 0;
         }
         __syncthreads();
-        if (!valid) continue;
-        for (int e = 0; e < m; e += kAhead) {
-            int tj[kAhead];
-#pragma unroll
-            for (int u = 0; u < kAhead; ++u) {  // loads first: independent of W
-                tj[u] = 0x7fffffff;               // padded input: never fires (R-NEVER)
-                if (e + u < m) {
-                    const int iy = s_y0[e + u] + i, ix = s_x0[e + u] + j;
-                    if (iy >= 0 && iy < g.Hi && ix >= 0 && ix < g.Wi)
-                        tj[u] = __ldg(lat_in + s_base[e + u] + c * HW + (long long)iy * g.Wi + ix);  // T: never
-                }
+        // phase 1: gathers, kUpdThreads / kUpdW winners per pass, several passes in flight
+        if (valid1) {
+            constexpr int kStep = kUpdThreads / kUpdW;
+#pragma unroll 4
+            for (int e = e_lane; e < m; e += kStep) {
+                int tj = 0x7fffffff;  // padded input: never fires (R-NEVER)
+                const int iy = s_y0[e] + i1, ix = s_x0[e] + j1;
+                if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
+                    tj = __ldg(lat_in + s_ofs[e] + own1);  // == T: never
+                s_le[e][wl] = (uint8_t)(tj <= s_t[e]);     // R-EQ4-TIE
             }
-#pragma unroll
-            for (int u = 0; u < kAhead; ++u) {
-                if (e + u >= m) break;
-                const spk_stdp_config cf = cfgs.c[s_cfg[e + u]];
-                const float A = (tj[u] <= s_t[e + u]) ? cf.a_plus : cf.a_minus;  // R-EQ4-TIE
-                float d;
-                if (cf.stabilize) {
-                    const float sw = __fmul_rn(__fsub_rn(W, cf.lower), __fsub_rn(cf.upper, W));  // (W-L)(U-W), Eq. 4
-                    d = __fmul_rn(A, sw);
-                } else {
-                    d = A;  // Eq. 5
-                }
+        }
+        __syncthreads();
+        // phase 2: the ordered chain
+        if (valid2) {
+#pragma unroll 8
+            for (int e = 0; e < m; ++e) {
+                const float A = s_le[e][threadIdx.x] ? s_ap[e] : s_am[e];
+                const float lo = s_lo[e], hi = s_hi[e];
+                // (W-L)(U-W) soft bound, Eq. 4; plain A, Eq. 5
+                const float d = s_st[e] ? __fmul_rn(A, __fmul_rn(__fsub_rn(W, lo), __fsub_rn(hi, W))) : A;
                 float nw = __fadd_rn(W, d);
-                if (nw > cf.upper) nw = cf.upper;  // Eq. 6 on W + dW (R-EQ6-CLAMP)
-                if (nw < cf.lower) nw = cf.lower;
+                if (nw > hi) nw = hi;  // Eq. 6 on W + dW (R-EQ6-CLAMP)
+                if (nw < lo) nw = lo;
                 W = nw;
             }
         }
     }
-    if (valid) w[(size_t)o * K + kk] = W;
+    if (valid2) w[(size_t)o * K + kk2] = W;
 }
 
 }  // namespace
@@ -128,7 +184,7 @@ __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restr
 extern "C" size_t spk_stdp_workspace(const spk_conv_geom* g, int k) {
     if (!g || g->Co < 1 || g->B < 1 || k < 1) return 0;
     const size_t cap = (size_t)g->B * (size_t)k;
-    return sizeof(int32_t) * ((size_t)g->Co * cap + (size_t)g->Co) + 256;
+    return sizeof(int32_t) * ((size_t)g->Co * cap + 2 * (size_t)g->Co + cap) + 256;
 }
 
 extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* lat_in, const spk_winner* win,
@@ -157,14 +213,20 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     const int Ho = (g->Hi + 2 * g->Ph - g->Kh) / g->Sh + 1, Wo = (g->Wi + 2 * g->Pw - g->Kw) / g->Sw + 1;
     const int cap = g->B * k;
     int32_t* list = static_cast<int32_t*>(ws);
-    int32_t* cnt = list + (size_t)g->Co * cap;
+    int32_t* start = list + (size_t)g->Co * cap;
+    int32_t* cnt = start + g->Co;
+    int32_t* slotmap = cnt + g->Co;
     cudaStream_t s = spk::as_cuda(stream);
-    stdp_bucket_kernel<<<g->Co, kBucketThreads, 0, s>>>(win, nwin, g->B, k, ncfg, Ho, Wo, cap, list, cnt);
-    spk_status st = spk::launched("stdp_bucket_kernel");
+    stdp_slotmap_kernel<<<spk::ceil_div((size_t)cap, 256), 256, 0, s>>>(win, nwin, g->B, k, ncfg, Ho, Wo, g->Co,
+                                                                      slotmap);
+    spk_status st = spk::launched("stdp_slotmap_kernel");
+    if (st != SPK_OK) return st;
+    stdp_bucket_kernel<<<g->Co, kBucketThreads, 0, s>>>(slotmap, cap, cap, list, start, cnt);
+    st = spk::launched("stdp_bucket_kernel");
     if (st != SPK_OK) return st;
     const size_t K = (size_t)g->Ci * g->Kh * g->Kw;
     SPK_CHECK(g->Co <= 65535, SPK_ERR_SHAPE, "Co=%d > 65535", g->Co);
-    const dim3 grid(spk::ceil_div(K, kUpdThreads), (unsigned)g->Co);
-    stdp_update_kernel<<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, cnt, cap, cc);
+    const dim3 grid(spk::ceil_div(K, kUpdW), (unsigned)g->Co);
+    stdp_update_kernel<<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
     return spk::launched("stdp_update_kernel");
 }
