@@ -114,6 +114,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 #ifndef SPK_IDLE_NS
 #define SPK_IDLE_NS 256
 #endif
+// A warp group waiting for one event: a single leader thread polls, the others
+// sleep in a named hardware barrier (no issue slots spent on polling).
+template <int ID, int NTHREADS>
+__device__ __forceinline__ void group_wait(uint32_t a, uint32_t parity, bool leader) {
+    if (leader) mbar_wait(a, parity);
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NTHREADS) : "memory");
+}
+// named barrier ids (0 is __syncthreads)
+constexpr int kBarProd = 1, kBarEpi = 2, kBarBand = 3;
 // waits of roles with slack (epilogue, loaders, flusher) back off between polls so that
 // their spinning does not take issue slots from the producers on the same scheduler
 __device__ __forceinline__ void mbar_wait_idle(uint32_t a, uint32_t parity) {
@@ -413,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (rc.on) pt[7] += tt0 - tprev;
             if (need_region) {
                 rb = rbn;
-                rc.wait_warp(rgf0 + 8 * rb, rgph);
+                group_wait<kBarProd, kProdWarps * 32>(rgf0 + 8 * rb, rgph, threadIdx.x == 0);
                 if (++rbn == a.nrb) rbn = 0, rgph ^= 1u;
             }
             const long long tt1 = rc.on ? clock64() : 0;
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 }
                 long long q3 = rc.on ? clock64() : 0;
                 // wait for the MMAs that last read this TMEM A stage, then overwrite it
-                rc.wait_warp(empty0 + 8 * s, ph ^ 1u);
+                group_wait<kBarProd, kProdWarps * 32>(empty0 + 8 * s, ph ^ 1u, threadIdx.x == 0);
                 long long q4 = rc.on ? clock64() : 0;
                 tc_fence_after();
 #if !(SPK_EXP & 4)
@@ -536,8 +545,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const int b = ti.b, nt = ti.nt;
             const int p0 = ti.j * PPT;
             const bool rvalid = p0 + pix < a.HWo && t < g.T;
-            if (EPI != SPK_EPI_POTENTIAL) rc.wait_warp_idle(fls0 + 8 * ob, ob_ph ^ 1u);
-            rc.wait_warp_idle(accf0 + 8 * buf, acc_ph);
+            // padded rows never fire: fold the row mask into the threshold
+            const long long thq = rvalid ? a.theta_q : 0x7fffffffffffffffll;
+            if (threadIdx.x == kProdWarps * 32 && EPI != SPK_EPI_POTENTIAL) mbar_wait(fls0 + 8 * ob, ob_ph ^ 1u);
+            group_wait<kBarEpi, kEpiWarps * 32>(accf0 + 8 * buf, acc_ph, threadIdx.x == kProdWarps * 32);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
             for (int n0 = eh * 16; n0 < a.Nt; n0 += 32) {
@@ -567,9 +578,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     float mine_ps = 0.0f;
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
-                        const long long X =
-                            (long long)(int)d2[jj] * 65536ll + ((long long)(int)d1[jj] * 256ll + (long long)(int)d0[jj]);
-                        const unsigned bal = __ballot_sync(0xffffffffu, rvalid && X > a.theta_q);
+                        // digit accumulators are >= 0 (u8 x u8): two wide multiply-adds
+                        const long long X = (long long)((unsigned long long)d2[jj] * 65536ull +
+                                                        ((unsigned long long)d1[jj] * 256ull + d0[jj]));
+                        const unsigned bal = __ballot_sync(0xffffffffu, X > thq);
                         if (jj == own_col) mine = bal;
                         if (PSTAR) {
                             const unsigned bits = (bal >> segbase) & segmask;
@@ -719,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             need_region = ti.region_ends(a);
             if (!load) continue;  // same staged region as the previous tile
             uint8_t* dst = RG + rb * a.rb_stride;
-            rc.wait_warp_idle(rge0 + 8 * rb, rph ^ 1u);
+            group_wait<kBarBand, kLoaders>(rge0 + 8 * rb, rph ^ 1u, lt == 0);
             // region[c][r][x] = min(lat[b][c][pr0 + r - Ph][x - Pw], 0x7F), 0x7F (never) in the halo
             const uint8_t* src = a.lat_in + (size_t)ti.b * g.Ci * plane;
             const int total = g.Ci * a.band;
