@@ -64,11 +64,24 @@ constexpr int kThreads = (kFlushWarp + 1) * 32;   // 672
 constexpr int kNOB = 4;                            // output staging ring (tiles)
 constexpr int kLoadBatch = 8;      // independent loads in flight per band-loader thread
 constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-bit column)
-constexpr int kACol0 = 512 - S * kACols;  // first TMEM column of the A stages
+constexpr int kMaxA = 8;           // TMEM A ring slots (<= 8; the rest of the 512 columns hold accumulators)
 
 // Optional per-role cycle accounting (SPK_CONV_PROF=1): [block][role][total, wait]
 constexpr int kProfRoles = 17;  // producer, epilogue, mma, b-loader, band-loader, mma:fence/issue/commit, producer sections x6
 __device__ unsigned long long g_conv_prof[1024][kProfRoles][2];
+#ifdef SPK_CONV_TRACE
+// event timestamps of CTA 0's first kTrace tiles (debug aid)
+constexpr int kTrace = 256;
+__device__ long long g_trace[8][kTrace];
+#define TRACE(ev, it)                                                        \
+    do {                                                                     \
+        if (blockIdx.x == 0 && (it) < kTrace) g_trace[ev][(it)] = clock64(); \
+    } while (0)
+#else
+#define TRACE(ev, it) \
+    do {              \
+    } while (0)
+#endif
 
 struct TcArgs {
     const uint8_t* lat_in;
@@ -77,7 +90,8 @@ struct TcArgs {
     float* out1;
     spk_conv_geom g;
     int Ho, Wo, HWo, K, nks, Nt, n_ntiles, NB, tps, NR, band, nrb, rb_stride, bres, stack, NS;
-    int retain;  // the A stages of an M tile stay in TMEM for all its N tiles (nks <= S)
+    int retain;  // the A stages of an M tile stay in TMEM for all its N tiles (nks <= NA)
+    int NA, aCol0;  // TMEM A ring: NA slots of kACols columns from column aCol0 = 512 - NA * kACols
     int WiP, HiP;  // padded input width/height: the staged region includes the zero-padding halo
     long long total_tiles;
     long long theta_q;  // fire iff X > theta_q
@@ -98,12 +112,21 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t a, uint32_t bytes) {
     asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(a), "r"(bytes)
                  : "memory");
 }
+#ifndef SPK_WAIT_TEST
+#define SPK_WAIT_TEST 0  // 1: poll with mbarrier.test_wait (never suspends) instead of try_wait
+#endif
 __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
     uint32_t ok;
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok)
-                 : "r"(a), "r"(parity)
-                 : "memory");
+    if (SPK_WAIT_TEST)
+        asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+    else
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
     return ok != 0;
 }
 // critical-path waits (producers, MMA issuer) poll
@@ -114,6 +137,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
 #ifndef SPK_IDLE_NS
 #define SPK_IDLE_NS 256
 #endif
+// Wait on up to three barriers with their first probes in flight together (an mbarrier
+// probe costs ~120 cycles of latency even when the phase is already complete).
+__device__ __forceinline__ void mbar_wait3(uint32_t a0, uint32_t p0, bool w0, uint32_t a1, uint32_t p1, bool w1,
+                                           uint32_t a2 = 0, uint32_t p2 = 0, bool w2 = false) {
+    bool d0 = !w0 || mbar_try(a0, p0);
+    bool d1 = !w1 || mbar_try(a1, p1);
+    bool d2 = !w2 || mbar_try(a2, p2);
+    while (!d0) d0 = mbar_try(a0, p0);
+    while (!d1) d1 = mbar_try(a1, p1);
+    while (!d2) d2 = mbar_try(a2, p2);
+}
 // A warp group waiting for one event: a single leader thread polls, the others
 // sleep in a named hardware barrier (no issue slots spent on polling).
 template <int ID, int NTHREADS>
@@ -292,6 +326,19 @@ struct RoleClock {
         if ((threadIdx.x & 31) == 0) wait_idle(bar, parity);
         __syncwarp();
     }
+    __device__ __forceinline__ void wait3(uint32_t a0, uint32_t p0, bool w0_, uint32_t a1, uint32_t p1, bool w1,
+                                          uint32_t a2 = 0, uint32_t p2 = 0, bool w2 = false) {
+        const long long w0 = on ? clock64() : 0;
+        mbar_wait3(a0, p0, w0_, a1, p1, w1, a2, p2, w2);
+        if (on) wait += clock64() - w0;
+    }
+    template <int ID, int N>
+    __device__ __forceinline__ void group_wait(uint32_t bar, uint32_t parity, bool leader) {
+        const long long w0 = on ? clock64() : 0;
+        if (leader) mbar_wait(bar, parity);
+        asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+        if (on) wait += clock64() - w0;
+    }
     __device__ void store(int role) {
         if (on && blockIdx.x < 1024) {
             g_conv_prof[blockIdx.x][role][0] = (unsigned long long)(clock64() - t0);
@@ -314,6 +361,15 @@ struct RoleClock {
         if ((threadIdx.x & 31) == 0) mbar_wait_idle(bar, parity);
         __syncwarp();
     }
+    __device__ __forceinline__ void wait3(uint32_t a0, uint32_t p0, bool w0, uint32_t a1, uint32_t p1, bool w1,
+                                          uint32_t a2 = 0, uint32_t p2 = 0, bool w2 = false) {
+        mbar_wait3(a0, p0, w0, a1, p1, w1, a2, p2, w2);
+    }
+    template <int ID, int N>
+    __device__ __forceinline__ void group_wait(uint32_t bar, uint32_t parity, bool leader) {
+        if (leader) mbar_wait(bar, parity);
+        asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+    }
     __device__ void store(int) {}
 };
 #endif
@@ -329,15 +385,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     const uint32_t* ktab = reinterpret_cast<const uint32_t*>(smem + a.kt_off);
     uint8_t* RG = smem + a.rg_off;  // staged input band(s): [nrb][Ci][NR][Wi]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.bar_off);
-    // barrier map: full[S] empty[S] (A stages in TMEM) accf[4] acce[4] rgf[2] rge[2] bres stg[4] fls[4]
-    // bfull[S] bempty[S] (streamed B stages in smem), then the TMEM address
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * S + 21);
-    const uint32_t bfull0 = smem_u32(bars + 2 * S + 21), bempty0 = smem_u32(bars + 3 * S + 21);
-    const uint32_t stg0 = smem_u32(bars + 2 * S + 13), fls0 = smem_u32(bars + 2 * S + 17);
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
-    const uint32_t accf0 = smem_u32(bars + 2 * S), acce0 = smem_u32(bars + 2 * S + 4);
-    const uint32_t rgf0 = smem_u32(bars + 2 * S + 8), rge0 = smem_u32(bars + 2 * S + 10);
-    const uint32_t bresb = smem_u32(bars + 2 * S + 12);
+    // barrier map: full[kMaxA] empty[kMaxA] (A ring in TMEM) accf[4] acce[4] rgf[2] rge[2] bres stg[4]
+    // fls[4] bfull[S] bempty[S] (streamed B stages in smem), then the TMEM address
+    constexpr int A2 = 2 * kMaxA;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + A2 + 21 + 2 * S);
+    const uint32_t bfull0 = smem_u32(bars + A2 + 21), bempty0 = smem_u32(bars + A2 + 21 + S);
+    const uint32_t stg0 = smem_u32(bars + A2 + 13), fls0 = smem_u32(bars + A2 + 17);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kMaxA);
+    const uint32_t accf0 = smem_u32(bars + A2), acce0 = smem_u32(bars + A2 + 4);
+    const uint32_t rgf0 = smem_u32(bars + A2 + 8), rge0 = smem_u32(bars + A2 + 10);
+    const uint32_t bresb = smem_u32(bars + A2 + 12);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const spk_conv_geom& g = a.g;
@@ -360,9 +417,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         for (int q = threadIdx.x; q < a.nrb * a.rb_stride / 4; q += kThreads) r4[q] = 0x7F7F7F7Fu;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < kMaxA; ++s) {
             mbar_init(full0 + 8 * s, kProdWarps);  // producer warps
             mbar_init(empty0 + 8 * s, 1);          // tcgen05.commit
+        }
+        for (int s = 0; s < S; ++s) {
             mbar_init(bfull0 + 8 * s, 1);          // B loader arrive.expect_tx
             mbar_init(bempty0 + 8 * s, 1);         // tcgen05.commit
         }
@@ -389,7 +448,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+#ifndef SPK_TMEM0
+#define SPK_TMEM0 1
+#endif
+#if SPK_TMEM0
+    // the kernel owns all 512 TMEM columns of its SM, so the allocation starts at 0: a
+    // compile-time base keeps every TMEM operand warp-uniform (checked once)
+    constexpr uint32_t tmem = 0;
+    if (threadIdx.x == 0 && *tmem_holder != 0u) __trap();
+#else
     const uint32_t tmem = *tmem_holder;
+#endif
 
     if (warp < kProdWarps) {
         // ======================= producers =======================
@@ -408,11 +477,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         const int gk = half * HK + ((GPIX == 2) ? (lane & 15) : lane) * GB;
         const int gpix_in_tile = ((quad * 32) >> LOGTP) + gslot;
         uint8_t* lcw = LC + warp * (4 * HK);         // [2 bufs][2 pixels][HK]
-        const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(kACol0 + half * (HK / 4));
+        const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a.aCol0 + half * (HK / 4));
         long long pt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         TileIter ti;
         ti.init(a);
         int sidx = 0, rb = 0, rbn = 0;
+        int sA = 0;           // A ring slot of the next stage
+        uint32_t phA = 0;     // and its phase
         uint32_t rgph = 0;
         bool need_region = true;
         long long tprev = rc.on ? clock64() : 0;
@@ -422,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (rc.on) pt[7] += tt0 - tprev;
             if (need_region) {
                 rb = rbn;
-                group_wait<kBarProd, kProdWarps * 32>(rgf0 + 8 * rb, rgph, threadIdx.x == 0);
+                rc.template group_wait<kBarProd, kProdWarps * 32>(rgf0 + 8 * rb, rgph, threadIdx.x == 0);
                 if (++rbn == a.nrb) rbn = 0, rgph ^= 1u;
             }
             const long long tt1 = rc.on ? clock64() : 0;
@@ -463,8 +534,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (rc.on) pt[6] += clock64() - tt1;
             for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
                 long long q0 = rc.on ? clock64() : 0;
-                const int s = sidx % S;
-                const uint32_t ph = (uint32_t)((sidx / S) & 1);
+                const int s = sA;
+                const uint32_t ph = phA;
+                if (++sA == a.NA) sA = 0, phA ^= 1u;
+#if (SPK_EXP & 64)  // timing experiment: producers only hand stages over
+                if (!(SPK_EXP & 16896)) rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + 8 * s, ph ^ 1u, threadIdx.x == 0);
+                if (threadIdx.x == 0) TRACE(6, sidx);
+                if (ks + 1 == a.nks && last_use) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(rge0 + 8 * rb);
+                }
+                __syncwarp();
+                if (lane == 0 && !(SPK_EXP & 16384)) mbar_arrive(full0 + 8 * s);
+                continue;
+#endif
                 uint8_t* lc = lcw + (sidx & 1) * (2 * HK);
                 if (GB == 4) *reinterpret_cast<uint32_t*>(lc + gslot * HK + (gk - half * HK)) = cur;
                 else *reinterpret_cast<uint16_t*>(lc + gslot * HK + (gk - half * HK)) = (uint16_t)cur;
@@ -489,7 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 }
                 long long q3 = rc.on ? clock64() : 0;
                 // wait for the MMAs that last read this TMEM A stage, then overwrite it
-                group_wait<kBarProd, kProdWarps * 32>(empty0 + 8 * s, ph ^ 1u, threadIdx.x == 0);
+                rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + 8 * s, ph ^ 1u, threadIdx.x == 0);
+                if (threadIdx.x == 0) TRACE(6, sidx);
                 long long q4 = rc.on ? clock64() : 0;
                 tc_fence_after();
 #if !(SPK_EXP & 4)
@@ -539,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         float* ob_ps = reinterpret_cast<float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
         TileIter ti;
         ti.init(a);
-        int buf = 0, ob = 0;
+        int buf = 0, ob = 0, ep_it = 0;
         uint32_t acc_ph = 0, ob_ph = 0;  // phase bits of the accumulator / staging rings
         for (; ti.valid(); ti.next(a)) {
             const int b = ti.b, nt = ti.nt;
@@ -547,11 +631,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const bool rvalid = p0 + pix < a.HWo && t < g.T;
             // padded rows never fire: fold the row mask into the threshold
             const long long thq = rvalid ? a.theta_q : 0x7fffffffffffffffll;
-            if (threadIdx.x == kProdWarps * 32 && EPI != SPK_EPI_POTENTIAL) mbar_wait(fls0 + 8 * ob, ob_ph ^ 1u);
-            group_wait<kBarEpi, kEpiWarps * 32>(accf0 + 8 * buf, acc_ph, threadIdx.x == kProdWarps * 32);
+            // the leader probes the staging slot and the accumulator together, the group sleeps
+            if (threadIdx.x == kProdWarps * 32)
+                rc.wait3(fls0 + 8 * ob, ob_ph ^ 1u, EPI != SPK_EPI_POTENTIAL, accf0 + 8 * buf, acc_ph,
+                         !(SPK_EXP & 8704));
+            asm volatile("bar.sync %0, %1;" ::"n"(kBarEpi), "n"(kEpiWarps * 32) : "memory");
+            if (threadIdx.x == kProdWarps * 32) TRACE(1, ep_it);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
-            for (int n0 = eh * 16; n0 < a.Nt; n0 += 32) {
+            for (int n0 = eh * 16; n0 < ((SPK_EXP & 128) ? 0 : a.Nt); n0 += 32) {
                 uint32_t d0[16], d1[16], d2[16];
 #if (SPK_EXP & 16)
 #pragma unroll
@@ -600,7 +688,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(acce0 + 8 * buf);
+            if (lane == 0 && !(SPK_EXP & 8192)) mbar_arrive(acce0 + 8 * buf);
+            if (threadIdx.x == kProdWarps * 32) TRACE(2, ep_it);
+            ++ep_it;
             if (EPI != SPK_EPI_POTENTIAL) {  // hand the staged tile to the flusher warp
                 __syncwarp();
                 if (lane == 0) mbar_arrive(stg0 + 8 * ob);
@@ -608,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (++buf == a.NB) buf = 0, acc_ph ^= 1u;
             if (++ob == kNOB) ob = 0, ob_ph ^= 1u;
         }
-        if (warp == kProdWarps && lane == 0) rc.store(1);
+        if (threadIdx.x == kProdWarps * 32) rc.store(1);
     } else if (warp == kMmaWarp) {
         // ======================= MMA issuer =======================
         RoleClock rc(a.prof != 0);
@@ -624,23 +714,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             long long f_fence = 0, f_issue = 0, f_commit = 0;
             TileIter ti;
             ti.init(a);
-            int asidx = 0, bs = 0, buf = 0;  // A ring (TMEM, S slots), B ring (smem, NS slots), accumulators
-            uint32_t b_ph = 0, acc_ph = 0;
+            int mma_it = 0, mma_st = 0;
+            int as_cur = 0, bs = 0, buf = 0;  // A ring (TMEM, NA slots), B ring (smem, NS slots), accumulators
+            uint32_t aph_cur = 0, b_ph = 0, acc_ph = 0;
             for (; ti.valid(); ti.next(a)) {
                 // a retained A is produced at the first N tile and released after the last one
                 const bool newA = !a.retain || ti.nt == 0, lastA = !a.retain || ti.nt == a.n_ntiles - 1;
-                rc.wait_warp(acce0 + 8 * buf, acc_ph ^ 1u);
+                const bool wacc = !(SPK_EXP & 8192);
+                if (lane == 0) TRACE(3, mma_it);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(buf * 3 * a.Nt);
+                int s = as_cur;
+                uint32_t aph = aph_cur;
                 for (int ks = 0; ks < a.nks; ++ks) {
-                    const int s = (asidx + ks) % S;
-                    if (newA) rc.wait_warp(full0 + 8 * s, (uint32_t)(((asidx + ks) / S) & 1));
-                    if (!a.bres) rc.wait_warp(bfull0 + 8 * bs, b_ph);
+                    if (ks) {
+                        if (++s == a.NA) s = 0, aph ^= 1u;
+                    }
+                    // all lanes probe (no divergence); the tile's accumulator wait joins stage 0's
+                    rc.wait3(full0 + 8 * s, aph, newA && !(SPK_EXP & 16384), bfull0 + 8 * bs, b_ph,
+                             !a.bres && !(SPK_EXP & 4096), acce0 + 8 * buf, acc_ph ^ 1u, wacc && ks == 0);
+                    if (lane == 0) TRACE(7, mma_st);
+                    ++mma_st;
                     const long long c0 = rc.on ? clock64() : 0;
                     tc_fence_after();
                     const long long c1 = rc.on ? clock64() : 0;
                     const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)bs) * bstage) >> 4);
-                    const uint32_t at = tmem + (uint32_t)(kACol0 + s * kACols);
+                    const uint32_t at = tmem + (uint32_t)(a.aCol0 + s * kACols);
                     // k-steps of 32 synapses this stage holds (the last stage may be partial)
                     const int nk = min(KS / 32, (a.K - ks * KS + 31) / 32);
                     const uint32_t acc0 = ks ? 1u : 0u;
@@ -662,11 +761,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                         }
                     }
                     const long long c2 = rc.on ? clock64() : 0;
-                    if (!a.bres) {
+                    if (!a.bres && !(SPK_EXP & 4096)) {
                         tc_commit_elect(bempty0 + 8 * bs);
                         if (++bs == a.NS) bs = 0, b_ph ^= 1u;
                     }
-                    if (lastA) tc_commit_elect(empty0 + 8 * s);
+                    if (lastA && !(SPK_EXP & 16384)) tc_commit_elect(empty0 + 8 * s);
                     if (rc.on) {
                         const long long c3 = clock64();
                         f_fence += c1 - c0;
@@ -674,8 +773,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                         f_commit += c3 - c2;
                     }
                 }
-                tc_commit_elect(accf0 + 8 * buf);
-                if (lastA) asidx += a.nks;
+                if (lane == 0) TRACE(0, mma_it);
+                if (!(SPK_EXP & 8192)) tc_commit_elect(accf0 + 8 * buf);
+                ++mma_it;
+                if (lastA) {  // the next M tile starts after this tile's stages
+                    as_cur = s + 1 == a.NA ? 0 : s + 1;
+                    if (s + 1 == a.NA) aph ^= 1u;
+                    aph_cur = aph;
+                }
                 if (++buf == a.NB) buf = 0, acc_ph ^= 1u;
             }
             if (lane == 0) rc.store(2);
@@ -692,7 +797,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         if (lane == 0) {
             const uint32_t bstage = 3u * a.Nt * KS;
             const uint32_t b_base = smem_u32(Bs);
-            if (a.bres) {
+            if (SPK_EXP & 4096) {
+            } else if (a.bres) {
                 // whole packed B of the (single) N tile, resident for the kernel
                 for (int ks = 0; ks < a.nks; ++ks) {
                     mbar_arrive_tx(bresb, bstage);
@@ -706,9 +812,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 for (; ti.valid(); ti.next(a)) {
                     for (int ks = 0; ks < a.nks; ++ks) {
                         rc.wait_idle(bempty0 + 8 * s, ph ^ 1u);
+#if (SPK_EXP & 256)  // timing experiment: no B traffic (stale smem operands)
+                        mbar_arrive(bfull0 + 8 * s);
+#else
                         mbar_arrive_tx(bfull0 + 8 * s, bstage);
                         bulk_g2s(b_base + s * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bstage,
                                  bfull0 + 8 * s);
+#endif
                         if (++s == a.NS) s = 0, ph ^= 1u;
                     }
                 }
@@ -731,11 +841,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             need_region = ti.region_ends(a);
             if (!load) continue;  // same staged region as the previous tile
             uint8_t* dst = RG + rb * a.rb_stride;
-            group_wait<kBarBand, kLoaders>(rge0 + 8 * rb, rph ^ 1u, lt == 0);
+            rc.template group_wait<kBarBand, kLoaders>(rge0 + 8 * rb, rph ^ 1u, lt == 0);
             // region[c][r][x] = min(lat[b][c][pr0 + r - Ph][x - Pw], 0x7F), 0x7F (never) in the halo
             const uint8_t* src = a.lat_in + (size_t)ti.b * g.Ci * plane;
             const int total = g.Ci * a.band;
-            if (a.NR == a.HiP) {
+            if (SPK_EXP & 2048) {  // timing experiment: no input staging (stale region)
+            } else if (a.NR == a.HiP) {
                 // whole padded sample: the halo was filled once at kernel start; copy the
                 // interior, one contiguous block of Ci*Hi*Wi bytes, 4 bytes per load when aligned
                 const int n = g.Ci * (int)plane;
@@ -813,10 +924,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         const float* ob_ps = reinterpret_cast<const float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
         TileIter ti;
         ti.init(a);
-        int ob = 0;
+        int ob = 0, fl_it = 0;
         uint32_t ph = 0;
         for (; ti.valid(); ti.next(a)) {
             if (lane == 0) mbar_wait_idle(stg0 + 8 * ob, ph);
+            if (lane == 0) TRACE(4, fl_it);
             __syncwarp();
             const int b = ti.b, nt = ti.nt, p0 = ti.j * PPT;
             const uint8_t* sl = ob_lat + ob * a.Nt * PPT;
@@ -841,6 +953,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(fls0 + 8 * ob);
+            if (lane == 0) TRACE(5, fl_it);
+            ++fl_it;
             if (++ob == kNOB) ob = 0, ph ^= 1u;
         }
     }
@@ -924,11 +1038,12 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     p.nks = (p.K + KS - 1) / KS;
     p.TP = g.T <= 16 ? 16 : 32;
     p.PPT = 128 / p.TP;
-    // N tiling: accumulators (3 digit planes) + the TMEM A stages share 512 columns
-    const int acc_cols = kACol0;  // 384
+    // N tiling: accumulators (3 digit planes) + the TMEM A ring share 512 columns; at least
+    // 4 A slots, at most 2 accumulator buffers, every remaining column to the A ring
+    const int acc_cols = 512 - 4 * kACols;  // 384
     // a reduction that fits the TMEM A ring is produced once per M tile and kept for every
     // N tile; N tiles of 64 then give two accumulator buffers (epilogue overlaps the MMAs)
-    p.retain = (p.nks <= S && g.Co > 64) ? 1 : 0;
+    p.retain = (p.nks <= 4 && g.Co > 64) ? 1 : 0;
     if (p.retain) {
         p.Nt = 64;
     } else if (g.Co <= 64) {
@@ -938,8 +1053,14 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
         const int per = (g.Co + nn - 1) / nn;
         p.Nt = ((per + 15) / 16) * 16;
     }
-    p.NB = std::min(4, acc_cols / (3 * p.Nt));  // TMEM accumulator buffers (MMA/epilogue overlap)
-    if (3 * p.Nt * p.NB > acc_cols) return false;
+    static const int nb_cap = [] {
+        const char* e = std::getenv("SPK_CONV_NB");  // tuning knob: accumulator buffers cap (1..4)
+        return e ? std::max(1, std::min(4, std::atoi(e))) : 2;
+    }();
+    p.NB = std::min(nb_cap, acc_cols / (3 * p.Nt));  // TMEM accumulator buffers (MMA/epilogue overlap)
+    if (p.NB < 1 || 3 * p.Nt * p.NB > acc_cols) return false;
+    p.NA = std::min(kMaxA, (512 - 3 * p.Nt * p.NB) / kACols);
+    p.aCol0 = 512 - p.NA * kACols;
     p.stack = (3 * p.Nt <= 256) ? 1 : 0;  // one MMA of N = 3 Nt covers the three digit planes
     p.n_ntiles = (g.Co + p.Nt - 1) / p.Nt;
     const int HWo = p.Ho * p.Wo;
@@ -1026,6 +1147,8 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.bres = p.bres;
     a.stack = p.stack;
     a.NS = p.NS;
+    a.NA = p.NA;
+    a.aCol0 = p.aCol0;
     a.retain = p.retain;
     a.total_tiles = p.total_tiles;
     // fire iff X * s 2^-23 > theta  <=>  X > floor(theta 2^23 / s)   (X integer, scaling exact)
@@ -1052,6 +1175,14 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
 
 // Debug: copy the per-role cycle counters of the last profiled conv (SPK_CONV_PROF=1)
 // into host memory [1024][17][2] (u64).  Not part of the public ABI.
+extern "C" __attribute__((visibility("default"))) int spk_debug_conv_trace(void* host) {
+#ifdef SPK_CONV_TRACE
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace));
+#else
+    (void)host;
+    return -1;
+#endif
+}
 extern "C" __attribute__((visibility("default"))) int spk_debug_conv_prof(void* host) {
     return (int)cudaMemcpyFromSymbol(host, g_conv_prof, sizeof(g_conv_prof));
 }

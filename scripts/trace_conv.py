@@ -1,0 +1,32 @@
+"""Event timestamps of CTA 0 of the tcgen05 conv (libspk built with -DSPK_CONV_TRACE)."""
+import ctypes, os, sys
+sys.path.insert(0, ".")
+import numpy as np, torch
+import synth
+from paper_2301_13659_b200 import spk
+from paper_2301_13659_b200.network import Network
+cfg = synth.load_config(sys.argv[1] if len(sys.argv) > 1 else "c2")
+B = cfg["batch"]
+net = Network(cfg, B)
+net.img.copy_(torch.from_numpy(synth.images(cfg, 0, B)))
+net.set_weights([torch.from_numpy(w) for w in synth.layer_weights(cfg)])
+net.front()
+L = spk.lib()
+tr = np.zeros((8, 256), np.int64)
+names = ["mma_commit_accf", "epi_wake", "epi_done", "mma_acce_wake", "fl_wake", "fl_done"]
+for li in range(len(net.layers)):
+    for rep in range(2):
+        net.layer(li, pstar=(li == cfg.get("train_layer")))
+        torch.cuda.synchronize()
+    L.spk_debug_conv_trace(tr.ctypes.data_as(ctypes.c_void_p))
+    t = tr - tr[0, 0]
+    n = 256
+    sl = slice(16, 200)
+    d = lambda a, b, lag=0: np.median((t[b, sl.start + lag:sl.stop + lag] - t[a, sl]))
+    print(f"layer {li}: per-tile period mma {np.median(np.diff(t[0, sl])):.0f}  epi {np.median(np.diff(t[2, sl])):.0f}  fl {np.median(np.diff(t[5, sl])):.0f} cycles")
+    print(f"   commit->epi_wake {d(0, 1):.0f}  epi_wake->epi_done {d(1, 2):.0f}  epi_done->mma_acce_wake(+NB) "
+          f"{np.median(t[3, sl.start + 4:sl.stop + 4] - t[2, sl]):.0f}  acce_wake->commit {d(3, 0):.0f}  "
+          f"epi_done->fl_wake {d(2, 4):.0f}  fl_wake->fl_done {d(4, 5):.0f}")
+    print("   first tiles (mma commit):", (t[0, :8]).tolist())
+    print("   stages: prod granted", np.diff(t[6, 16:24]).tolist(), " mma full-wake", np.diff(t[7, 16:24]).tolist())
+    print("   prod granted -> mma wake (same stage):", (t[7, 16:32] - t[6, 16:32]).tolist())
