@@ -161,7 +161,9 @@ class Network:
             self.infer(mark)
 
     # ------------------------------------------------------------ CUDA graph
-    def capture(self, warmup: int = 1):
+    def capture(self, warmup: int = 1, mark=None):
+        """Capture one step in a CUDA graph; `mark(name)` hooks (e.g. external timing
+        events) are captured with it as graph nodes."""
         s = torch.cuda.Stream(device=self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
@@ -170,7 +172,7 @@ class Network:
         torch.cuda.current_stream(self.dev).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.step()
+            self.step_marked(mark or _nomark)
         self.graph = g
         return g
 
