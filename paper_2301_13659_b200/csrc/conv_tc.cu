@@ -206,6 +206,26 @@ __device__ __forceinline__ void tc_stage_sep(uint32_t d0, uint32_t d1, uint32_t 
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) tc_kstep3(d0, d1, d2, a0 + 8u * kk, bdesc + inck * kk, incd, idesc, kk ? 1u : acc0);
 }
+// one k-step with planes 0-1 stacked (N = 2 Nt, accumulators d01 .. d01 + 2 Nt) and plane 2
+// alone (N = Nt): two MMAs instead of three when 3 Nt > 256 >= 2 Nt
+__device__ __forceinline__ void tc_kstep2(uint32_t d01, uint32_t d2, uint32_t a, uint64_t x0, uint64_t inc2,
+                                          uint32_t idesc01, uint32_t idesc2, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p, e;\n.reg .b64 x2;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %7, 0;\n add.s64 x2, %3, %4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%2], %3, %5, p;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%2], x2, %6, p;\n}\n" ::"r"(d01),
+        "r"(d2), "r"(a), "l"(x0), "l"(inc2), "r"(idesc01), "r"(idesc2), "r"(acc)
+        : "memory");
+}
+template <int NK>
+__device__ __forceinline__ void tc_stage_pair(uint32_t d01, uint32_t d2, uint32_t a0, uint64_t bdesc, uint64_t inck,
+                                              uint64_t inc2, uint32_t idesc01, uint32_t idesc2, uint32_t acc0) {
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk)
+        tc_kstep2(d01, d2, a0 + 8u * kk, bdesc + inck * kk, inc2, idesc01, idesc2, kk ? 1u : acc0);
+}
 template <int NK>
 __device__ __forceinline__ void tc_stage_stacked(uint32_t d0, uint32_t a0, uint64_t bdesc, uint64_t inck,
                                                  uint32_t idesc, uint32_t acc0) {
@@ -703,8 +723,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         // ======================= MMA issuer =======================
         RoleClock rc(a.prof != 0);
         {  // the whole warp runs the loop (uniform control flow); elected lanes issue
-            const int nmma = a.stack ? 3 * a.Nt : a.Nt;  // N of one MMA
-            const uint32_t idesc = (2u << 4) | ((uint32_t)(nmma >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            auto mk_idesc = [](int n) {  // s32 D, u8 A/B, K-major, M = 128
+                return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            };
+            const uint32_t idesc = mk_idesc(a.stack == 1 ? 3 * a.Nt : a.Nt);  // N of one MMA
+            const uint32_t idesc01 = mk_idesc(2 * a.Nt);                      // planes 0-1 (stack == 2)
             const uint32_t b_base = smem_u32(Bs);
             const uint32_t bstage = 3u * a.Nt * KS, bchunk = 3u * a.Nt * 16;  // chunk stride (LBO)
             const uint64_t d0 = smem_desc(b_base, bchunk, 128);                // descriptor template
@@ -744,7 +767,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     const int nk = min(KS / 32, (a.K - ks * KS + 31) / 32);
                     const uint32_t acc0 = ks ? 1u : 0u;
                     if (SPK_EXP & 32) {
-                    } else if (a.stack) {
+                    } else if (a.stack == 2) {
+                        const uint32_t e2 = dbase + 2 * a.Nt;
+                        switch (nk) {
+                            case 1: tc_stage_pair<1>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
+                            case 2: tc_stage_pair<2>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
+                            case 3: tc_stage_pair<3>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
+                            default: tc_stage_pair<4>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
+                        }
+                    } else if (a.stack == 1) {
                         switch (nk) {
                             case 1: tc_stage_stacked<1>(dbase, at, dst, inck, idesc, acc0); break;
                             case 2: tc_stage_stacked<2>(dbase, at, dst, inck, idesc, acc0); break;
@@ -1061,7 +1092,8 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     if (p.NB < 1 || 3 * p.Nt * p.NB > acc_cols) return false;
     p.NA = std::min(kMaxA, (512 - 3 * p.Nt * p.NB) / kACols);
     p.aCol0 = 512 - p.NA * kACols;
-    p.stack = (3 * p.Nt <= 256) ? 1 : 0;  // one MMA of N = 3 Nt covers the three digit planes
+    // digit planes per MMA: all three (N = 3 Nt), planes 0-1 + plane 2, or one each
+    p.stack = (3 * p.Nt <= 256) ? 1 : (2 * p.Nt <= 256) ? 2 : 0;
     p.n_ntiles = (g.Co + p.Nt - 1) / p.Nt;
     const int HWo = p.Ho * p.Wo;
     p.tps = (HWo + p.PPT - 1) / p.PPT;
