@@ -53,7 +53,7 @@
 namespace {
 
 constexpr int KS = kTcKS;          // synapses per stage (4 MMAs of K=32)
-static_assert(KS == 128, "tc_stage_* issue exactly 4 k-steps");
+static_assert(KS == 128, "an A slot holds 4 k-steps of 32 synapses");
 constexpr int S = kTcStages;       // pipeline depth
 constexpr int kProdWarps = 8;      // warps 0-7: producers
 constexpr int kEpiWarps = 8;       // warps 8-15: epilogue (two per TMEM lane quadrant)
@@ -92,6 +92,8 @@ struct TcArgs {
     int Ho, Wo, HWo, K, nks, Nt, n_ntiles, NB, tps, NR, band, nrb, rb_stride, bres, stack, NS;
     int retain;  // the A stages of an M tile stay in TMEM for all its N tiles (nks <= NA)
     int NA, aCol0;  // TMEM A ring: NA slots of kACols columns from column aCol0 = 512 - NA * kACols
+    int G;          // K slots per hand-off (1 or 2): one mbarrier round trip per G * KS synapses
+    int kt16;       // synapse offsets fit 16 bits: the table is u16 (half the smem)
     int WiP, HiP;  // padded input width/height: the staged region includes the zero-padding halo
     long long total_tiles;
     long long theta_q;  // fire iff X > theta_q
@@ -202,7 +204,7 @@ __device__ __forceinline__ void tc_kstep3(uint32_t d0, uint32_t d1, uint32_t d2,
 template <int NK>
 __device__ __forceinline__ void tc_stage_sep(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t a0, uint64_t bdesc,
                                              uint64_t inck, uint64_t incd, uint32_t idesc, uint32_t acc0) {
-    static_assert(NK >= 1 && NK <= 4, "k-steps per stage");
+    static_assert(NK >= 1 && NK <= 8, "k-steps per hand-off");
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) tc_kstep3(d0, d1, d2, a0 + 8u * kk, bdesc + inck * kk, incd, idesc, kk ? 1u : acc0);
 }
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     {  // synapse table: offset c*NR*WiP + i*WiP + j into the halo'd staged region;
        // padding synapses k >= K point at the "never" sentinel block after the region
         uint32_t* kt = reinterpret_cast<uint32_t*>(smem + a.kt_off);
+        uint16_t* kt16 = reinterpret_cast<uint16_t*>(smem + a.kt_off);
         const int KhKw = g.Kh * g.Kw;
         for (int k = threadIdx.x; k < a.nks * KS; k += kThreads) {
             uint32_t e = (uint32_t)(g.Ci * a.band);  // sentinel (reads 0x7F there)
@@ -429,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 const int c = k / KhKw, r = k - c * KhKw, i = r / g.Kw, j = r - i * g.Kw;
                 e = (uint32_t)(c * a.band + i * a.WiP + j);
             }
-            kt[k] = e;
+            if (a.kt16) kt16[k] = (uint16_t)e;
+            else kt[k] = e;
         }
     }
     if (a.NR == a.HiP) {  // whole padded samples: the halo never changes, fill it (and all) once
@@ -534,7 +538,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #endif
                 if (!pvalid) return 0x7F7F7F7Fu;
                 uint32_t te[GB];
-                if (GB == 4) {
+                if (a.kt16) {
+                    const uint16_t* k16 = reinterpret_cast<const uint16_t*>(ktab) + ks * KS + gk;
+                    if (GB == 4) {
+                        const uint2 v = *reinterpret_cast<const uint2*>(k16);
+                        te[0] = v.x & 0xFFFFu;
+                        te[1] = v.x >> 16;
+                        te[2] = v.y & 0xFFFFu;
+                        te[3] = v.y >> 16;
+                    } else {
+                        const uint32_t v = *reinterpret_cast<const uint32_t*>(k16);
+                        te[0] = v & 0xFFFFu;
+                        te[1] = v >> 16;
+                    }
+                } else if (GB == 4) {
                     const uint4 t4 = *reinterpret_cast<const uint4*>(ktab + ks * KS + gk);
                     te[0] = t4.x;
                     te[1] = t4.y;
@@ -554,18 +571,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (rc.on) pt[6] += clock64() - tt1;
             for (int ks = 0; ks < a.nks; ++ks, ++sidx) {
                 long long q0 = rc.on ? clock64() : 0;
-                const int s = sA;
+                // slot group sA (G consecutive slots, one hand-off) holds stages gi*G .. gi*G+G-1
+                const int kin = a.G == 1 ? 0 : (ks & 1);
+                const bool gfirst = kin == 0, glast = kin == a.G - 1 || ks + 1 == a.nks;
+                const int s = sA * a.G + kin;  // TMEM slot
                 const uint32_t ph = phA;
-                if (++sA == a.NA) sA = 0, phA ^= 1u;
+                const uint32_t gbar = 8u * (uint32_t)sA;
+                if (glast && ++sA == a.NA / a.G) sA = 0, phA ^= 1u;
 #if (SPK_EXP & 64)  // timing experiment: producers only hand stages over
-                if (!(SPK_EXP & 16896)) rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + 8 * s, ph ^ 1u, threadIdx.x == 0);
+                if (!(SPK_EXP & 16896) && gfirst)
+                    rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + gbar, ph ^ 1u, threadIdx.x == 0);
                 if (threadIdx.x == 0) TRACE(6, sidx);
                 if (ks + 1 == a.nks && last_use) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(rge0 + 8 * rb);
                 }
                 __syncwarp();
-                if (lane == 0 && !(SPK_EXP & 16384)) mbar_arrive(full0 + 8 * s);
+                if (lane == 0 && !(SPK_EXP & 16384) && glast) mbar_arrive(full0 + gbar);
                 continue;
 #endif
                 uint8_t* lc = lcw + (sidx & 1) * (2 * HK);
@@ -592,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 }
                 long long q3 = rc.on ? clock64() : 0;
                 // wait for the MMAs that last read this TMEM A stage, then overwrite it
-                rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + 8 * s, ph ^ 1u, threadIdx.x == 0);
+                if (gfirst) rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + gbar, ph ^ 1u, threadIdx.x == 0);
                 if (threadIdx.x == 0) TRACE(6, sidx);
                 long long q4 = rc.on ? clock64() : 0;
                 tc_fence_after();
@@ -605,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 tc_fence_before();
                 long long q5 = rc.on ? clock64() : 0;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(full0 + 8 * s);
+                if (lane == 0 && glast) mbar_arrive(full0 + gbar);
                 if (rc.on) {
                     const long long q6 = clock64();
                     pt[0] += q1 - q0;  // latcol store + syncwarp
@@ -747,13 +769,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 if (lane == 0) TRACE(3, mma_it);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(buf * 3 * a.Nt);
-                int s = as_cur;
+                int s = as_cur;  // slot group (G slots per hand-off)
                 uint32_t aph = aph_cur;
-                for (int ks = 0; ks < a.nks; ++ks) {
+                const int ngrp = a.NA / a.G;
+                for (int ks = 0; ks < a.nks; ks += a.G) {
                     if (ks) {
-                        if (++s == a.NA) s = 0, aph ^= 1u;
+                        if (++s == ngrp) s = 0, aph ^= 1u;
                     }
-                    // all lanes probe (no divergence); the tile's accumulator wait joins stage 0's
+                    // all lanes probe (no divergence); the tile's accumulator wait joins the first hand-off's
                     rc.wait3(full0 + 8 * s, aph, newA && !(SPK_EXP & 16384), bfull0 + 8 * bs, b_ph,
                              !a.bres && !(SPK_EXP & 4096), acce0 + 8 * buf, acc_ph ^ 1u, wacc && ks == 0);
                     if (lane == 0) TRACE(7, mma_st);
@@ -761,36 +784,40 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     const long long c0 = rc.on ? clock64() : 0;
                     tc_fence_after();
                     const long long c1 = rc.on ? clock64() : 0;
-                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)bs) * bstage) >> 4);
-                    const uint32_t at = tmem + (uint32_t)(a.aCol0 + s * kACols);
-                    // k-steps of 32 synapses this stage holds (the last stage may be partial)
-                    const int nk = min(KS / 32, (a.K - ks * KS + 31) / 32);
+                    // the group's slots and B blocks are contiguous: k-step kk at + 8 kk, dst + kk inck
+                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)(bs * a.G)) * bstage) >> 4);
+                    const uint32_t at = tmem + (uint32_t)(a.aCol0 + s * a.G * kACols);
+                    // k-steps of 32 synapses this hand-off holds (the last one may be partial)
+                    const int nk = min(a.G * (KS / 32), (a.K - ks * KS + 31) / 32);
                     const uint32_t acc0 = ks ? 1u : 0u;
+#define SPK_NK_SWITCH(CALL)            \
+    switch (nk) {                      \
+        case 1: CALL(1); break;        \
+        case 2: CALL(2); break;        \
+        case 3: CALL(3); break;        \
+        case 4: CALL(4); break;        \
+        case 5: CALL(5); break;        \
+        case 6: CALL(6); break;        \
+        case 7: CALL(7); break;        \
+        default: CALL(8); break;       \
+    }
                     if (SPK_EXP & 32) {
                     } else if (a.stack == 2) {
                         const uint32_t e2 = dbase + 2 * a.Nt;
-                        switch (nk) {
-                            case 1: tc_stage_pair<1>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
-                            case 2: tc_stage_pair<2>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
-                            case 3: tc_stage_pair<3>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
-                            default: tc_stage_pair<4>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0); break;
-                        }
+#define SPK_PAIR(n) tc_stage_pair<n>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0)
+                        SPK_NK_SWITCH(SPK_PAIR)
+#undef SPK_PAIR
                     } else if (a.stack == 1) {
-                        switch (nk) {
-                            case 1: tc_stage_stacked<1>(dbase, at, dst, inck, idesc, acc0); break;
-                            case 2: tc_stage_stacked<2>(dbase, at, dst, inck, idesc, acc0); break;
-                            case 3: tc_stage_stacked<3>(dbase, at, dst, inck, idesc, acc0); break;
-                            default: tc_stage_stacked<4>(dbase, at, dst, inck, idesc, acc0); break;
-                        }
+#define SPK_STACKED(n) tc_stage_stacked<n>(dbase, at, dst, inck, idesc, acc0)
+                        SPK_NK_SWITCH(SPK_STACKED)
+#undef SPK_STACKED
                     } else {
                         const uint32_t e1 = dbase + a.Nt, e2 = dbase + 2 * a.Nt;
-                        switch (nk) {
-                            case 1: tc_stage_sep<1>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
-                            case 2: tc_stage_sep<2>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
-                            case 3: tc_stage_sep<3>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
-                            default: tc_stage_sep<4>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0); break;
-                        }
+#define SPK_SEP(n) tc_stage_sep<n>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0)
+                        SPK_NK_SWITCH(SPK_SEP)
+#undef SPK_SEP
                     }
+#undef SPK_NK_SWITCH
                     const long long c2 = rc.on ? clock64() : 0;
                     if (!a.bres && !(SPK_EXP & 4096)) {
                         tc_commit_elect(bempty0 + 8 * bs);
@@ -807,9 +834,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 if (lane == 0) TRACE(0, mma_it);
                 if (!(SPK_EXP & 8192)) tc_commit_elect(accf0 + 8 * buf);
                 ++mma_it;
-                if (lastA) {  // the next M tile starts after this tile's stages
-                    as_cur = s + 1 == a.NA ? 0 : s + 1;
-                    if (s + 1 == a.NA) aph ^= 1u;
+                if (lastA) {  // the next M tile starts after this tile's slot groups
+                    as_cur = s + 1 == ngrp ? 0 : s + 1;
+                    if (s + 1 == ngrp) aph ^= 1u;
                     aph_cur = aph;
                 }
                 if (++buf == a.NB) buf = 0, acc_ph ^= 1u;
@@ -841,13 +868,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 int s = 0;
                 uint32_t ph = 0;
                 for (; ti.valid(); ti.next(a)) {
-                    for (int ks = 0; ks < a.nks; ++ks) {
+                    for (int ks = 0; ks < a.nks; ks += a.G) {  // one copy per slot group
+                        const uint32_t bytes = (uint32_t)min(a.G, a.nks - ks) * bstage;
                         rc.wait_idle(bempty0 + 8 * s, ph ^ 1u);
 #if (SPK_EXP & 256)  // timing experiment: no B traffic (stale smem operands)
                         mbar_arrive(bfull0 + 8 * s);
 #else
-                        mbar_arrive_tx(bfull0 + 8 * s, bstage);
-                        bulk_g2s(b_base + s * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bstage,
+                        mbar_arrive_tx(bfull0 + 8 * s, bytes);
+                        bulk_g2s(b_base + s * a.G * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bytes,
                                  bfull0 + 8 * s);
 #endif
                         if (++s == a.NS) s = 0, ph ^= 1u;
@@ -1115,7 +1143,9 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     p.total_tiles = p.n_mtiles * p.n_ntiles;
     p.packed_bytes = (size_t)p.n_ntiles * p.nks * 3 * p.Nt * KS;
     p.ws_bytes = 256 + p.packed_bytes;
-    const size_t bstage = (size_t)3 * p.Nt * KS, lc = 8 * 4 * (KS / 2), kt = 4 * (size_t)p.nks * KS;
+    p.kt16 = (size_t)g.Ci * p.band + 16 < 65536 ? 1 : 0;
+    const size_t bstage = (size_t)3 * p.Nt * KS, lc = 8 * 4 * (KS / 2),
+                 kt = (p.kt16 ? 2 : 4) * (size_t)p.nks * KS;
     const size_t ob = (size_t)kNOB * p.Nt * p.PPT * 5;  // output staging ring (lat + P*)
     const size_t region = ((size_t)g.Ci * p.band + 16 + 15) & ~(size_t)15;  // + sentinel block
     const size_t cap = 227 * 1024;
@@ -1124,10 +1154,21 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     // resident B when there is one N tile and all its K stages fit next to two band buffers
     const size_t bres_bytes = (size_t)p.nks * bstage;
     p.bres = (p.n_ntiles == 1 && bres_bytes + other + 2 * region <= cap) ? 1 : 0;
-    // streamed B: as many stages (<= S) as fit next to one band buffer
+    // hand-offs of G = 2 slots (half the mbarrier round trips) when the ring keeps >= 2
+    // groups and at least two streamed B groups fit; a retained A keeps G = 1
+    static const int g_cap = [] {
+        const char* e = std::getenv("SPK_CONV_G");  // tuning knob: 1 or 2
+        return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+    }();
+    p.G = 1;
+    if (g_cap == 2 && !p.retain && p.nks >= 2 && p.NA >= 4 &&
+        (p.bres || 2 * 2 * bstage + other + region <= cap))
+        p.G = 2;
+    // streamed B: as many groups (<= S) as fit next to one band buffer
+    const size_t gstage = (size_t)p.G * bstage;
     p.NS = S;
-    while (!p.bres && p.NS > 2 && (size_t)p.NS * bstage + other + region > cap) --p.NS;
-    const size_t b = p.bres ? bres_bytes : (size_t)p.NS * bstage;
+    while (!p.bres && p.NS > 2 && (size_t)p.NS * gstage + other + region > cap) --p.NS;
+    const size_t b = p.bres ? bres_bytes : (size_t)p.NS * gstage;
     const size_t fixed = b + other;
     if (fixed + region > cap) return false;
     p.nrb = (fixed + 2 * region <= cap) ? 2 : 1;
@@ -1181,6 +1222,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.NS = p.NS;
     a.NA = p.NA;
     a.aCol0 = p.aCol0;
+    a.G = p.G;
     a.retain = p.retain;
     a.total_tiles = p.total_tiles;
     // fire iff X * s 2^-23 > theta  <=>  X > floor(theta 2^23 / s)   (X integer, scaling exact)
@@ -1194,9 +1236,10 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.prof = prof_env;
     const size_t bstage = (size_t)3 * p.Nt * KS;
     a.b_off = 0;
-    a.lc_off = (uint32_t)(p.bres ? p.nks * bstage : p.NS * bstage);
+    a.lc_off = (uint32_t)(p.bres ? p.nks * bstage : p.NS * p.G * bstage);
     a.kt_off = a.lc_off + 8u * 4u * (KS / 2);
-    a.rg_off = (a.kt_off + (uint32_t)(4 * p.nks * KS) + 15u) & ~15u;
+    a.rg_off = (a.kt_off + (uint32_t)((p.kt16 ? 2 : 4) * p.nks * KS) + 15u) & ~15u;
+    a.kt16 = p.kt16;
     a.ob_off = (a.rg_off + (uint32_t)(p.nrb * p.rb_stride) + 15u) & ~15u;
     a.bar_off = (a.ob_off + (uint32_t)(kNOB * p.Nt * p.PPT * 5) + 15u) & ~15u;
     const long long grid = p.total_tiles < sm_count() ? p.total_tiles : sm_count();
