@@ -5,7 +5,7 @@
 // Geometry of the tcgen05 exact path (see conv_tc.cu).
 struct TcPlan {
     int Ho, Wo, K, KS, nks, TP, PPT, Nt, n_ntiles, NB;
-    int tps, NR, band, nrb, bres, stack, NS, WiP, HiP, retain, NA, aCol0, G, kt16;  // M tiles per sample, staged input rows per tile, bytes per channel band, band buffers, resident B
+    int tps, NR, band, nrb, bres, stack, NS, WiP, HiP, retain, NA, aCol0, G, kt16, GB;  // M tiles per sample, staged input rows per tile, bytes per channel band, band buffers, resident B
     size_t rb_stride;
     long long NP, n_mtiles, total_tiles;
     size_t packed_bytes, ws_bytes, smem_bytes;

@@ -72,7 +72,7 @@ __device__ unsigned long long g_conv_prof[1024][kProfRoles][2];
 #ifdef SPK_CONV_TRACE
 // event timestamps of CTA 0's first kTrace tiles (debug aid)
 constexpr int kTrace = 256;
-__device__ long long g_trace[8][kTrace];
+__device__ long long g_trace[12][kTrace];
 #define TRACE(ev, it)                                                        \
     do {                                                                     \
         if (blockIdx.x == 0 && (it) < kTrace) g_trace[ev][(it)] = clock64(); \
@@ -94,6 +94,7 @@ struct TcArgs {
     int NA, aCol0;  // TMEM A ring: NA slots of kACols columns from column aCol0 = 512 - NA * kACols
     int G;          // K slots per hand-off (1 or 2): one mbarrier round trip per G * KS synapses
     int kt16;       // synapse offsets fit 16 bits: the table is u16 (half the smem)
+    int GB;         // K slots per streamed B hand-off (a multiple of G; = nks: one B copy per tile)
     int WiP, HiP;  // padded input width/height: the staged region includes the zero-padding halo
     long long total_tiles;
     long long theta_q;  // fire iff X > theta_q
@@ -484,7 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     const uint32_t tmem = *tmem_holder;
 #endif
 
-    if (warp < kProdWarps) {
+    if (warp < kProdWarps && (SPK_EXP & 32768)) {  // timing experiment: no producers (MMA skips A waits)
+    } else if (warp < kProdWarps) {
         // ======================= producers =======================
         RoleClock rc(a.prof != 0);
         const int quad = warp & 3, half = warp >> 2;
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const long long thq = rvalid ? a.theta_q : 0x7fffffffffffffffll;
             // the leader probes the staging slot and the accumulator together, the group sleeps
             if (threadIdx.x == kProdWarps * 32)
-                rc.wait3(fls0 + 8 * ob, ob_ph ^ 1u, EPI != SPK_EPI_POTENTIAL, accf0 + 8 * buf, acc_ph,
+                rc.wait3(fls0 + 8 * ob, ob_ph ^ 1u, EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 65536), accf0 + 8 * buf, acc_ph,
                          !(SPK_EXP & 8704));
             asm volatile("bar.sync %0, %1;" ::"n"(kBarEpi), "n"(kEpiWarps * 32) : "memory");
             if (threadIdx.x == kProdWarps * 32) TRACE(1, ep_it);
@@ -769,6 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 if (lane == 0) TRACE(3, mma_it);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(buf * 3 * a.Nt);
+                int kb_next = 0;
                 int s = as_cur;  // slot group (G slots per hand-off)
                 uint32_t aph = aph_cur;
                 const int ngrp = a.NA / a.G;
@@ -776,16 +779,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     if (ks) {
                         if (++s == ngrp) s = 0, aph ^= 1u;
                     }
+                    if (lane == 0) TRACE(9, mma_st);
                     // all lanes probe (no divergence); the tile's accumulator wait joins the first hand-off's
+                    const int kb = kb_next;  // slot offset inside the current B hand-off
+                    kb_next = kb + a.G >= a.GB ? 0 : kb + a.G;
                     rc.wait3(full0 + 8 * s, aph, newA && !(SPK_EXP & 16384), bfull0 + 8 * bs, b_ph,
-                             !a.bres && !(SPK_EXP & 4096), acce0 + 8 * buf, acc_ph ^ 1u, wacc && ks == 0);
+                             !a.bres && !(SPK_EXP & 4096) && kb == 0, acce0 + 8 * buf, acc_ph ^ 1u, wacc && ks == 0);
                     if (lane == 0) TRACE(7, mma_st);
                     ++mma_st;
                     const long long c0 = rc.on ? clock64() : 0;
                     tc_fence_after();
                     const long long c1 = rc.on ? clock64() : 0;
                     // the group's slots and B blocks are contiguous: k-step kk at + 8 kk, dst + kk inck
-                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)(bs * a.G)) * bstage) >> 4);
+                    const uint64_t dst = d0 + (((a.bres ? (uint32_t)ks : (uint32_t)(bs * a.GB + kb)) * bstage) >> 4);
                     const uint32_t at = tmem + (uint32_t)(a.aCol0 + s * a.G * kACols);
                     // k-steps of 32 synapses this hand-off holds (the last one may be partial)
                     const int nk = min(a.G * (KS / 32), (a.K - ks * KS + 31) / 32);
@@ -818,12 +824,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #undef SPK_SEP
                     }
 #undef SPK_NK_SWITCH
+                    if (lane == 0) TRACE(10, mma_st - 1);
                     const long long c2 = rc.on ? clock64() : 0;
-                    if (!a.bres && !(SPK_EXP & 4096)) {
+                    if (!a.bres && !(SPK_EXP & 4096) && (kb_next == 0 || ks + a.G >= a.nks)) {
                         tc_commit_elect(bempty0 + 8 * bs);
                         if (++bs == a.NS) bs = 0, b_ph ^= 1u;
                     }
                     if (lastA && !(SPK_EXP & 16384)) tc_commit_elect(empty0 + 8 * s);
+                    if (lane == 0) TRACE(11, mma_st - 1);
                     if (rc.on) {
                         const long long c3 = clock64();
                         f_fence += c1 - c0;
@@ -865,17 +873,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             } else {
                 TileIter ti;
                 ti.init(a);
-                int s = 0;
+                int s = 0, bl_st = 0;
                 uint32_t ph = 0;
                 for (; ti.valid(); ti.next(a)) {
-                    for (int ks = 0; ks < a.nks; ks += a.G) {  // one copy per slot group
-                        const uint32_t bytes = (uint32_t)min(a.G, a.nks - ks) * bstage;
+                    for (int ks = 0; ks < a.nks; ks += a.GB) {  // one copy per B hand-off
+                        const uint32_t bytes = (uint32_t)min(a.GB, a.nks - ks) * bstage;
                         rc.wait_idle(bempty0 + 8 * s, ph ^ 1u);
+                        TRACE(8, bl_st);
+                        ++bl_st;
 #if (SPK_EXP & 256)  // timing experiment: no B traffic (stale smem operands)
                         mbar_arrive(bfull0 + 8 * s);
 #else
                         mbar_arrive_tx(bfull0 + 8 * s, bytes);
-                        bulk_g2s(b_base + s * a.G * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bytes,
+                        bulk_g2s(b_base + s * a.GB * bstage, a.wpk + ((size_t)ti.nt * a.nks + ks) * bstage, bytes,
                                  bfull0 + 8 * s);
 #endif
                         if (++s == a.NS) s = 0, ph ^= 1u;
@@ -885,6 +895,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             rc.store(3);
         }
         __syncwarp();
+    } else if (warp < kFlushWarp && (SPK_EXP & 32768)) {  // no band loaders either
     } else if (warp < kFlushWarp) {
         // ======================= input band loaders =======================
         RoleClock rc(a.prof != 0);
@@ -977,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         if (lt == 0) rc.store(4);
     }
 
-    if (warp == kFlushWarp && EPI != SPK_EPI_POTENTIAL) {
+    if (warp == kFlushWarp && EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 65536)) {
         // ======================= flusher: staged tile -> one run of PPT pixels per output map
         const uint8_t* ob_lat = smem + a.ob_off;
         const float* ob_ps = reinterpret_cast<const float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
@@ -1161,11 +1172,17 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
         return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
     }();
     p.G = 1;
-    if (g_cap == 2 && !p.retain && p.nks >= 2 && p.NA >= 4 &&
-        (p.bres || 2 * 2 * bstage + other + region <= cap))
-        p.G = 2;
-    // streamed B: as many groups (<= S) as fit next to one band buffer
-    const size_t gstage = (size_t)p.G * bstage;
+    {
+        // a retained A needs room for two M tiles' groups, a streamed one for two groups
+        const int need = p.retain ? 2 * ((p.nks + 1) / 2) : 2;
+        if (g_cap == 2 && p.nks >= 2 && p.NA / 2 >= need && (p.bres || 2 * 2 * bstage + other + region <= cap))
+            p.G = 2;
+    }
+    // streamed B: one hand-off per tile when two whole-tile B stages fit (retained A: the
+    // MMA warp then probes once per N tile), else per slot group
+    p.GB = p.G;
+    if (!p.bres && p.retain && (size_t)2 * p.nks * bstage + other + region <= cap) p.GB = p.nks;
+    const size_t gstage = (size_t)p.GB * bstage;
     p.NS = S;
     while (!p.bres && p.NS > 2 && (size_t)p.NS * gstage + other + region > cap) --p.NS;
     const size_t b = p.bres ? bres_bytes : (size_t)p.NS * gstage;
@@ -1223,6 +1240,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.NA = p.NA;
     a.aCol0 = p.aCol0;
     a.G = p.G;
+    a.GB = p.GB;
     a.retain = p.retain;
     a.total_tiles = p.total_tiles;
     // fire iff X * s 2^-23 > theta  <=>  X > floor(theta 2^23 / s)   (X integer, scaling exact)
@@ -1236,7 +1254,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.prof = prof_env;
     const size_t bstage = (size_t)3 * p.Nt * KS;
     a.b_off = 0;
-    a.lc_off = (uint32_t)(p.bres ? p.nks * bstage : p.NS * p.G * bstage);
+    a.lc_off = (uint32_t)(p.bres ? p.nks * bstage : p.NS * p.GB * bstage);
     a.kt_off = a.lc_off + 8u * 4u * (KS / 2);
     a.rg_off = (a.kt_off + (uint32_t)((p.kt16 ? 2 : 4) * p.nks * KS) + 15u) & ~15u;
     a.kt16 = p.kt16;

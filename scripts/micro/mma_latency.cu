@@ -24,7 +24,7 @@ __global__ void k(int N, int n, int reps, long long* out) {
     const uint32_t tmem = holder;
     if (threadIdx.x == 0) {
         const uint32_t idesc = (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        long long tot = 0;
+        long long tot = 0, tiss = 0;
         for (int r = 0; r < reps; ++r) {
             const long long t0 = clock64();
             for (int i = 0; i < n; ++i) {
@@ -32,6 +32,7 @@ __global__ void k(int N, int n, int reps, long long* out) {
                 asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;}" ::"r"(tmem),
                              "r"(tmem + 384 + (i & 3) * 8), "l"(bd), "r"(idesc), "r"(i) : "memory");
             }
+            const long long t_issue = clock64();
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
             uint32_t ok = 0;
             do {
@@ -39,8 +40,10 @@ __global__ void k(int N, int n, int reps, long long* out) {
                              : "=r"(ok) : "r"(su32(&bar)), "r"((uint32_t)(r & 1)) : "memory");
             } while (!ok);
             tot += clock64() - t0;
+            tiss += t_issue - t0;
         }
         out[blockIdx.x] = tot / reps;
+        out[148 + blockIdx.x] = tiss / reps;
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -49,15 +52,16 @@ __global__ void k(int N, int n, int reps, long long* out) {
 }
 int main() {
     long long* d;
-    cudaMalloc(&d, 148 * 8);
-    long long h[1];
+    cudaMalloc(&d, 296 * 8);
+    long long h[296];
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    for (int N : {32, 96, 192, 256})
-        for (int n : {0, 1, 2, 4, 8, 16}) {
+    for (int N : {96, 256})
+        for (int n : {1, 4, 8, 16, 32, 64}) {
             k<<<148, 128, 64 * 1024>>>(N, n, 200, d);
             cudaDeviceSynchronize();
-            cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
-            printf("N=%3d n=%2d: issue->commit arrival %6lld cycles (%s)\n", N, n, h[0], cudaGetErrorString(cudaGetLastError()));
+            cudaMemcpy(h, d, 296 * 8, cudaMemcpyDeviceToHost);
+            printf("N=%3d n=%2d: issue of n MMAs %6lld cycles, issue->commit arrival %6lld cycles (%s)\n", N, n, h[148], h[0],
+                   cudaGetErrorString(cudaGetLastError()));
         }
     return 0;
 }

@@ -12,7 +12,7 @@ net.img.copy_(torch.from_numpy(synth.images(cfg, 0, B)))
 net.set_weights([torch.from_numpy(w) for w in synth.layer_weights(cfg)])
 net.front()
 L = spk.lib()
-tr = np.zeros((8, 256), np.int64)
+tr = np.zeros((12, 256), np.int64)
 names = ["mma_commit_accf", "epi_wake", "epi_done", "mma_acce_wake", "fl_wake", "fl_done"]
 for li in range(len(net.layers)):
     for rep in range(2):
@@ -28,5 +28,13 @@ for li in range(len(net.layers)):
           f"{np.median(t[3, sl.start + 4:sl.stop + 4] - t[2, sl]):.0f}  acce_wake->commit {d(3, 0):.0f}  "
           f"epi_done->fl_wake {d(2, 4):.0f}  fl_wake->fl_done {d(4, 5):.0f}")
     print("   first tiles (mma commit):", (t[0, :8]).tolist())
-    print("   stages: prod granted", np.diff(t[6, 16:24]).tolist(), " mma full-wake", np.diff(t[7, 16:24]).tolist())
+    print("   stages: prod granted", np.diff(t[6, 16:24]).tolist(), " mma stage-wake", np.diff(t[7, 16:40]).tolist())
+    print("   mma stage wakes rel. to tile acce-wake:", [(t[7, k] - t[3, 0]) for k in range(0, 12)], "tile commits:", [(t[0, k] - t[3, 0]) for k in range(0, 4)], "acce wakes:", [(t[3, k] - t[3, 0]) for k in range(0, 4)])
     print("   prod granted -> mma wake (same stage):", (t[7, 16:32] - t[6, 16:32]).tolist())
+    print("   mma wait3 duration per stage:", (t[7, 16:40] - t[9, 16:40]).tolist())
+    print("   B copy issue -> mma wake (same B stage):", (t[7, 16:40] - t[8, 16:40]).tolist())
+    print("   B copy issue deltas:", np.diff(t[8, 16:40]).tolist())
+    print("   per stage: wait3", (t[7, 16:28] - t[9, 16:28]).tolist())
+    print("   per stage: issue", (t[10, 16:28] - t[7, 16:28]).tolist())
+    print("   per stage: commits", (t[11, 16:28] - t[10, 16:28]).tolist())
+    print("   per stage: to next wait", (t[9, 17:29] - t[11, 16:28]).tolist())
