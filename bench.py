@@ -39,7 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--prec", default="exact", choices=["exact", "fp32"])
+    ap.add_argument("--prec", default="auto", choices=["auto", "exact", "event", "fp32"],
+                    help="conv engine: auto = event form for small-N layers, tcgen05 otherwise (bit-identical)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8, help="images in the oracle cpu_baseline sample")
     return ap.parse_args()
@@ -308,10 +309,11 @@ def main():
             "higher_is_better": True,
             "scaling": "strong" if forward else "weak",
             "vs_baseline": None,
-            "dtype": "u8 spikes x u8 weight digits -> s32 (exact)" if args.prec == "exact" else "f32",
+            "dtype": ("int32/int64 exact: u8 spikes x 23-bit fixed-point weights" if args.prec != "fp32" else "f32"),
             "data": "synthetic (seeded MNIST-like images, N(0.5, 0.02) initial weights)",
             "config": {"workload": f"{cfg['name']}: {cfg['about']}", "global_batch": total_imgs, "per_gpu_batch": B,
                        "T": T, "precision": args.prec,
+                       "conv_engines": {f"conv{i}": rec["prec"] for i, rec in enumerate(net.layers)},
                        "parallelism": (f"dp{world}: image shards, NCCL weight broadcast ({bcast_ms:.3f} ms, untimed)"
                                        if forward else f"replicas x{world} (no data-path collective)"),
                        "l2": "flushed between timed steps (256 MiB write)", "cuda_graph": True},

@@ -138,7 +138,14 @@ typedef enum {
      * two >= w_max), spikes as u8 {0,1}, kind::i8 MMAs with s32 accumulators;
      * potentials are the exact integer sums rounded once to fp32 (error
      * <= n_active * s * 2^-24 against the fp32-weight sum). */
-    SPK_PREC_EXACT_I8 = 1
+    SPK_PREC_EXACT_I8 = 1,
+    /* event (latency-histogram) form on CUDA cores (the paper's
+     * sparse interface): every input fires at most once, so
+     * P[t] = sum_{t' <= t} H[t'] with H[t'] the weight sum of the synapses of
+     * latency t'; only active synapses are touched.  Same fixed-point weights,
+     * integer sums, fire test and rounding as EXACT_I8: outputs are
+     * bit-identical to it.  Faster when inputs are sparse and Co is small. */
+    SPK_PREC_EVENT = 2
 } spk_precision;
 
 typedef enum {
@@ -167,7 +174,8 @@ SPK_API size_t spk_conv_workspace(const spk_conv_geom* g, spk_precision prec);
  *   ws     workspace of spk_conv_workspace(g, prec) bytes (weight digit planes).
  * Errors: SPK_ERR_ARG (null, theta < 0 or not finite, w_max <= 0),
  * SPK_ERR_SHAPE (Eq. 2 violated, sizes < 1), SPK_ERR_UNSUPPORTED (T > 254, or
- * EXACT_I8 with T > 32, Ci*Kh*Kw > 8192 or Kh,Kw > 16), SPK_ERR_WORKSPACE, SPK_ERR_CUDA. */
+ * EXACT_I8 with T > 32, Ci*Kh*Kw > 8192 or Kh,Kw > 16, or EVENT whose weight
+ * block does not fit shared memory), SPK_ERR_WORKSPACE, SPK_ERR_CUDA. */
 SPK_API spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
                     spk_precision prec, spk_epilogue epi, float theta, float w_max, void* out0,
                     void* out1, void* ws, size_t ws_bytes, spk_stream stream);

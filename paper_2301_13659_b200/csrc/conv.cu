@@ -25,7 +25,12 @@ spk_status check_geom(const spk_conv_geom* g, int& Ho, int& Wo) {
 }  // namespace
 
 extern "C" size_t spk_conv_workspace(const spk_conv_geom* g, spk_precision prec) {
-    if (!g || prec != SPK_PREC_EXACT_I8) return 0;
+    if (!g) return 0;
+    if (prec == SPK_PREC_EVENT) {
+        EvPlan e;
+        return ev_plan(*g, e) ? e.ws_bytes : 0;
+    }
+    if (prec != SPK_PREC_EXACT_I8) return 0;
     TcPlan p;
     if (!tc_plan(*g, p)) return 0;
     return p.ws_bytes;
@@ -45,8 +50,16 @@ extern "C" spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_
     SPK_CHECK(std::isfinite(theta) && theta >= 0.0f, SPK_ERR_ARG, "theta must be finite and >= 0");
     cudaStream_t s = spk::as_cuda(stream);
     if (prec == SPK_PREC_FP32) return spk_conv_fp32(lat_in, w, g, Ho, Wo, epi, theta, out0, out1, s);
-    SPK_CHECK(prec == SPK_PREC_EXACT_I8, SPK_ERR_ARG, "unknown precision %d", (int)prec);
+    SPK_CHECK(prec == SPK_PREC_EXACT_I8 || prec == SPK_PREC_EVENT, SPK_ERR_ARG, "unknown precision %d", (int)prec);
     SPK_CHECK(std::isfinite(w_max) && w_max > 0.0f, SPK_ERR_ARG, "w_max must be finite and > 0");
+    if (prec == SPK_PREC_EVENT) {
+        EvPlan e;
+        SPK_CHECK(ev_plan(*g, e), SPK_ERR_UNSUPPORTED, "EVENT: a 32-map weight block of K=%d synapses does not fit shared memory",
+                  g->Ci * g->Kh * g->Kw);
+        SPK_CHECK(ws != nullptr && ws_bytes >= e.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
+                  e.ws_bytes);
+        return spk_conv_event(lat_in, w, *g, e, epi, theta, w_max, out0, out1, ws, s);
+    }
     TcPlan p;
     SPK_CHECK(tc_plan(*g, p), SPK_ERR_UNSUPPORTED,
               "EXACT_I8 needs T <= 32, Ci*Kh*Kw <= %d, Kh,Kw <= 16, Ci*Hi*Wi < 2^24", kTcMaxK);

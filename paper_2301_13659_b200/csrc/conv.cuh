@@ -16,6 +16,16 @@ constexpr int kTcStages = 4;    // pipeline depth (A stages in TMEM, B stages in
 constexpr int kTcMaxK = 8192;   // synapses per neuron supported by the tcgen05 path
 
 bool tc_plan(const spk_conv_geom& g, TcPlan& p);
+
+// Geometry of the event (latency-histogram) path (see conv_event.cu).
+struct EvPlan {
+    int Ho, Wo, K, MB, n_mb, Co_pad, acc64, stage, pch;
+    size_t smem_bytes, ws_bytes;
+};
+bool ev_plan(const spk_conv_geom& g, EvPlan& p);
+spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const EvPlan& p,
+                          spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
+                          cudaStream_t s);
 spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const TcPlan& p,
                        spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
                        cudaStream_t s);

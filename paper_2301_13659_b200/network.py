@@ -22,6 +22,10 @@ def _nomark(name: str) -> None:
 
 class Network:
     def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "exact"):
+        """prec: "exact" (tcgen05 EXACT_I8 for every conv), "event" (latency-histogram
+        form on CUDA cores where its weight block fits), "auto" (event for small-N
+        layers, Co <= 64, tensor cores otherwise) or "fp32".  exact/event/auto give
+        bit-identical outputs."""
         self.cfg = cfg
         self.B = batch
         self.T = cfg["T"]
@@ -50,13 +54,17 @@ class Network:
             Wo = (w + 2 * L["pad"] - L["K"]) // L["stride"] + 1
             geom = spk.ConvGeom(batch, self.T, ci, h, w, L["Co"], L["K"], L["K"], L["stride"], L["stride"],
                                 L["pad"], L["pad"])
+            lp = prec
+            if prec in ("auto", "event"):
+                ok = spk.conv_workspace(geom, "event") > 0
+                lp = "event" if ok and (prec == "event" or L["Co"] <= 64) else "exact"
             rec = dict(
-                L=L, geom=geom, Ho=Ho, Wo=Wo,
+                L=L, geom=geom, Ho=Ho, Wo=Wo, prec=lp,
                 lat=torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.uint8, device=self.dev),
                 # P* (potential at the first crossing) is only needed by the trained layer
                 pstar=(torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.float32, device=self.dev)
                        if li == tl else None),
-                ws=torch.empty(max(1, spk.conv_workspace(geom, prec)), dtype=torch.uint8, device=self.dev),
+                ws=torch.empty(max(1, spk.conv_workspace(geom, lp)), dtype=torch.uint8, device=self.dev),
             )
             if L["pool"]:
                 p = L["pool"]
@@ -110,7 +118,7 @@ class Network:
     def layer(self, li: int, pstar: bool = False, mark=_nomark):
         rec = self.layers[li]
         L = rec["L"]
-        spk.conv(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=self.prec, epi="fire",
+        spk.conv(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=rec["prec"], epi="fire",
                  theta=L["theta"], w_max=1.0, out0=rec["lat"], out1=rec["pstar"] if pstar else None, ws=rec["ws"],
                  want_pstar=pstar)
         mark(f"conv{li}")

@@ -16,7 +16,7 @@ import torch
 _LIB_PATH = Path(os.environ.get("SPK_LIB_OVERRIDE", Path(__file__).resolve().parent / "libspk.so"))
 _lib = None
 
-SPK_PREC = {"fp32": 0, "exact": 1}
+SPK_PREC = {"fp32": 0, "exact": 1, "event": 2}
 SPK_EPI = {"potential": 0, "fire": 1}
 
 

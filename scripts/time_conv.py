@@ -9,7 +9,7 @@ from paper_2301_13659_b200.network import Network
 cfg = synth.load_config(sys.argv[1] if len(sys.argv) > 1 else "c2")
 tag = sys.argv[2] if len(sys.argv) > 2 else os.environ.get("SPK_LIB_OVERRIDE", "base")
 B = cfg["batch"]
-net = Network(cfg, B)
+net = Network(cfg, B, prec=os.environ.get("SPK_PREC", "exact"))
 net.img.copy_(torch.from_numpy(synth.images(cfg, 0, B)))
 net.set_weights([torch.from_numpy(w) for w in synth.layer_weights(cfg)])
 net.front()

@@ -97,21 +97,28 @@ def _conv_inputs(B, T, Ci, Hi, Wi, Co, K, dens=0.5):
     return lat, w
 
 
+def _skip_unsupported(spk, lat, w, T, s, p, prec):
+    if prec == "event" and spk.conv_workspace(spk.conv_geom(cu(lat), cu(w), T, s, p), "event") == 0:
+        pytest.skip("event path: weight block does not fit shared memory")
+
+
 @pytest.mark.parametrize("case", CONV_CASES)
-@pytest.mark.parametrize("prec", ["exact", "fp32"])
+@pytest.mark.parametrize("prec", ["exact", "fp32", "event"])
 def test_conv_potentials(spk, case, prec):
     B, T, Ci, Hi, Wi, Co, K, s, p = case
     lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K)
+    _skip_unsupported(spk, lat, w, T, s, p, prec)
     ref = oracle.conv_event(lat, T, w, (s, s), (p, p))
     got = host(spk.conv(cu(lat), cu(w), T, s, p, prec=prec, epi="potential"))
     assert_potentials(got, ref)
 
 
 @pytest.mark.parametrize("case", CONV_CASES)
-@pytest.mark.parametrize("prec", ["exact", "fp32"])
+@pytest.mark.parametrize("prec", ["exact", "fp32", "event"])
 def test_conv_fire_epilogue(spk, case, prec):
     B, T, Ci, Hi, Wi, Co, K, s, p = case
     lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K)
+    _skip_unsupported(spk, lat, w, T, s, p, prec)
     P = oracle.conv_event(lat, T, w, (s, s), (p, p))
     theta = float(np.percentile(P[:, -1], 60)) + 0.123  # fire for roughly 40 % of neurons
     ref_lat, ref_ps = lat_and_pstar(P, theta)
@@ -124,12 +131,30 @@ def test_conv_fire_epilogue(spk, case, prec):
     assert (gps[glat == T] == 0).all()
 
 
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("dens", [0.05, 0.5, 1.0])
+def test_conv_event_equals_exact_bitwise(spk, case, dens):
+    """The event (latency-histogram) form sums the same fixed-point weights exactly, so its
+    latencies and P* equal the tensor-core path's bit for bit (any density, any T)."""
+    B, T, Ci, Hi, Wi, Co, K, s, p = case
+    lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K, dens)
+    _skip_unsupported(spk, lat, w, T, s, p, "event")
+    P = oracle.conv_event(lat, T, w, (s, s), (p, p))
+    theta = float(np.percentile(P[:, -1], 60)) + 0.123
+    el, ep = spk.conv(cu(lat), cu(w), T, s, p, prec="event", epi="fire", theta=theta)
+    xl, xp = spk.conv(cu(lat), cu(w), T, s, p, prec="exact", epi="fire", theta=theta)
+    np.testing.assert_array_equal(host(el), host(xl))
+    np.testing.assert_array_equal(host(ep), host(xp))
+    np.testing.assert_array_equal(host(spk.conv(cu(lat), cu(w), T, s, p, prec="event", epi="potential")),
+                                  host(spk.conv(cu(lat), cu(w), T, s, p, prec="exact", epi="potential")))
+
+
 def test_conv_quantised_weights_exact_integers(spk):
     # binary weights (Listing 4 quantize) make potentials exact integers on every path
     lat, _ = _conv_inputs(2, 15, 30, 14, 14, 250, 3)
     w = RNG.integers(0, 2, (250, 30, 3, 3)).astype(np.float32)
     ref = oracle.conv_event(lat, 15, w, (1, 1), (1, 1))
-    for prec in ("exact", "fp32"):
+    for prec in ("exact", "fp32", "event"):
         np.testing.assert_array_equal(host(spk.conv(cu(lat), cu(w), 15, 1, 1, prec=prec, epi="potential")), ref)
 
 
@@ -325,7 +350,7 @@ def test_pipeline_c1(spk):
     assert _check_pipeline(synth.load_config("c1"), 1) == 0
 
 
-@pytest.mark.parametrize("prec", ["exact", "fp32"])
+@pytest.mark.parametrize("prec", ["exact", "fp32", "auto", "event"])
 def test_pipeline_c2_small_batch(spk, prec):
     assert _check_pipeline(synth.load_config("c2"), 12, prec=prec) <= 1
 
@@ -344,7 +369,7 @@ def test_c2_full_batch_sampled(spk):
     B, T = cfg["batch"], cfg["T"]
     imgs = synth.images(cfg, 0, B)
     Ws = synth.layer_weights(cfg)
-    net = Network(cfg, B)
+    net = Network(cfg, B, prec="auto")  # bench.py's engines: event form for conv1, tcgen05 for conv2/conv3
     net.img.copy_(cu(imgs))
     net.set_weights([cu(w) for w in Ws])
     net.capture(warmup=1)
