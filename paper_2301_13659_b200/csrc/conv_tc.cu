@@ -24,7 +24,7 @@
 //   s 2^-30 (A carries the spike as 128 = 2^7); fire iff X > floor(theta 2^30 / s);
 //   P = X s 2^-30 rounded once.
 //
-// Persistent, warp-specialised CTA (one per SM), 20 warps:
+// Persistent, warp-specialised CTA (one per SM), 20 warps (5 per scheduler: 96 registers each):
 //   warps 0-7   producers: im2col gather of latencies from the staged input
 //               band, expand to A rows, tcgen05.st into the TMEM A stage
 //               (warp w writes lane quadrant w%4, K half w/4); A = 128 [lat <= t]
@@ -35,7 +35,8 @@
 //               run of 128/TP pixels per output map
 //   warp  16    MMA issuer (one thread), TMEM allocator
 //   warp  17    B loader: cp.async.bulk of pre-packed digit planes
-//   warps 18-19 band loaders: copy the input rows a tile needs into smem
+//   warp  18    band loader: copies the input rows a tile needs into smem
+//   warp  19    flusher: writes each staged output tile, one run per output map
 // Pipelines (mbarriers): input band (1-2 buffers), K stages (8; A in TMEM,
 // B in smem), TMEM accumulators (1-2 buffers).
 #include <algorithm>
@@ -57,10 +58,10 @@ static_assert(KS == 128, "an A slot holds 4 k-steps of 32 synapses");
 constexpr int S = kTcStages;       // pipeline depth
 constexpr int kProdWarps = 8;      // warps 0-7: producers
 constexpr int kEpiWarps = 8;       // warps 8-15: epilogue (two per TMEM lane quadrant)
-constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 16: MMA issuer; 17: B loader; 18-19: band loaders
-constexpr int kLoaders = 64;
-constexpr int kFlushWarp = kMmaWarp + 4;           // warp 20: writes staged output tiles to HBM
-constexpr int kThreads = (kFlushWarp + 1) * 32;   // 672
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 16: MMA issuer; 17: B loader; 18: band loader
+constexpr int kLoaders = 32;  // one band-loader warp: 20 warps keep 96 registers per thread
+constexpr int kFlushWarp = kMmaWarp + 3;           // warp 19: writes staged output tiles to HBM
+constexpr int kThreads = (kFlushWarp + 1) * 32;   // 640
 constexpr int kNOB = 4;                            // output staging ring (tiles)
 constexpr int kLoadBatch = 8;      // independent loads in flight per band-loader thread
 constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-bit column)
@@ -255,6 +256,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
@@ -399,6 +405,7 @@ struct RoleClock {
 
 // ------------------------------------------------------------------ the kernel
 template <int EPI, bool PSTAR, int TP>
+// 20 warps: 5 per scheduler, whose 16K-register file then allows 96 registers per thread
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     constexpr int LOGTP = TP == 16 ? 4 : 5;
     constexpr int PPT = 128 / TP;
@@ -683,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (threadIdx.x == kProdWarps * 32) TRACE(1, ep_it);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
-            for (int n0 = eh * 16; n0 < ((SPK_EXP & 128) ? 0 : a.Nt); n0 += 32) {
+            for (int n0 = eh * 16; n0 < ((SPK_EXP & 128) || EPI != SPK_EPI_POTENTIAL ? 0 : a.Nt); n0 += 32) {
                 uint32_t d0[16], d1[16], d2[16];
 #if (SPK_EXP & 16)
 #pragma unroll
@@ -730,9 +737,68 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0 && !(SPK_EXP & 8192)) mbar_arrive(acce0 + 8 * buf);
+            bool released = false;
+            if (EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 128)) {
+                // 16-column chunks n0 = eh*16 + 32 i, each read as two 8-column halves; the
+                // TMEM loads of the next half overlap the threshold work on the current one,
+                // and the accumulator is released as soon as its last load has landed
+                uint32_t ra[24], rb[24];
+                auto ld8 = [&](int n0, uint32_t* r) {
+                    tmem_ld8(tbase + n0, r);
+                    tmem_ld8(tbase + a.Nt + n0, r + 8);
+                    tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
+                };
+                uint32_t mine = 0;
+                float mine_ps = 0.0f;
+                auto half = [&](const uint32_t* r, int j0) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        // digit accumulators are >= 0 (u8 x u8): two wide multiply-adds
+                        const long long X = (long long)((unsigned long long)r[16 + j] * 65536ull +
+                                                        ((unsigned long long)r[8 + j] * 256ull + r[j]));
+                        const unsigned bal = __ballot_sync(0xffffffffu, X > thq);
+                        if (j0 + j == own_col) mine = bal;
+                        if (PSTAR) {
+                            const unsigned bits = (bal >> segbase) & segmask;
+                            const int l = g.T - __popc(bits);  // fired steps are exactly t = lat .. T-1
+                            const long long Xs = __shfl_sync(0xffffffffu, X, segbase + min(l, TP - 1));
+                            if (j0 + j == own_col) mine_ps = bits ? __fmul_rn(__ll2float_rn(Xs), a.out_scale) : 0.0f;
+                        }
+                    }
+                };
+                int n0 = eh * 16;
+                if (n0 < a.Nt) {
+                    ld8(n0, ra);
+                    tmem_wait_ld();
+                }
+                for (; n0 < a.Nt; n0 += 32) {
+                    ld8(n0 + 8, rb);
+                    half(ra, 0);
+                    tmem_wait_ld();
+                    const bool more = n0 + 32 < a.Nt;
+                    if (more) {
+                        ld8(n0 + 32, ra);
+                    } else if (!(SPK_EXP & 8192)) {  // every TMEM read of this buffer has landed
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(acce0 + 8 * buf);
+                        released = true;
+                    }
+                    half(rb, 8);
+                    if (more) tmem_wait_ld();
+                    if (own_lane) {  // stage (map, pixel) -> smem
+                        const unsigned bits = (mine >> (own_seg * TP)) & segmask;
+                        const int ol = (n0 + own_col) * PPT + own_pix;
+                        ob_lat[ob * a.Nt * PPT + ol] = (uint8_t)(g.T - __popc(bits));
+                        if (PSTAR) ob_ps[ob * a.Nt * PPT + ol] = mine_ps;
+                    }
+                }
+            }
+            if (!released) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0 && !(SPK_EXP & 8192)) mbar_arrive(acce0 + 8 * buf);
+            }
             if (threadIdx.x == kProdWarps * 32) TRACE(2, ep_it);
             ++ep_it;
             if (EPI != SPK_EPI_POTENTIAL) {  // hand the staged tile to the flusher warp
@@ -899,7 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     } else if (warp < kFlushWarp) {
         // ======================= input band loaders =======================
         RoleClock rc(a.prof != 0);
-        const int lt = threadIdx.x - (kMmaWarp + 2) * 32;  // 0..63
+        const int lt = threadIdx.x - (kMmaWarp + 2) * 32;  // 0..kLoaders-1
         const size_t plane = (size_t)g.Hi * g.Wi;
         TileIter ti;
         ti.init(a);
