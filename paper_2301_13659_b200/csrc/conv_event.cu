@@ -12,7 +12,7 @@
 // rounding of the potential — so the outputs are bit-identical to the tensor path.
 //
 // Grid (pixel chunks, blocks of 32 maps, B); small samples are staged whole in shared
-// memory and one CTA covers all their pixels.  8 warps, each owns every 8th pixel of
+// memory and one CTA covers all their pixels.  16 warps, each owns every 16th pixel of
 // the chunk; a lane owns one output map.  Per pixel the warp
 // (1) compacts the active synapses of the receptive field into a shared list
 // (ballot), (2) adds each one's weight column into per-lane latency bins H[t][lane]
@@ -25,7 +25,7 @@
 
 namespace {
 
-constexpr int kEvThreads = 256, kEvWarps = kEvThreads / 32, kMB = 32;
+constexpr int kEvThreads = 512, kEvWarps = kEvThreads / 32, kMB = 32;
 constexpr int kStageMax = 48 * 1024;  // input samples up to this many bytes are staged in smem
 constexpr int kPchMax = 4096;         // output pixels per CTA (a whole sample when it fits)
 
@@ -76,7 +76,7 @@ __host__ __device__ inline EvSmem ev_smem(int K, int T, int accb, int pch, size_
 }
 
 // ACC = uint32_t when K * 2^23 < 2^32, else unsigned long long
-template <typename ACC, int EPI, bool PSTAR>
+template <typename ACC, int EPI, bool PSTAR, bool SMALLK>
 __global__ void __launch_bounds__(kEvThreads) conv_event_kernel(const EvArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const spk_conv_geom& g = a.g;
@@ -123,32 +123,63 @@ __global__ void __launch_bounds__(kEvThreads) conv_event_kernel(const EvArgs a) 
     ACC* h = H + (size_t)warp * T * 32;
     for (int t = 0; t < T; ++t) h[t * 32 + lane] = 0;
     const uint32_t* wcol = sq + lane;
-    for (int pl = warp; pl < npix; pl += kEvWarps) {
+    // small receptive fields: this lane's synapse offsets stay in registers
+    constexpr int kRegChunks = 8;  // K <= 256
+    int rko[kRegChunks], rij[kRegChunks];
+    if (SMALLK) {
+#pragma unroll
+        for (int c = 0; c < kRegChunks; ++c) {
+            const int k = c * 32 + lane;
+            rko[c] = k < K ? koff[k] : 0;
+            rij[c] = k < K ? kij[k] : 0xFFFF;  // out of the window: never active
+        }
+    }
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+    const int pstep = kEvWarps;
+    int pl = warp;
+    int y = (p0 + pl) / a.Wo, x = (p0 + pl) - y * a.Wo;  // advanced incrementally
+    for (; pl < npix; pl += pstep) {
         const int p = p0 + pl;
-        const int y = p / a.Wo, x = p - y * a.Wo;
         const int y0 = y * g.Sh - g.Ph, x0 = x * g.Sw - g.Pw;
         const ptrdiff_t org = (ptrdiff_t)y0 * g.Wi + x0;
         // (1) compact the active synapses of the receptive field; list entry =
         //     (byte offset of the weight row k * 128) << 8 | latency
         const bool interior = y0 >= 0 && x0 >= 0 && y0 + g.Kh <= g.Hi && x0 + g.Kw <= g.Wi;  // warp-uniform
         int n = 0;
-        for (int k0 = 0; k0 < K; k0 += 32) {
-            const int k = k0 + lane;
-            int lat = T;
-            if (k < K) {
+        auto take = [&](int k, int lat) {
+            const bool act = lat < T;
+            const unsigned m = __ballot_sync(0xffffffffu, act);
+            if (act) list[n + __popc(m & lanemask_lt)] = ((uint32_t)k << 15) | (uint32_t)lat;
+            n += __popc(m);
+        };
+        if (SMALLK) {
+#pragma unroll
+            for (int c = 0; c < kRegChunks; ++c) {
+                if (c * 32 >= K) break;
+                int lat = T;
                 if (interior) {
-                    lat = src[org + koff[k]];
+                    if (c * 32 + lane < K) lat = src[org + rko[c]];
                 } else {
+                    const int iy = y0 + (rij[c] >> 8), ix = x0 + (rij[c] & 255);
+                    if (c * 32 + lane < K && (unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
+                        lat = src[org + rko[c]];  // padded taps never fire
+                }
+                take(c * 32 + lane, lat);
+            }
+        } else {
+            for (int k0 = 0; k0 < K; k0 += 32) {
+                const int k = k0 + lane;
+                int lat = T;
+                if (k < K) {
                     const int ij = kij[k], iy = y0 + (ij >> 8), ix = x0 + (ij & 255);
                     if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
                         lat = src[org + koff[k]];  // padded taps never fire
                 }
+                take(k, lat);
             }
-            const bool act = lat < T;
-            const unsigned m = __ballot_sync(0xffffffffu, act);
-            if (act) list[n + __popc(m & ((1u << lane) - 1u))] = ((uint32_t)k << 15) | (uint32_t)lat;
-            n += __popc(m);
         }
+        x += pstep;
+        while (x >= a.Wo) x -= a.Wo, ++y;
         __syncwarp();
         // (2) latency bins: H[lat] += W_k (exact integer sums); the bins were zeroed by
         //     the previous pixel's prefix pass (or at start)
@@ -179,6 +210,16 @@ __global__ void __launch_bounds__(kEvThreads) conv_event_kernel(const EvArgs a) 
                     static_cast<float*>(a.out0)[(((size_t)b * T + t) * g.Co + o) * a.HWo + p] =
                         __fmul_rn(__ll2float_rn((long long)S * 128ll), a.out_scale);
             }
+        } else if (!PSTAR) {
+            // potentials are non-decreasing in t (W >= 0), so the steps at or below the
+            // threshold are exactly t < lat: lat = their count
+            int lat = 0;
+            for (int t = 0; t < T; ++t) {
+                S += h[t * 32 + lane];
+                h[t * 32 + lane] = 0;
+                lat += (S <= (ACC)a.th);
+            }
+            olat[lane * a.pch + pl] = (uint8_t)lat;
         } else {
             int lat = T;
             ACC Sf = 0;
@@ -211,7 +252,7 @@ __global__ void __launch_bounds__(kEvThreads) conv_event_kernel(const EvArgs a) 
 
 template <typename ACC, int EPI, bool PSTAR>
 spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
-    auto k = conv_event_kernel<ACC, EPI, PSTAR>;
+    auto k = a.K <= 256 ? conv_event_kernel<ACC, EPI, PSTAR, true> : conv_event_kernel<ACC, EPI, PSTAR, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return spk::launched("conv_event_kernel(attr)");
     k<<<grid, kEvThreads, smem, s>>>(a);
