@@ -19,7 +19,7 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p);
 
 // Geometry of the event (latency-histogram) path (see conv_event.cu).
 struct EvPlan {
-    int Ho, Wo, K, MB, n_mb, Co_pad, acc64, stage, pch;
+    int Ho, Wo, K, MB, n_mb, Co_pad, acc64, stage, pch, nw;
     size_t smem_bytes, ws_bytes;
 };
 bool ev_plan(const spk_conv_geom& g, EvPlan& p);

@@ -25,7 +25,7 @@
 
 namespace {
 
-constexpr int kEvThreads = 512, kEvWarps = kEvThreads / 32, kMB = 32;
+constexpr int kMB = 32;  // maps per CTA (one per lane); warps per CTA NW = 16, or 8 for large footprints
 constexpr int kStageMax = 48 * 1024;  // input samples up to this many bytes are staged in smem
 constexpr int kPchMax = 4096;         // output pixels per CTA (a whole sample when it fits)
 
@@ -35,7 +35,7 @@ struct EvArgs {
     void* out0;
     float* out1;
     spk_conv_geom g;
-    int Ho, Wo, HWo, K, Co_pad, pch, stage;
+    int Ho, Wo, HWo, K, Co_pad, pch, stage, nw;
     uint32_t th;          // fire iff S > th  (S = sum of q; th = floor(theta 2^30 / s) >> 7)
     float out_scale;      // P = (128 S) * out_scale  (identical to the tensor path's rounding)
 };
@@ -61,28 +61,29 @@ struct EvSmem {
     size_t sq, koff, kij, in, lists, H, olat, ops, total;
 };
 __host__ __device__ inline size_t ev_al(size_t x) { return (x + 15) & ~(size_t)15; }
-__host__ __device__ inline EvSmem ev_smem(int K, int T, int accb, int pch, size_t in_bytes, bool pstar) {
+__host__ __device__ inline EvSmem ev_smem(int K, int T, int accb, int pch, size_t in_bytes, bool pstar, int nw) {
     EvSmem m;
     m.sq = 0;
     m.koff = ev_al(m.sq + (size_t)K * kMB * 4);
     m.kij = ev_al(m.koff + (size_t)K * 4);
     m.in = ev_al(m.kij + (size_t)K * 2);
     m.lists = ev_al(m.in + in_bytes);
-    m.H = ev_al(m.lists + (size_t)kEvWarps * ((K + 3) & ~3) * 4);
-    m.olat = ev_al(m.H + (size_t)kEvWarps * T * 32 * accb);
+    m.H = ev_al(m.lists + (size_t)nw * ((K + 3) & ~3) * 4);
+    m.olat = ev_al(m.H + (size_t)nw * T * 32 * accb);
     m.ops = ev_al(m.olat + (size_t)kMB * pch);
     m.total = ev_al(m.ops + (pstar ? (size_t)kMB * pch * 4 : 0));
     return m;
 }
 
 // ACC = uint32_t when K * 2^23 < 2^32, else unsigned long long
-template <typename ACC, int EPI, bool PSTAR, bool SMALLK>
-__global__ void __launch_bounds__(kEvThreads) conv_event_kernel(const EvArgs a) {
+template <typename ACC, int EPI, bool PSTAR, bool SMALLK, int NW>
+__global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
+    constexpr int kEvThreads = NW * 32, kEvWarps = NW;
     extern __shared__ __align__(16) unsigned char sm[];
     const spk_conv_geom& g = a.g;
     const int K = a.K, T = g.T;
     const size_t HWi = (size_t)g.Hi * g.Wi;
-    const EvSmem ms = ev_smem(K, T, (int)sizeof(ACC), a.pch, a.stage ? (size_t)g.Ci * HWi : 0, PSTAR);
+    const EvSmem ms = ev_smem(K, T, (int)sizeof(ACC), a.pch, a.stage ? (size_t)g.Ci * HWi : 0, PSTAR, NW);
     uint32_t* sq = reinterpret_cast<uint32_t*>(sm + ms.sq);        // [K][32] weight columns
     int* koff = reinterpret_cast<int*>(sm + ms.koff);              // [K] c*Hi*Wi + i*Wi + j
     uint16_t* kij = reinterpret_cast<uint16_t*>(sm + ms.kij);      // [K] (i << 8) | j
@@ -252,10 +253,11 @@ __global__ void __launch_bounds__(kEvThreads) conv_event_kernel(const EvArgs a) 
 
 template <typename ACC, int EPI, bool PSTAR>
 spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
-    auto k = a.K <= 256 ? conv_event_kernel<ACC, EPI, PSTAR, true> : conv_event_kernel<ACC, EPI, PSTAR, false>;
+    auto k = a.nw == 16 ? (a.K <= 256 ? conv_event_kernel<ACC, EPI, PSTAR, true, 16> : conv_event_kernel<ACC, EPI, PSTAR, false, 16>)
+                        : (a.K <= 256 ? conv_event_kernel<ACC, EPI, PSTAR, true, 8> : conv_event_kernel<ACC, EPI, PSTAR, false, 8>);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return spk::launched("conv_event_kernel(attr)");
-    k<<<grid, kEvThreads, smem, s>>>(a);
+    k<<<grid, a.nw * 32, smem, s>>>(a);
     return spk::launched("conv_event_kernel");
 }
 
@@ -272,8 +274,13 @@ bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
     const size_t in_bytes = (size_t)g.Ci * g.Hi * g.Wi;
     p.stage = in_bytes <= (size_t)kStageMax ? 1 : 0;
     p.pch = std::min(HWo, p.stage ? kPchMax : 256);
-    // smem with P* staging (the larger of the two epilogue variants)
-    p.smem_bytes = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, p.stage ? in_bytes : 0, true).total;
+    // smem with P* staging (the larger of the two epilogue variants); 16 warps when it fits
+    p.nw = 16;
+    p.smem_bytes = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, p.stage ? in_bytes : 0, true, 16).total;
+    if (p.smem_bytes > 200 * 1024) {
+        p.nw = 8;
+        p.smem_bytes = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, p.stage ? in_bytes : 0, true, 8).total;
+    }
     if (p.smem_bytes > 200 * 1024) return false;
     p.n_mb = (g.Co + kMB - 1) / kMB;
     p.Co_pad = p.n_mb * kMB;
@@ -318,7 +325,8 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     const dim3 grid((unsigned)((a.HWo + p.pch - 1) / p.pch), (unsigned)p.n_mb, (unsigned)g.B);
     const bool ps = out1 != nullptr && epi == SPK_EPI_FIRE;
     const size_t in_bytes = p.stage ? (size_t)g.Ci * g.Hi * g.Wi : 0;
-    const size_t smem = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, in_bytes, ps).total;
+    a.nw = p.nw;
+    const size_t smem = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, in_bytes, ps, p.nw).total;
     if (epi == SPK_EPI_POTENTIAL)
         return p.acc64 ? launch_ev<unsigned long long, SPK_EPI_POTENTIAL, false>(a, grid, smem, s)
                        : launch_ev<uint32_t, SPK_EPI_POTENTIAL, false>(a, grid, smem, s);
