@@ -1179,7 +1179,11 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     const int acc_cols = 512 - 4 * kACols;  // 384
     // a reduction that fits the TMEM A ring is produced once per M tile and kept for every
     // N tile; N tiles of 64 then give two accumulator buffers (epilogue overlaps the MMAs)
-    p.retain = (p.nks <= 4 && g.Co > 64) ? 1 : 0;
+    static const int retain_ok = [] {
+        const char* e = std::getenv("SPK_CONV_RETAIN");  // tuning knob: 0 disables A retention
+        return e ? std::atoi(e) : 1;
+    }();
+    p.retain = (retain_ok && p.nks <= 4 && g.Co > 64) ? 1 : 0;
     if (p.retain) {
         p.Nt = 64;
     } else if (g.Co <= 64) {
