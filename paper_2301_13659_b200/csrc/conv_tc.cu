@@ -99,6 +99,10 @@ struct TcArgs {
     int WiP, HiP;  // padded input width/height: the staged region includes the zero-padding halo
     long long total_tiles;
     long long theta_q;  // fire iff X > theta_q
+    // small reductions (digit sums < 2^24): fire iff d2 + ((d1*256 + d0 + thC) >> 16) > thH,
+    // the same test in 32-bit arithmetic (thH = theta_q >> 16, thC = 65535 - (theta_q & 65535))
+    int small_x, thH;
+    uint32_t thC;
     float out_scale;
     uint32_t b_off, lc_off, kt_off, rg_off, ob_off, bar_off;  // smem carve-up
     int prof;
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const bool rvalid = p0 + pix < a.HWo && t < g.T;
             // padded rows never fire: fold the row mask into the threshold
             const long long thq = rvalid ? a.theta_q : 0x7fffffffffffffffll;
+            const int thh = rvalid ? a.thH : 0x7fffffff;
             // the leader probes the staging slot and the accumulator together, the group sleeps
             if (threadIdx.x == kProdWarps * 32)
                 rc.wait3(fls0 + 8 * ob, ob_ph ^ 1u, EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 65536), accf0 + 8 * buf, acc_ph,
@@ -751,6 +756,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 uint32_t mine = 0;
                 float mine_ps = 0.0f;
                 auto half = [&](const uint32_t* r, int j0) {
+                    if (a.small_x) {  // 32-bit form of X > theta_q (see TcArgs)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const uint32_t tl = r[8 + j] * 256u + r[j] + a.thC;
+                            const unsigned bal = __ballot_sync(0xffffffffu, (int)(r[16 + j] + (tl >> 16)) > thh);
+                            if (j0 + j == own_col) mine = bal;
+                            if (PSTAR) {
+                                const unsigned bits = (bal >> segbase) & segmask;
+                                const int l = g.T - __popc(bits);  // fired steps are exactly t = lat .. T-1
+                                const int src = segbase + min(l, TP - 1);
+                                const uint32_t d2s = __shfl_sync(0xffffffffu, r[16 + j], src);
+                                const uint32_t tls = __shfl_sync(0xffffffffu, tl, src);
+                                const long long Xs = (long long)d2s * 65536ll + (long long)(tls - a.thC);
+                                if (j0 + j == own_col) mine_ps = bits ? __fmul_rn(__ll2float_rn(Xs), a.out_scale) : 0.0f;
+                            }
+                        }
+                        return;
+                    }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         // digit accumulators are >= 0 (u8 x u8): two wide multiply-adds
@@ -1316,6 +1339,11 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     // fire iff X * s 2^-23 > theta  <=>  X > floor(theta 2^23 / s)   (X integer, scaling exact)
     // spikes enter the MMA as 128: X is in units of s 2^-30
     a.theta_q = (long long)std::floor((double)theta * (1073741824.0 / scale));
+    // digit sums are at most 128 * 255 * K: the 32-bit test needs them below 2^24
+    // (and d1*256 + d0 + thC below 2^32)
+    a.small_x = ((double)p.K * 32640.0 * 257.0 + 65536.0 < 4294967296.0 && a.theta_q < (1ll << 46)) ? 1 : 0;
+    a.thH = (int)(a.theta_q >> 16);
+    a.thC = 65535u - (uint32_t)(a.theta_q & 65535);
     a.out_scale = (float)(scale / 1073741824.0);
     static const int prof_env = [] {
         const char* e = std::getenv("SPK_CONV_PROF");
