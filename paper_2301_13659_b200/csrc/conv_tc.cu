@@ -754,22 +754,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
                 };
                 uint32_t mine = 0;
-                float mine_ps = 0.0f;
-                auto half = [&](const uint32_t* r, int j0) {
+                // P*: the lane holding a (pixel, map)'s first crossing (its bit set, the previous
+                // step's clear) writes the potential straight into the staging tile — no shuffle
+                const unsigned segstart = (TP == 16) ? 0x00010001u : 0x1u;
+                float* ps_tile = ob_ps + ob * a.Nt * PPT + pix;
+                auto half = [&](const uint32_t* r, int j0, int c0) {  // c0: tile column of r[0]
                     if (a.small_x) {  // 32-bit form of X > theta_q (see TcArgs)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             const uint32_t tl = r[8 + j] * 256u + r[j] + a.thC;
                             const unsigned bal = __ballot_sync(0xffffffffu, (int)(r[16 + j] + (tl >> 16)) > thh);
                             if (j0 + j == own_col) mine = bal;
-                            if (PSTAR) {
-                                const unsigned bits = (bal >> segbase) & segmask;
-                                const int l = g.T - __popc(bits);  // fired steps are exactly t = lat .. T-1
-                                const int src = segbase + min(l, TP - 1);
-                                const uint32_t d2s = __shfl_sync(0xffffffffu, r[16 + j], src);
-                                const uint32_t tls = __shfl_sync(0xffffffffu, tl, src);
-                                const long long Xs = (long long)d2s * 65536ll + (long long)(tls - a.thC);
-                                if (j0 + j == own_col) mine_ps = bits ? __fmul_rn(__ll2float_rn(Xs), a.out_scale) : 0.0f;
+                            if (PSTAR && ((bal & ~((bal << 1) & ~segstart)) >> lane) & 1u) {
+                                const long long X = (long long)r[16 + j] * 65536ll + (long long)(tl - a.thC);
+                                ps_tile[(c0 + j) * PPT] = __fmul_rn(__ll2float_rn(X), a.out_scale);
                             }
                         }
                         return;
@@ -781,12 +779,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                                                         ((unsigned long long)r[8 + j] * 256ull + r[j]));
                         const unsigned bal = __ballot_sync(0xffffffffu, X > thq);
                         if (j0 + j == own_col) mine = bal;
-                        if (PSTAR) {
-                            const unsigned bits = (bal >> segbase) & segmask;
-                            const int l = g.T - __popc(bits);  // fired steps are exactly t = lat .. T-1
-                            const long long Xs = __shfl_sync(0xffffffffu, X, segbase + min(l, TP - 1));
-                            if (j0 + j == own_col) mine_ps = bits ? __fmul_rn(__ll2float_rn(Xs), a.out_scale) : 0.0f;
-                        }
+                        if (PSTAR && ((bal & ~((bal << 1) & ~segstart)) >> lane) & 1u)
+                            ps_tile[(c0 + j) * PPT] = __fmul_rn(__ll2float_rn(X), a.out_scale);
                     }
                 };
                 int n0 = eh * 16;
@@ -796,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 }
                 for (; n0 < a.Nt; n0 += 32) {
                     ld8(n0 + 8, rb);
-                    half(ra, 0);
+                    half(ra, 0, n0);
                     tmem_wait_ld();
                     const bool more = n0 + 32 < a.Nt;
                     if (more) {
@@ -807,13 +801,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                         if (lane == 0) mbar_arrive(acce0 + 8 * buf);
                         released = true;
                     }
-                    half(rb, 8);
+                    half(rb, 8, n0 + 8);
                     if (more) tmem_wait_ld();
                     if (own_lane) {  // stage (map, pixel) -> smem
                         const unsigned bits = (mine >> (own_seg * TP)) & segmask;
                         const int ol = (n0 + own_col) * PPT + own_pix;
                         ob_lat[ob * a.Nt * PPT + ol] = (uint8_t)(g.T - __popc(bits));
-                        if (PSTAR) ob_ps[ob * a.Nt * PPT + ol] = mine_ps;
+                        if (PSTAR && bits == 0) ob_ps[ob * a.Nt * PPT + ol] = 0.0f;  // never fired
                     }
                 }
             }

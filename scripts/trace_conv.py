@@ -38,3 +38,9 @@ for li in range(len(net.layers)):
     print("   per stage: issue", (t[10, 16:28] - t[7, 16:28]).tolist())
     print("   per stage: commits", (t[11, 16:28] - t[10, 16:28]).tolist())
     print("   per stage: to next wait", (t[9, 17:29] - t[11, 16:28]).tolist())
+    gpt = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # hand-offs per tile (to line up tile boundaries)
+    if gpt:
+        for i in range(1, 4):
+            c, ew, ed, mw0, mw1 = t[0, i - 1], t[1, i - 1], t[2, i - 1], t[9, i * gpt], t[7, i * gpt]
+            print(f"   tile {i-1}->{i}: accf commit issued {c}, epi wake +{ew - c}, epi done +{ed - c}, "
+                  f"MMA starts waiting +{mw0 - c}, MMA wakes +{mw1 - c}")
