@@ -180,6 +180,18 @@ SPK_API spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_con
                     spk_precision prec, spk_epilogue epi, float theta, float w_max, void* out0,
                     void* out1, void* ws, size_t ws_bytes, spk_stream stream);
 
+/* spk_conv_fire_pool — spk_conv(FIRE) followed by spk_pool (Eq. 3) on its latency
+ * map, fused (Listing 5 `fire` then `pool`): out [dev] u8 pooled lat
+ * [B][Co][Hp][Wp], Hp = floor((Ho + 2Ph - Lh)/Sh) + 1; the unpooled map is never
+ * written and no P* is produced (layers that are not trained need neither).
+ * Supported for prec = SPK_PREC_EVENT when a whole output map of a sample fits one
+ * CTA — query spk_conv_fire_pool_supported (1 = yes).  ws as spk_conv(EVENT).
+ * Errors: as spk_conv; SPK_ERR_UNSUPPORTED when not supported. */
+SPK_API int spk_conv_fire_pool_supported(const spk_conv_geom* g, spk_precision prec, const spk_pool_geom* pool);
+SPK_API spk_status spk_conv_fire_pool(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
+                                      spk_precision prec, float theta, float w_max, const spk_pool_geom* pool,
+                                      uint8_t* out, void* ws, size_t ws_bytes, spk_stream stream);
+
 /* spk_fire — IF activation on materialised potentials (Listing 3
  * `spyker.fire(data, th)`): lat[b][c][y][x] = first t with pot[b][t][c][y][x] >
  * theta (T if none), pstar (nullable) = pot at that step (0 if never).

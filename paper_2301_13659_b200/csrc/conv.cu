@@ -68,6 +68,38 @@ extern "C" spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_
     return spk_conv_tc(lat_in, w, *g, p, epi, theta, w_max, out0, out1, ws, s);
 }
 
+extern "C" int spk_conv_fire_pool_supported(const spk_conv_geom* g, spk_precision prec, const spk_pool_geom* pool) {
+    if (!g || !pool || prec != SPK_PREC_EVENT) return 0;
+    EvPlan e;
+    if (!ev_plan(*g, e)) return 0;
+    return e.stage && e.pch == e.Ho * e.Wo && pool->Lh >= 1 && pool->Lw >= 1 && pool->Sh >= 1 && pool->Sw >= 1 &&
+                   pool->Ph >= 0 && pool->Pw >= 0 && e.Ho + 2 * pool->Ph >= pool->Lh && e.Wo + 2 * pool->Pw >= pool->Lw
+               ? 1
+               : 0;
+}
+
+extern "C" spk_status spk_conv_fire_pool(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
+                                         spk_precision prec, float theta, float w_max, const spk_pool_geom* pool,
+                                         uint8_t* out, void* ws, size_t ws_bytes, spk_stream stream) {
+    spk::clear_error();
+    int Ho = 0, Wo = 0;
+    spk_status st = check_geom(g, Ho, Wo);
+    if (st != SPK_OK) return st;
+    SPK_CHECK_PTR(lat_in);
+    SPK_CHECK_PTR(w);
+    SPK_CHECK_PTR(pool);
+    SPK_CHECK_PTR(out);
+    SPK_CHECK(std::isfinite(theta) && theta >= 0.0f, SPK_ERR_ARG, "theta must be finite and >= 0");
+    SPK_CHECK(std::isfinite(w_max) && w_max > 0.0f, SPK_ERR_ARG, "w_max must be finite and > 0");
+    SPK_CHECK(spk_conv_fire_pool_supported(g, prec, pool), SPK_ERR_UNSUPPORTED,
+              "fused fire+pool needs prec=EVENT with a whole sample per CTA and a valid pool geometry (Eq. 3)");
+    EvPlan e;
+    ev_plan(*g, e);
+    SPK_CHECK(ws != nullptr && ws_bytes >= e.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
+              e.ws_bytes);
+    return spk_conv_event(lat_in, w, *g, e, SPK_EPI_FIRE, theta, w_max, out, nullptr, ws, spk::as_cuda(stream), pool);
+}
+
 extern "C" spk_status spk_conv_status(const void* ws, int* flag_out, spk_stream stream) {
     spk::clear_error();
     SPK_CHECK_PTR(ws);

@@ -25,7 +25,7 @@ struct EvPlan {
 bool ev_plan(const spk_conv_geom& g, EvPlan& p);
 spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const EvPlan& p,
                           spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
-                          cudaStream_t s);
+                          cudaStream_t s, const spk_pool_geom* pool = nullptr);
 spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const TcPlan& p,
                        spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
                        cudaStream_t s);

@@ -36,6 +36,8 @@ struct EvArgs {
     float* out1;
     spk_conv_geom g;
     int Ho, Wo, HWo, K, Co_pad, pch, stage, nw;
+    int pool, Hp, Wp;   // fused pooling (Eq. 3) of the latency map in the write-out: out0 = pooled lat
+    spk_pool_geom pg;
     uint32_t th;          // fire iff S > th  (S = sum of q; th = floor(theta 2^30 / s) >> 7)
     float out_scale;      // P = (128 S) * out_scale  (identical to the tensor path's rounding)
 };
@@ -239,6 +241,25 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     }
     if (EPI == SPK_EPI_POTENTIAL) return;
     __syncthreads();
+    if (a.pool) {  // whole sample staged: window minimum of latencies (Eq. 3), padding never fires
+        const int HWp = a.Hp * a.Wp;
+        for (int r = warp; r < kMB; r += kEvWarps) {
+            const int om = m0 + r;
+            if (om >= g.Co) continue;
+            uint8_t* dl = static_cast<uint8_t*>(a.out0) + ((size_t)b * g.Co + om) * HWp;
+            const uint8_t* ml = olat + r * a.pch;
+            for (int q = lane; q < HWp; q += 32) {
+                const int py = q / a.Wp, px = q - py * a.Wp;
+                const int y0 = py * a.pg.Sh - a.pg.Ph, x0 = px * a.pg.Sw - a.pg.Pw;
+                int m = T;
+                for (int i = max(0, -y0); i < a.pg.Lh && y0 + i < a.Ho; ++i)
+                    for (int j = max(0, -x0); j < a.pg.Lw && x0 + j < a.Wo; ++j)
+                        m = min(m, (int)ml[(y0 + i) * a.Wo + x0 + j]);
+                dl[q] = (uint8_t)m;
+            }
+        }
+        return;
+    }
     // coalesced write-out: one run of npix latencies (and P*) per map
     for (int r = warp; r < kMB; r += kEvWarps) {
         const int om = m0 + r;
@@ -291,7 +312,7 @@ bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
 
 spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const EvPlan& p,
                           spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
-                          cudaStream_t s) {
+                          cudaStream_t s, const spk_pool_geom* pool) {
     // same scale and fixed point as the tensor path: s = smallest power of two >= w_max
     int ex = 0;
     std::frexp((double)w_max, &ex);
@@ -319,6 +340,12 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     a.Co_pad = p.Co_pad;
     a.pch = p.pch;
     a.stage = p.stage;
+    if (pool) {  // caller checked: FIRE, whole sample in one CTA
+        a.pool = 1;
+        a.pg = *pool;
+        a.Hp = (p.Ho + 2 * pool->Ph - pool->Lh) / pool->Sh + 1;
+        a.Wp = (p.Wo + 2 * pool->Pw - pool->Lw) / pool->Sw + 1;
+    }
     const long long theta_q = (long long)std::floor((double)theta * (1073741824.0 / scale));  // tensor path's
     a.th = (uint32_t)std::min<long long>(theta_q >> 7, 0xffffffffll);
     a.out_scale = (float)(scale / 1073741824.0);

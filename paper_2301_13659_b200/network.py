@@ -66,6 +66,8 @@ class Network:
                        if li == tl else None),
                 ws=torch.empty(max(1, spk.conv_workspace(geom, lp)), dtype=torch.uint8, device=self.dev),
             )
+            rec["fused_pool"] = bool(L["pool"]) and li != tl and lp == "event" and spk.conv_fire_pool_supported(
+                geom, lp, L["pool"]["kernel"], L["pool"]["stride"], L["pool"]["pad"])
             if L["pool"]:
                 p = L["pool"]
                 Hp = (Ho + 2 * p["pad"] - p["kernel"]) // p["stride"] + 1
@@ -118,6 +120,13 @@ class Network:
     def layer(self, li: int, pstar: bool = False, mark=_nomark):
         rec = self.layers[li]
         L = rec["L"]
+        if rec["fused_pool"] and not pstar:  # layer output only feeds the next layer: conv + pool fused
+            p = L["pool"]
+            spk.conv_fire_pool(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=rec["prec"],
+                               theta=L["theta"], w_max=1.0, pool_kernel=p["kernel"], pool_stride=p["stride"],
+                               pool_pad=p["pad"], out=rec["pooled"], ws=rec["ws"])
+            mark(f"conv{li}")
+            return
         spk.conv(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=rec["prec"], epi="fire",
                  theta=L["theta"], w_max=1.0, out0=rec["lat"], out1=rec["pstar"] if pstar else None, ws=rec["ws"],
                  want_pstar=pstar)

@@ -41,7 +41,7 @@ EXPORTS = [
     "spk_last_error", "spk_abi_version", "spk_last_kernel", "spk_launch_count", "spk_dog", "spk_gabor",
     "spk_rank_code_workspace", "spk_rank_code", "spk_conv_workspace", "spk_conv", "spk_fire", "spk_pool",
     "spk_inhibit", "spk_wta", "spk_stdp_workspace", "spk_stdp", "spk_rstdp_route", "spk_gather",
-    "spk_lat_to_dense", "spk_dense_to_lat", "spk_conv_status",
+    "spk_lat_to_dense", "spk_dense_to_lat", "spk_conv_status", "spk_conv_fire_pool_supported", "spk_conv_fire_pool",
 ]
 
 
@@ -76,6 +76,8 @@ def lib():
             "spk_lat_to_dense": ([V, I, I, Z, V, V], I),
             "spk_dense_to_lat": ([V, I, I, Z, V, V, V], I),
             "spk_conv_status": ([V, ctypes.POINTER(I), V], I),
+            "spk_conv_fire_pool_supported": ([ctypes.POINTER(ConvGeom), I, ctypes.POINTER(PoolGeom)], I),
+            "spk_conv_fire_pool": ([V, V, ctypes.POINTER(ConvGeom), I, F, F, ctypes.POINTER(PoolGeom), V, V, Z, V], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -225,6 +227,39 @@ def pool(lat: torch.Tensor, T: int, kernel, stride=None, pad=0, out=None) -> tor
     if out is None:
         out = torch.empty((B, C, Ho, Wo), dtype=torch.uint8, device=lat.device)
     _check("spk_pool", lib().spk_pool(_p(lat), B, C, H, W, T, ctypes.byref(geom), _p(out), _s()))
+    return out
+
+
+def _pool_geom(kernel, stride=None, pad=0):
+    k = kernel if isinstance(kernel, (tuple, list)) else (kernel, kernel)
+    s = stride if stride is not None else k
+    s = s if isinstance(s, (tuple, list)) else (s, s)
+    p = pad if isinstance(pad, (tuple, list)) else (pad, pad)
+    return PoolGeom(k[0], k[1], s[0], s[1], p[0], p[1])
+
+
+def conv_fire_pool_supported(g: ConvGeom, prec: str, kernel, stride=None, pad=0) -> bool:
+    return bool(lib().spk_conv_fire_pool_supported(ctypes.byref(g), SPK_PREC[prec],
+                                                   ctypes.byref(_pool_geom(kernel, stride, pad))))
+
+
+def conv_fire_pool(lat_in: torch.Tensor, w: torch.Tensor, T: int, stride=1, pad=0, prec: str = "event",
+                   theta: float = 0.0, w_max: float = 1.0, pool_kernel=2, pool_stride=None, pool_pad=0,
+                   out=None, ws=None) -> torch.Tensor:
+    """spk_conv(FIRE) + spk_pool fused: pooled latencies [B][Co][Hp][Wp]."""
+    g = conv_geom(lat_in, w, T, stride, pad)
+    Ho, Wo = conv_out_hw(g)
+    pg = _pool_geom(pool_kernel, pool_stride, pool_pad)
+    Hp, Wp = (Ho + 2 * pg.Ph - pg.Lh) // pg.Sh + 1, (Wo + 2 * pg.Pw - pg.Lw) // pg.Sw + 1
+    if out is None:
+        out = torch.empty((g.B, g.Co, Hp, Wp), dtype=torch.uint8, device=lat_in.device)
+    need = conv_workspace(g, prec)
+    if ws is None and need:
+        ws = torch.empty(need, dtype=torch.uint8, device=lat_in.device)
+    nbytes = ws.numel() if ws is not None else 0
+    _check("spk_conv_fire_pool", lib().spk_conv_fire_pool(_p(lat_in), _p(w), ctypes.byref(g), SPK_PREC[prec],
+                                                          float(theta), float(w_max), ctypes.byref(pg), _p(out),
+                                                          _p(ws), nbytes, _s()))
     return out
 
 

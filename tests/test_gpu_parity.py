@@ -301,6 +301,23 @@ def _gpu_train(cfg, imgs, Ws, labels=None, prec="exact"):
     return net
 
 
+def _layer_out_diff(rec, L, rlat, excl, excluded, T):
+    """GPU output of a non-trained layer vs the oracle's latencies: the latency map itself,
+    or — when the layer's conv and pool run fused — the pooled map, a pooled neuron being
+    excluded when a near-threshold neuron lies in its window (Eq. 3)."""
+    if rec.get("fused_pool"):
+        p = L["pool"]
+        k, st, pd = (p["kernel"],) * 2, (p["stride"],) * 2, (p["pad"],) * 2
+        rlat = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(rlat, T), k, st, pd))
+        excl = oracle.pool(excl[:, None].astype(np.uint8), k, st, pd)[:, 0].astype(bool)
+        glat = host(rec["pooled"])
+    else:
+        glat = host(rec["lat"])
+    diff = (glat != rlat) & ~excluded[:, None, None, None]
+    assert not (diff & ~excl).any(), "unexplained latency mismatches"
+    return diff.any(axis=(1, 2, 3))
+
+
 def _check_pipeline(cfg, n, labels=False, prec="exact"):
     imgs = synth.images(cfg, 0, n)
     lab = synth.labels(cfg, 0, n) if labels else None
@@ -316,12 +333,8 @@ def _check_pipeline(cfg, n, labels=False, prec="exact"):
         L = cfg["layers"][li]
         P = oracle.conv_event(oracle.dense_to_lat(ref["inputs"][li]), T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
         excl = near_threshold(P, L["theta"])
-        rec = net.layers[li]
-        glat = host(rec["lat"])
         rlat, _ = lat_and_pstar(P, L["theta"])
-        diff = (glat != rlat) & ~excluded_samples[:, None, None, None]
-        assert not (diff & ~excl).any(), f"layer {li}: unexplained latency mismatches"
-        excluded_samples |= diff.any(axis=(1, 2, 3))
+        excluded_samples |= _layer_out_diff(net.layers[li], L, rlat, excl, excluded_samples, T)
     # trained layer: (lat, P*) after inhibition, winners, weights
     L = cfg["layers"][tl]
     excl = near_threshold(ref["P"], L["theta"])
@@ -396,13 +409,13 @@ def test_pipeline_c4_train_t30(spk):
     assert _check_pipeline(synth.load_config("c4"), 1) <= 1
 
 
-def _check_forward(cfg, n):
+def _check_forward(cfg, n, prec="exact"):
     from paper_2301_13659_b200.network import Network
 
     imgs = synth.images(cfg, 0, n)
     Ws = synth.layer_weights(cfg)
     T = cfg["T"]
-    net = Network(cfg, n)
+    net = Network(cfg, n, prec=prec)
     net.img.copy_(cu(imgs))
     net.set_weights([cu(w) for w in Ws])
     net.infer()
@@ -416,10 +429,7 @@ def _check_forward(cfg, n):
         rlat, _ = lat_and_pstar(P, L["theta"])
         excl = near_threshold(P, L["theta"])
         del P
-        glat = host(net.layers[li]["lat"])
-        diff = (glat != rlat) & ~excluded[:, None, None, None]
-        assert not (diff & ~excl).any(), f"layer {li}: unexplained latency mismatches"
-        excluded |= diff.any(axis=(1, 2, 3))
+        excluded |= _layer_out_diff(net.layers[li], L, rlat, excl, excluded, T)
         if L["pool"]:
             p = L["pool"]
             lat = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(rlat, T), (p["kernel"],) * 2,
@@ -438,5 +448,24 @@ def test_pipeline_c5_forward(spk):
     assert _check_forward(synth.load_config("c5"), 1) == 0
 
 
-def test_forward_c2_all_layers(spk):
-    assert _check_forward(synth.load_config("c2"), 6) <= 1
+@pytest.mark.parametrize("prec", ["exact", "auto"])
+def test_forward_c2_all_layers(spk, prec):
+    assert _check_forward(synth.load_config("c2"), 6, prec) <= 1
+
+
+@pytest.mark.parametrize("case", [(3, 15, 6, 28, 28, 30, 5, 1, 2, 2, 2, 0), (2, 15, 6, 28, 28, 30, 5, 1, 2, 3, 2, 1),
+                                  (2, 30, 4, 20, 23, 40, 5, 1, 2, 2, 2, 0), (2, 7, 3, 9, 11, 20, 3, 2, 0, 3, 3, 0)])
+def test_conv_fire_pool_fused(spk, case):
+    """spk_conv_fire_pool == spk_pool(spk_conv(FIRE)) bit for bit (EVENT engine)."""
+    B, T, Ci, Hi, Wi, Co, K, s, p, L, ps, pp = case
+    lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K, 0.3)
+    g = spk.conv_geom(cu(lat), cu(w), T, s, p)
+    if not spk.conv_fire_pool_supported(g, "event", L, ps, pp):
+        pytest.skip("fused fire+pool not supported for this geometry")
+    P = oracle.conv_event(lat, T, w, (s, s), (p, p))
+    theta = float(np.percentile(P[:, -1], 60)) + 0.123
+    flat, _ = spk.conv(cu(lat), cu(w), T, s, p, prec="event", epi="fire", theta=theta)
+    ref = spk.pool(flat, T, L, ps, pp)
+    got = spk.conv_fire_pool(cu(lat), cu(w), T, s, p, prec="event", theta=theta, pool_kernel=L, pool_stride=ps,
+                             pool_pad=pp)
+    np.testing.assert_array_equal(host(got), host(ref))
