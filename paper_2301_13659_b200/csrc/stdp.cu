@@ -150,14 +150,24 @@ __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restr
         __syncthreads();
         // phase 1: gathers, kUpdThreads / kUpdW winners per pass, several passes in flight
         if (valid1) {
-            constexpr int kStep = kUpdThreads / kUpdW;
-#pragma unroll 4
-            for (int e = e_lane; e < m; e += kStep) {
-                int tj = 0x7fffffff;  // padded input: never fires (R-NEVER)
-                const int iy = s_y0[e] + i1, ix = s_x0[e] + j1;
-                if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
-                    tj = __ldg(lat_in + s_ofs[e] + own1);  // == T: never
-                s_le[e][wl] = (uint8_t)(tj <= s_t[e]);     // R-EQ4-TIE
+            constexpr int kStep = kUpdThreads / kUpdW, kBatch = 16;  // kBatch independent loads in flight
+            for (int e0b = e_lane; e0b < m; e0b += kStep * kBatch) {
+                int tj[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int e = e0b + u * kStep;
+                    tj[u] = 0x7fffffff;  // padded input: never fires (R-NEVER)
+                    if (e < m) {
+                        const int iy = s_y0[e] + i1, ix = s_x0[e] + j1;
+                        if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
+                            tj[u] = __ldg(lat_in + s_ofs[e] + own1);  // == T: never
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int e = e0b + u * kStep;
+                    if (e < m) s_le[e][wl] = (uint8_t)(tj[u] <= s_t[e]);  // R-EQ4-TIE
+                }
             }
         }
         __syncthreads();
