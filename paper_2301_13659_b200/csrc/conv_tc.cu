@@ -879,34 +879,36 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     // k-steps of 32 synapses this hand-off holds (the last one may be partial)
                     const int nk = min(a.G * (KS / 32), (a.K - ks * KS + 31) / 32);
                     const uint32_t acc0 = ks ? 1u : 0u;
-#define SPK_NK_SWITCH(CALL)            \
-    switch (nk) {                      \
-        case 1: CALL(1); break;        \
-        case 2: CALL(2); break;        \
-        case 3: CALL(3); break;        \
-        case 4: CALL(4); break;        \
-        case 5: CALL(5); break;        \
-        case 6: CALL(6); break;        \
-        case 7: CALL(7); break;        \
-        default: CALL(8); break;       \
+// full hand-offs take one straight-line block; a partial last one issues single
+// k-steps in a loop (no jump table: an indirect branch costs a constant-bank load and
+// an instruction fetch at a far target on every hand-off)
+#define SPK_NK_DISPATCH(CALL)                                                 \
+    if (nk == 8) {                                                            \
+        CALL(8, 0);                                                           \
+    } else if (nk == 4) {                                                     \
+        CALL(4, 0);                                                           \
+    } else {                                                                  \
+        for (int kk = 0; kk < nk; ++kk) CALL(1, kk);                          \
     }
                     if (SPK_EXP & 32) {
                     } else if (a.stack == 2) {
                         const uint32_t e2 = dbase + 2 * a.Nt;
-#define SPK_PAIR(n) tc_stage_pair<n>(dbase, e2, at, dst, inck, 2 * incd, idesc01, idesc, acc0)
-                        SPK_NK_SWITCH(SPK_PAIR)
+#define SPK_PAIR(n, kk) \
+    tc_stage_pair<n>(dbase, e2, at + 8u * (kk), dst + inck * (kk), inck, 2 * incd, idesc01, idesc, (kk) ? 1u : acc0)
+                        SPK_NK_DISPATCH(SPK_PAIR)
 #undef SPK_PAIR
                     } else if (a.stack == 1) {
-#define SPK_STACKED(n) tc_stage_stacked<n>(dbase, at, dst, inck, idesc, acc0)
-                        SPK_NK_SWITCH(SPK_STACKED)
+#define SPK_STACKED(n, kk) tc_stage_stacked<n>(dbase, at + 8u * (kk), dst + inck * (kk), inck, idesc, (kk) ? 1u : acc0)
+                        SPK_NK_DISPATCH(SPK_STACKED)
 #undef SPK_STACKED
                     } else {
                         const uint32_t e1 = dbase + a.Nt, e2 = dbase + 2 * a.Nt;
-#define SPK_SEP(n) tc_stage_sep<n>(dbase, e1, e2, at, dst, inck, incd, idesc, acc0)
-                        SPK_NK_SWITCH(SPK_SEP)
+#define SPK_SEP(n, kk) \
+    tc_stage_sep<n>(dbase, e1, e2, at + 8u * (kk), dst + inck * (kk), inck, incd, idesc, (kk) ? 1u : acc0)
+                        SPK_NK_DISPATCH(SPK_SEP)
 #undef SPK_SEP
                     }
-#undef SPK_NK_SWITCH
+#undef SPK_NK_DISPATCH
                     if (lane == 0) TRACE(10, mma_st - 1);
                     const long long c2 = rc.on ? clock64() : 0;
                     if (!a.bres && !(SPK_EXP & 4096) && (kb_next == 0 || ks + a.G >= a.nks)) {
