@@ -883,12 +883,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 // k-steps in a loop (no jump table: an indirect branch costs a constant-bank load and
 // an instruction fetch at a far target on every hand-off)
 #define SPK_NK_DISPATCH(CALL)                                                 \
-    if (nk == 8) {                                                            \
-        CALL(8, 0);                                                           \
-    } else if (nk == 4) {                                                     \
-        CALL(4, 0);                                                           \
-    } else {                                                                  \
-        for (int kk = 0; kk < nk; ++kk) CALL(1, kk);                          \
+    {                                                                         \
+        uint32_t f8 = nk == 8, f4 = nk == 4;                                  \
+        asm volatile("" : "+r"(f8), "+r"(f4));                                \
+        if (f8) {                                                             \
+            CALL(8, 0);                                                       \
+        } else if (f4) {                                                      \
+            CALL(4, 0);                                                       \
+        } else {                                                              \
+            _Pragma("unroll 1") for (int kk = 0; kk < nk; ++kk) CALL(1, kk);  \
+        }                                                                     \
     }
                     if (SPK_EXP & 32) {
                     } else if (a.stack == 2) {
