@@ -311,15 +311,25 @@ struct TileIter {
         }
     }
     // the next tile stages a different input region (or there is no next tile)
+    // (band mode: the next M tile of the sample keeps the band when its first row is the same)
+    template <int PPT>
+    __device__ __forceinline__ bool next_m_same_region(const TcArgs& a) const {
+        if (j + 1 == a.tps) return false;  // next sample
+        if (a.NR == a.HiP) return true;
+        const int lo0 = ((j * PPT) / a.Wo) * a.g.Sh, lo1 = (((j + 1) * PPT) / a.Wo) * a.g.Sh;
+        return max(0, min(lo0, a.HiP - a.NR)) == max(0, min(lo1, a.HiP - a.NR));
+    }
+    template <int PPT>
     __device__ __forceinline__ bool region_ends(const TcArgs& a) const {
         if (tile + 1 >= t1) return true;
         if (nt + 1 < a.n_ntiles) return false;
-        return a.NR == a.HiP ? (j + 1 == a.tps) : true;
+        return !next_m_same_region<PPT>(a);
     }
     // same, asked at the first N tile of an M tile about the whole M tile (retained A)
+    template <int PPT>
     __device__ __forceinline__ bool region_ends_m(const TcArgs& a) const {
         if (tile + (a.n_ntiles - nt) >= t1) return true;
-        return a.NR == a.HiP ? (j + 1 == a.tps) : true;
+        return !next_m_same_region<PPT>(a);
     }
     // first staged row of this tile, in padded-image rows (input row + Ph)
     template <int PPT>
@@ -535,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             }
             const long long tt1 = rc.on ? clock64() : 0;
             if (rc.on) pt[8] += tt1 - tt0;
-            const bool last_use = a.retain ? ti.region_ends_m(a) : ti.region_ends(a);
+            const bool last_use = a.retain ? ti.template region_ends_m<PPT>(a) : ti.template region_ends<PPT>(a);
             need_region = last_use;
             const uint8_t* region = RG + rb * a.rb_stride;
             const int p = ti.j * PPT + gpix_in_tile;
@@ -997,7 +1007,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         bool need_region = true;
         for (; ti.valid(); ti.next(a)) {
             const bool load = need_region;
-            need_region = ti.region_ends(a);
+            need_region = ti.template region_ends<PPT>(a);
             if (!load) continue;  // same staged region as the previous tile
             uint8_t* dst = RG + rb * a.rb_stride;
             rc.template group_wait<kBarBand, kLoaders>(rge0 + 8 * rb, rph ^ 1u, lt == 0);
