@@ -11,14 +11,15 @@
 // integers, the same fire test (128 S > floor(theta 2^30 / s)) and the same single
 // rounding of the potential — so the outputs are bit-identical to the tensor path.
 //
-// Grid (pixel chunks, blocks of 32 maps, B); small samples are staged whole in shared
-// memory and one CTA covers all their pixels.  16 warps, each owns every 16th pixel of
-// the chunk; a lane owns one output map.  Per pixel the warp
-// (1) compacts the active synapses of the receptive field into a shared list
-// (ballot), (2) adds each one's weight column into per-lane latency bins H[t][lane]
-// in shared memory, (3) prefix-sums the bins: first crossing -> lat, P* (FIRE), or
-// every P[t] (POTENTIAL).  Weights of the map block live in shared memory,
-// transposed [k][map] so a warp's 32 lanes read one 128-byte row.
+// Grid (chunks of whole output rows, blocks of 32 maps, B); the chunk's input band is
+// staged in shared memory with its zero-padding halo written as "never fires", and a
+// small sample is one chunk.  16 warps, each owns every 16th pixel of the chunk; a lane
+// owns one output map.  Per pixel the warp (1) counting-sorts the receptive field's
+// active synapses by latency into a shared list, (2) walks the list once keeping the
+// running potential in a register: the first element that lifts it above the
+// threshold gives lat, the end of that latency group gives P* (FIRE), or every P[t]
+// is written (POTENTIAL).  Weights of the map block live in shared memory, transposed
+// [k][map] so a warp's 32 lanes read one 128-byte row.
 #include <cmath>
 
 #include "conv.cuh"
@@ -35,7 +36,8 @@ struct EvArgs {
     void* out0;
     float* out1;
     spk_conv_geom g;
-    int Ho, Wo, HWo, K, Co_pad, pch, stage, nw;
+    int Ho, Wo, HWo, K, Co_pad, pch, nw;
+    int rpc, Wq, band;  // output rows per CTA, staged row length, staged band bytes
     int pool, Hp, Wp;   // fused pooling (Eq. 3) of the latency map in the write-out: out0 = pooled lat
     spk_pool_geom pg;
     uint32_t th;          // fire iff S > th  (S = sum of q; th = floor(theta 2^30 / s) >> 7)
@@ -60,182 +62,221 @@ __global__ void ev_pack_kernel(const float* __restrict__ w, int Co, int K, int C
 
 // shared-memory carve-up (bytes), 16-byte aligned pieces
 struct EvSmem {
-    size_t sq, koff, kij, in, lists, H, olat, ops, total;
+    size_t sq, koff, in, lists, cnt, olat, ops, total;
 };
 __host__ __device__ inline size_t ev_al(size_t x) { return (x + 15) & ~(size_t)15; }
-__host__ __device__ inline EvSmem ev_smem(int K, int T, int accb, int pch, size_t in_bytes, bool pstar, int nw) {
+__host__ __device__ inline int ev_list_len(int K) { return (K + 3) & ~3; }   // padded to whole uint4 batches
+__host__ __device__ inline int ev_cnt_len(int T) { return (T + 32) & ~31; }  // T bins, 32-lane chunks
+__host__ __device__ inline EvSmem ev_smem(int K, int T, int pch, size_t in_bytes, bool pstar, int nw) {
     EvSmem m;
     m.sq = 0;
-    m.koff = ev_al(m.sq + (size_t)K * kMB * 4);
-    m.kij = ev_al(m.koff + (size_t)K * 4);
-    m.in = ev_al(m.kij + (size_t)K * 2);
+    m.koff = ev_al(m.sq + (size_t)(K + 1) * kMB * 4);  // + one zero row for list padding
+    m.in = ev_al(m.koff + (size_t)K * 4);
     m.lists = ev_al(m.in + in_bytes);
-    m.H = ev_al(m.lists + (size_t)nw * ((K + 3) & ~3) * 4);
-    m.olat = ev_al(m.H + (size_t)nw * T * 32 * accb);
+    m.cnt = ev_al(m.lists + (size_t)nw * ev_list_len(K) * 4);
+    m.olat = ev_al(m.cnt + (size_t)nw * ev_cnt_len(T) * 4);
     m.ops = ev_al(m.olat + (size_t)kMB * pch);
     m.total = ev_al(m.ops + (pstar ? (size_t)kMB * pch * 4 : 0));
     return m;
 }
 
-// ACC = uint32_t when K * 2^23 < 2^32, else unsigned long long
-template <typename ACC, int EPI, bool PSTAR, bool SMALLK, int NW>
+// ACC = uint32_t when K * 2^23 < 2^32, else unsigned long long.
+// Per output pixel, one warp (lane = output map):
+//  (1) counting sort of the receptive field's ACTIVE synapses by latency: shared
+//      counters per latency, a warp scan, and placement through the running
+//      cursors — the list holds (weight-row byte offset << 8 | lat), latency-ascending;
+//  (2) one pass over the sorted list in uint4 batches: acc += W_k (exact integer
+//      sums, registers only).  Potentials are non-decreasing (R-NONNEG), so the
+//      first element whose running sum exceeds the threshold has the output latency;
+//      P* = the running sum at the end of that latency group (its end is the
+//      group's final cursor).  Zero-weight padding entries complete the last batch.
+__device__ __forceinline__ int lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));  // the band is read-only after staging
+    return (int)v;
+}
+
+// NCH = ceil(K / 32) synapse chunks held in registers (1..8), or 0 for large receptive fields
+template <typename ACC, int EPI, bool PSTAR, int NCH, int NW>
 __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
+    constexpr bool SMALLK = NCH > 0;
     constexpr int kEvThreads = NW * 32, kEvWarps = NW;
     extern __shared__ __align__(16) unsigned char sm[];
     const spk_conv_geom& g = a.g;
     const int K = a.K, T = g.T;
     const size_t HWi = (size_t)g.Hi * g.Wi;
-    const EvSmem ms = ev_smem(K, T, (int)sizeof(ACC), a.pch, a.stage ? (size_t)g.Ci * HWi : 0, PSTAR, NW);
-    uint32_t* sq = reinterpret_cast<uint32_t*>(sm + ms.sq);        // [K][32] weight columns
+    const EvSmem ms = ev_smem(K, T, a.pch, (size_t)a.band, PSTAR, NW);
+    uint32_t* sq = reinterpret_cast<uint32_t*>(sm + ms.sq);        // [K+1][32] weight rows (row K = 0)
     int* koff = reinterpret_cast<int*>(sm + ms.koff);              // [K] c*Hi*Wi + i*Wi + j
-    uint16_t* kij = reinterpret_cast<uint16_t*>(sm + ms.kij);      // [K] (i << 8) | j
-    uint8_t* sin = sm + ms.in;                                     // staged input sample (a.stage)
-    uint32_t* lists = reinterpret_cast<uint32_t*>(sm + ms.lists);  // [warps][K] (k << 8) | lat
-    ACC* H = reinterpret_cast<ACC*>(sm + ms.H);                    // [warps][T][32] latency bins
+    uint8_t* sin = sm + ms.in;                                     // staged input band [Ci][rows][Wq]
+    uint32_t* lists = reinterpret_cast<uint32_t*>(sm + ms.lists);  // [warps][K pad 4] (k << 15) | lat
+    uint32_t* cnts = reinterpret_cast<uint32_t*>(sm + ms.cnt);     // [warps][T pad] counters / cursors
     uint8_t* olat = sm + ms.olat;                                  // [32][pch]
     float* ops = reinterpret_cast<float*>(sm + ms.ops);            // [32][pch] (P*)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.z, m0 = blockIdx.y * kMB, p0 = blockIdx.x * a.pch;
-    const int npix = min(a.pch, a.HWo - p0);
+    const int b = blockIdx.z, m0 = blockIdx.y * kMB;
+    const int ya = blockIdx.x * a.rpc;                 // first output row of this CTA's chunk
+    const int p0 = ya * a.Wo;
+    const int npix = min(a.rpc, a.Ho - ya) * a.Wo;
+    const int nrows = (min(a.rpc, a.Ho - ya) - 1) * g.Sh + g.Kh;  // staged input rows (halo incl.)
+    const int Wq = a.Wq;                                // staged row length (Wi + 2 Pw)
     const uint8_t* L = a.lat_in + (size_t)b * g.Ci * HWi;
 
-    // stage this map block's weight columns, the synapse table and (small samples) the input
+    // stage this map block's weight rows, the synapse table and the input band with its
+    // zero-padding halo written as "never fires", so synapse reads need no bounds test
     for (int q = threadIdx.x; q < K * kMB; q += kEvThreads) sq[q] = a.qT[(size_t)(q >> 5) * a.Co_pad + m0 + (q & 31)];
+    if (threadIdx.x < kMB) sq[K * kMB + threadIdx.x] = 0u;
     const int KhKw = g.Kh * g.Kw;
     for (int k = threadIdx.x; k < K; k += kEvThreads) {
         const int c = k / KhKw, r = k - c * KhKw, i = r / g.Kw, j = r - i * g.Kw;
-        koff[k] = (int)(c * HWi) + i * g.Wi + j;
-        kij[k] = (uint16_t)((i << 8) | j);
+        koff[k] = (c * nrows + i) * Wq + j;
     }
-    if (a.stage) {
-        const int n = g.Ci * (int)HWi;
-        if (((reinterpret_cast<uintptr_t>(L) | (uintptr_t)n) & 15) == 0) {
-            const uint4* s4 = reinterpret_cast<const uint4*>(L);
-            uint4* d4 = reinterpret_cast<uint4*>(sin);
-            for (int q = threadIdx.x; q < n / 16; q += kEvThreads) d4[q] = __ldg(s4 + q);
-        } else {
-            for (int q = threadIdx.x; q < n; q += kEvThreads) sin[q] = __ldg(L + q);
+    {
+        const int per_c = nrows * Wq, n = g.Ci * per_c;
+        const int iy0 = ya * g.Sh - g.Ph;
+        for (int q = threadIdx.x; q < n; q += kEvThreads) {
+            const int c = q / per_c, r = q - c * per_c, rr = r / Wq, xx = r - rr * Wq;
+            const int iy = iy0 + rr, ix = xx - g.Pw;
+            sin[q] = ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
+                         ? __ldg(L + (size_t)c * HWi + (size_t)iy * g.Wi + ix)
+                         : (uint8_t)T;
         }
     }
+    const int ncnt = ev_cnt_len(T);
+    for (int q = threadIdx.x; q < kEvWarps * ncnt; q += kEvThreads) cnts[q] = 0u;
     __syncthreads();
-    const uint8_t* src = a.stage ? sin : L;
 
     const int o = m0 + lane;  // this lane's output map
-    uint32_t* list = lists + (size_t)warp * ((K + 3) & ~3);  // 16-byte aligned per warp
-    ACC* h = H + (size_t)warp * T * 32;
-    for (int t = 0; t < T; ++t) h[t * 32 + lane] = 0;
-    const uint32_t* wcol = sq + lane;
+    uint32_t* list = lists + (size_t)warp * ev_list_len(K);  // 16-byte aligned per warp
+    uint32_t* cnt = cnts + (size_t)warp * ncnt;
+    const unsigned char* wrow = reinterpret_cast<const unsigned char*>(sq + lane);
+    const uint32_t pad_entry = ((uint32_t)K << 15) | (uint32_t)T;  // zero weight row, never a crossing
     // small receptive fields: this lane's synapse offsets stay in registers
-    constexpr int kRegChunks = 8;  // K <= 256
-    int rko[kRegChunks], rij[kRegChunks];
+    constexpr int kRegChunks = SMALLK ? NCH : 1;
+    int rko[kRegChunks];
+    const bool last_ok = (kRegChunks - 1) * 32 + lane < K;  // lanes of the last chunk inside K
     if (SMALLK) {
 #pragma unroll
         for (int c = 0; c < kRegChunks; ++c) {
             const int k = c * 32 + lane;
             rko[c] = k < K ? koff[k] : 0;
-            rij[c] = k < K ? kij[k] : 0xFFFF;  // out of the window: never active
         }
     }
-    const unsigned lanemask_lt = (1u << lane) - 1u;
+    const uint32_t sin_s = (uint32_t)__cvta_generic_to_shared(sin);
     const int pstep = kEvWarps;
     int pl = warp;
-    int y = (p0 + pl) / a.Wo, x = (p0 + pl) - y * a.Wo;  // advanced incrementally
+    int y = pl / a.Wo, x = pl - y * a.Wo;  // chunk-relative, advanced incrementally
     for (; pl < npix; pl += pstep) {
         const int p = p0 + pl;
-        const int y0 = y * g.Sh - g.Ph, x0 = x * g.Sw - g.Pw;
-        const ptrdiff_t org = (ptrdiff_t)y0 * g.Wi + x0;
-        // (1) compact the active synapses of the receptive field; list entry =
-        //     (byte offset of the weight row k * 128) << 8 | latency
-        const bool interior = y0 >= 0 && x0 >= 0 && y0 + g.Kh <= g.Hi && x0 + g.Kw <= g.Wi;  // warp-uniform
-        int n = 0;
-        auto take = [&](int k, int lat) {
-            const bool act = lat < T;
-            const unsigned m = __ballot_sync(0xffffffffu, act);
-            if (act) list[n + __popc(m & lanemask_lt)] = ((uint32_t)k << 15) | (uint32_t)lat;
-            n += __popc(m);
+        const uint32_t bs = sin_s + (uint32_t)(y * g.Sh * Wq + x * g.Sw);  // receptive field origin in the band
+        x += pstep;
+        while (x >= a.Wo) x -= a.Wo, ++y;
+        auto lat_of = [&](int k, int c) -> int {  // input latency of synapse k (T: padded / never)
+            if (SMALLK) {
+                const int l = lds_u8(bs + (uint32_t)rko[c]);
+                return (c < kRegChunks - 1 || last_ok) ? l : T;
+            }
+            return k < K ? lds_u8(bs + (uint32_t)koff[k]) : T;
         };
+        // (1a) count active synapses per latency
+        int lr[kRegChunks];
         if (SMALLK) {
 #pragma unroll
             for (int c = 0; c < kRegChunks; ++c) {
-                if (c * 32 >= K) break;
-                int lat = T;
-                if (interior) {
-                    if (c * 32 + lane < K) lat = src[org + rko[c]];
-                } else {
-                    const int iy = y0 + (rij[c] >> 8), ix = x0 + (rij[c] & 255);
-                    if (c * 32 + lane < K && (unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
-                        lat = src[org + rko[c]];  // padded taps never fire
-                }
-                take(c * 32 + lane, lat);
+                lr[c] = lat_of(c * 32 + lane, c);
+                if (lr[c] < T) atomicAdd(cnt + lr[c], 1u);
             }
         } else {
             for (int k0 = 0; k0 < K; k0 += 32) {
-                const int k = k0 + lane;
-                int lat = T;
-                if (k < K) {
-                    const int ij = kij[k], iy = y0 + (ij >> 8), ix = x0 + (ij & 255);
-                    if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
-                        lat = src[org + koff[k]];  // padded taps never fire
-                }
-                take(k, lat);
+                const int l = lat_of(k0 + lane, 0);
+                if (l < T) atomicAdd(cnt + l, 1u);
             }
         }
-        x += pstep;
-        while (x >= a.Wo) x -= a.Wo, ++y;
         __syncwarp();
-        // (2) latency bins: H[lat] += W_k (exact integer sums); the bins were zeroed by
-        //     the previous pixel's prefix pass (or at start)
-        const unsigned char* wrow = reinterpret_cast<const unsigned char*>(wcol);
-        int e = 0;
-        for (; e + 4 <= n; e += 4) {
-            const uint4 v = *reinterpret_cast<const uint4*>(list + e);  // 16-byte aligned: e % 4 == 0
-            const ACC w0 = *reinterpret_cast<const uint32_t*>(wrow + (v.x >> 8)),
-                      w1 = *reinterpret_cast<const uint32_t*>(wrow + (v.y >> 8)),
-                      w2 = *reinterpret_cast<const uint32_t*>(wrow + (v.z >> 8)),
-                      w3 = *reinterpret_cast<const uint32_t*>(wrow + (v.w >> 8));
-            h[(v.x & 255) * 32 + lane] += w0;
-            h[(v.y & 255) * 32 + lane] += w1;
-            h[(v.z & 255) * 32 + lane] += w2;
-            h[(v.w & 255) * 32 + lane] += w3;
+        // (1b) exclusive scan of the counts -> group starts (cursors)
+        uint32_t carry = 0;
+        if (T <= 32) {  // one 32-lane chunk (every config)
+            const uint32_t c = lane < T ? cnt[lane] : 0u;
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            if (lane < T) cnt[lane] = incl - c;
+            carry = __shfl_sync(0xffffffffu, incl, 31);
+        } else
+        for (int t0 = 0; t0 < T; t0 += 32) {
+            const int t = t0 + lane;
+            const uint32_t c = t < T ? cnt[t] : 0u;
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            if (t < T) cnt[t] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        for (; e < n; ++e) {
-            const uint32_t v = list[e];
-            h[(v & 255) * 32 + lane] += (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v >> 8));
+        const int n = (int)carry;
+        const int n4 = (n + 3) & ~3;
+        if (lane < n4 - n) list[n + lane] = pad_entry;
+        __syncwarp();
+        // (1c) place: after this, cnt[t] = end of latency group t
+        if (SMALLK) {
+#pragma unroll
+            for (int c = 0; c < kRegChunks; ++c)
+                if (lr[c] < T)
+                    list[atomicAdd(cnt + lr[c], 1u)] = ((uint32_t)(c * 32 + lane) << 15) | (uint32_t)lr[c];
+        } else {
+            for (int k0 = 0; k0 < K; k0 += 32) {
+                const int l = lat_of(k0 + lane, 0);
+                if (l < T) list[atomicAdd(cnt + l, 1u)] = ((uint32_t)(k0 + lane) << 15) | (uint32_t)l;
+            }
         }
-        // (3) prefix over latencies
-        ACC S = 0;
+        __syncwarp();
+        // (2) running sums over the latency-sorted list
         if (EPI == SPK_EPI_POTENTIAL) {
+            ACC S = 0;
+            int e = 0;
             for (int t = 0; t < T; ++t) {
-                S += h[t * 32 + lane];
-                h[t * 32 + lane] = 0;
+                const int end = (int)cnt[t];
+                for (; e < end; ++e) S += (ACC)*reinterpret_cast<const uint32_t*>(wrow + (list[e] >> 8));
                 if (o < g.Co)
                     static_cast<float*>(a.out0)[(((size_t)b * T + t) * g.Co + o) * a.HWo + p] =
                         __fmul_rn(__ll2float_rn((long long)S * 128ll), a.out_scale);
             }
-        } else if (!PSTAR) {
-            // potentials are non-decreasing in t (W >= 0), so the steps at or below the
-            // threshold are exactly t < lat: lat = their count
-            int lat = 0;
-            for (int t = 0; t < T; ++t) {
-                S += h[t * 32 + lane];
-                h[t * 32 + lane] = 0;
-                lat += (S <= (ACC)a.th);
-            }
-            olat[lane * a.pch + pl] = (uint8_t)lat;
         } else {
-            int lat = T;
-            ACC Sf = 0;
-            for (int t = 0; t < T; ++t) {
-                S += h[t * 32 + lane];
-                h[t * 32 + lane] = 0;
-                if (lat == T && S > (ACC)a.th) {
-                    lat = t;
-                    Sf = S;
+            const ACC th = (ACC)a.th;
+            ACC S = 0, Sps = 0;
+            int lo = T;             // output latency (first crossing)
+            int pe = 0x7fffffff;    // PSTAR: end index of the crossing's latency group
+            for (int e = 0; e < n4; e += 4) {
+                const uint4 v = *reinterpret_cast<const uint4*>(list + e);
+                const ACC s0 = S + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.x >> 8));
+                const ACC s1 = s0 + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.y >> 8));
+                const ACC s2 = s1 + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.z >> 8));
+                const ACC s3 = s2 + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.w >> 8));
+                if (lo == T && s3 > th) {  // this lane crosses inside the batch (once per lane)
+                    lo = (int)((s0 > th ? v.x : s1 > th ? v.y : s2 > th ? v.z : v.w) & 255u);
+                    if (PSTAR) pe = (int)cnt[lo];
                 }
+                if (PSTAR && pe <= e + 4) {  // the crossing's group ends inside this batch
+                    const int j = pe - e;     // 1..4 (pe > e: groups end after their crossing)
+                    Sps = j == 1 ? s0 : j == 2 ? s1 : j == 3 ? s2 : s3;
+                    pe = 0x7fffffff;
+                }
+                S = s3;
             }
-            olat[lane * a.pch + pl] = (uint8_t)lat;
-            if (PSTAR) ops[lane * a.pch + pl] = lat < T ? __fmul_rn(__ll2float_rn((long long)Sf * 128ll), a.out_scale) : 0.0f;
+            olat[lane * a.pch + pl] = (uint8_t)lo;
+            if (PSTAR) ops[lane * a.pch + pl] = lo < T ? __fmul_rn(__ll2float_rn((long long)Sps * 128ll), a.out_scale) : 0.0f;
+        }
+        __syncwarp();
+        if (T <= 32) {  // counters for the next pixel
+            if (lane < T) cnt[lane] = 0u;
+        } else {
+            for (int t = lane; t < T; t += 32) cnt[t] = 0u;
         }
         __syncwarp();
     }
@@ -272,14 +313,32 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     }
 }
 
-template <typename ACC, int EPI, bool PSTAR>
-spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
-    auto k = a.nw == 16 ? (a.K <= 256 ? conv_event_kernel<ACC, EPI, PSTAR, true, 16> : conv_event_kernel<ACC, EPI, PSTAR, false, 16>)
-                        : (a.K <= 256 ? conv_event_kernel<ACC, EPI, PSTAR, true, 8> : conv_event_kernel<ACC, EPI, PSTAR, false, 8>);
+template <typename ACC, int EPI, bool PSTAR, int NCH, int NW>
+spk_status launch_ev1(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+    auto k = conv_event_kernel<ACC, EPI, PSTAR, NCH, NW>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return spk::launched("conv_event_kernel(attr)");
-    k<<<grid, a.nw * 32, smem, s>>>(a);
+    k<<<grid, NW * 32, smem, s>>>(a);
     return spk::launched("conv_event_kernel");
+}
+
+template <typename ACC, int EPI, bool PSTAR>
+spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+    if (a.nw == 8) return launch_ev1<ACC, EPI, PSTAR, 0, 8>(a, grid, smem, s);
+    if constexpr (sizeof(ACC) == 4) {  // K <= 256 always sums in 32 bits
+        switch ((a.K + 31) / 32) {
+            case 1: return launch_ev1<ACC, EPI, PSTAR, 1, 16>(a, grid, smem, s);
+            case 2: return launch_ev1<ACC, EPI, PSTAR, 2, 16>(a, grid, smem, s);
+            case 3: return launch_ev1<ACC, EPI, PSTAR, 3, 16>(a, grid, smem, s);
+            case 4: return launch_ev1<ACC, EPI, PSTAR, 4, 16>(a, grid, smem, s);
+            case 5: return launch_ev1<ACC, EPI, PSTAR, 5, 16>(a, grid, smem, s);
+            case 6: return launch_ev1<ACC, EPI, PSTAR, 6, 16>(a, grid, smem, s);
+            case 7: return launch_ev1<ACC, EPI, PSTAR, 7, 16>(a, grid, smem, s);
+            case 8: return launch_ev1<ACC, EPI, PSTAR, 8, 16>(a, grid, smem, s);
+            default: break;
+        }
+    }
+    return launch_ev1<ACC, EPI, PSTAR, 0, 16>(a, grid, smem, s);
 }
 
 }  // namespace
@@ -291,18 +350,21 @@ bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
     if (g.Kh > 255 || g.Kw > 255 || g.T > 254 || p.K >= (1 << 17)) return false;  // list entry k << 15
     if ((double)g.Ci * g.Hi * g.Wi >= 2147483647.0) return false;
     p.acc64 = (double)p.K * 8388608.0 >= 4294967296.0 ? 1 : 0;
-    const int HWo = p.Ho * p.Wo;
-    const size_t in_bytes = (size_t)g.Ci * g.Hi * g.Wi;
-    p.stage = in_bytes <= (size_t)kStageMax ? 1 : 0;
-    p.pch = std::min(HWo, p.stage ? kPchMax : 256);
-    // smem with P* staging (the larger of the two epilogue variants); 16 warps when it fits
+    p.Wq = g.Wi + 2 * g.Pw;
+    // whole output rows per CTA: the staged band (with halo) and the output staging must fit;
+    // a whole sample per CTA when possible (enables the fused pooling write-out)
+    auto band = [&](int r) { return (size_t)g.Ci * (size_t)((r - 1) * g.Sh + g.Kh) * p.Wq; };
+    auto smem = [&](int r, int nw) { return ev_smem(p.K, g.T, r * p.Wo, band(r), true, nw).total; };
+    int r = std::max(1, std::min(p.Ho, kPchMax / std::max(1, p.Wo)));
+    while (r > 1 && (band(r) > (size_t)kStageMax || smem(r, 16) > 200 * 1024)) --r;
     p.nw = 16;
-    p.smem_bytes = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, p.stage ? in_bytes : 0, true, 16).total;
-    if (p.smem_bytes > 200 * 1024) {
-        p.nw = 8;
-        p.smem_bytes = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, p.stage ? in_bytes : 0, true, 8).total;
-    }
-    if (p.smem_bytes > 200 * 1024) return false;
+    if (smem(r, 16) > 200 * 1024) p.nw = 8;
+    if (band(r) > (size_t)kStageMax * 2 || smem(r, p.nw) > 200 * 1024 || r * p.Wo > 65535) return false;
+    p.rpc = r;
+    p.pch = r * p.Wo;
+    p.band = band(r);
+    p.stage = r >= p.Ho ? 1 : 0;  // whole sample in one CTA
+    p.smem_bytes = smem(r, p.nw);
     p.n_mb = (g.Co + kMB - 1) / kMB;
     p.Co_pad = p.n_mb * kMB;
     p.MB = kMB;
@@ -339,7 +401,9 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     a.K = p.K;
     a.Co_pad = p.Co_pad;
     a.pch = p.pch;
-    a.stage = p.stage;
+    a.rpc = p.rpc;
+    a.Wq = p.Wq;
+    a.band = (int)p.band;
     if (pool) {  // caller checked: FIRE, whole sample in one CTA
         a.pool = 1;
         a.pg = *pool;
@@ -349,11 +413,10 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     const long long theta_q = (long long)std::floor((double)theta * (1073741824.0 / scale));  // tensor path's
     a.th = (uint32_t)std::min<long long>(theta_q >> 7, 0xffffffffll);
     a.out_scale = (float)(scale / 1073741824.0);
-    const dim3 grid((unsigned)((a.HWo + p.pch - 1) / p.pch), (unsigned)p.n_mb, (unsigned)g.B);
+    const dim3 grid((unsigned)((p.Ho + p.rpc - 1) / p.rpc), (unsigned)p.n_mb, (unsigned)g.B);
     const bool ps = out1 != nullptr && epi == SPK_EPI_FIRE;
-    const size_t in_bytes = p.stage ? (size_t)g.Ci * g.Hi * g.Wi : 0;
     a.nw = p.nw;
-    const size_t smem = ev_smem(p.K, g.T, p.acc64 ? 8 : 4, p.pch, in_bytes, ps, p.nw).total;
+    const size_t smem = ev_smem(p.K, g.T, p.pch, p.band, ps, p.nw).total;
     if (epi == SPK_EPI_POTENTIAL)
         return p.acc64 ? launch_ev<unsigned long long, SPK_EPI_POTENTIAL, false>(a, grid, smem, s)
                        : launch_ev<uint32_t, SPK_EPI_POTENTIAL, false>(a, grid, smem, s);

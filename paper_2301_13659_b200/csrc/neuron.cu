@@ -54,6 +54,117 @@ __global__ void __launch_bounds__(kT) pool_kernel(const uint8_t* __restrict__ la
     out[(size_t)bc * plane_out + r] = (uint8_t)min(m, T);
 }
 
+
+// Planes that fit shared memory (every config's pooling): a CTA copies a run of
+// whole input planes — one contiguous byte range — with 16-byte loads, takes the
+// window minima from shared memory and writes its contiguous run of output planes
+// with 16-byte stores: one HBM read of the input and one write of the output.
+constexpr int kPoolSmem = 96 * 1024;
+
+__device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t n) {
+    if ((((uintptr_t)dst | (uintptr_t)src | n) & 15) == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (size_t q = threadIdx.x; q < n / 16; q += blockDim.x) d4[q] = s4[q];
+    } else if ((((uintptr_t)dst | (uintptr_t)src | n) & 3) == 0) {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+        for (size_t q = threadIdx.x; q < n / 4; q += blockDim.x) d4[q] = s4[q];
+    } else {
+        for (size_t q = threadIdx.x; q < n; q += blockDim.x) dst[q] = src[q];
+    }
+}
+
+template <bool BULK>
+__global__ void __launch_bounds__(kT) pool_smem_kernel(const uint8_t* __restrict__ lat, long long BC, int ppc, int H,
+                                                       int W, int T, spk_pool_geom g, int Ho, int Wo,
+                                                       uint8_t* __restrict__ out) {
+    extern __shared__ __align__(128) uint8_t psm[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int HW = H * W, HWo = Ho * Wo;
+    const long long bc0 = (long long)blockIdx.x * ppc;
+    const int np = (int)min((long long)ppc, BC - bc0);
+    uint8_t* sin = psm;
+    uint8_t* sout = psm + (((size_t)ppc * HW + 127) & ~(size_t)127);
+    const uint32_t nin = (uint32_t)np * HW;
+    if (BULK) {  // one TMA bulk copy of the run of planes (16-byte multiples, checked on the host)
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nin) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    (uint32_t)__cvta_generic_to_shared(sin)),
+                "l"(lat + bc0 * HW), "r"(nin), "r"(b)
+                : "memory");
+        }
+        __syncthreads();  // barrier initialised before anyone polls it
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done)
+                         : "r"(b)
+                         : "memory");
+    } else {
+        copy_bytes(sin, lat + bc0 * HW, nin);
+        __syncthreads();
+    }
+    const int n = np * HWo;
+    // one output row per warp iteration (divisions amortised over the row)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool p2 = g.Lh == 2 && g.Lw == 2 && g.Sh == 2 && g.Sw == 2 && g.Ph == 0 && g.Pw == 0;
+    const uint32_t tt = 0x01010101u * (uint32_t)T;
+    for (int row = warp; row < np * Ho; row += kT / 32) {
+        const int pl = row / Ho, y = row - pl * Ho;
+        const uint8_t* r0 = sin + pl * HW + (y * g.Sh - g.Ph) * W;
+        uint8_t* orow = sout + row * Wo;
+        if (p2 && (W & 7) == 0 && (Wo & 3) == 0) {  // 2x2/2: four outputs from two 8-byte reads
+            for (int xq = lane; xq < (Wo >> 2); xq += 32) {
+                const uint2 a = *reinterpret_cast<const uint2*>(r0 + 8 * xq);
+                const uint2 b = *reinterpret_cast<const uint2*>(r0 + W + 8 * xq);
+                const uint32_t m0 = __vminu4(a.x, b.x), m1 = __vminu4(a.y, b.y);
+                const uint32_t h0 = __vminu4(m0 & 0x00ff00ffu, (m0 >> 8) & 0x00ff00ffu);  // bytes 0, 2
+                const uint32_t h1 = __vminu4(m1 & 0x00ff00ffu, (m1 >> 8) & 0x00ff00ffu);
+                const uint32_t v = (h0 & 0xffu) | ((h0 >> 8) & 0xff00u) | ((h1 & 0xffu) << 16) | ((h1 << 8) & 0xff000000u);
+                *reinterpret_cast<uint32_t*>(orow + 4 * xq) = __vminu4(v, tt);
+            }
+        } else if (p2 && (W & 1) == 0) {  // 2x2/2: one output from two 2-byte reads
+            for (int x = lane; x < Wo; x += 32) {
+                const uint32_t a = *reinterpret_cast<const uint16_t*>(r0 + 2 * x);
+                const uint32_t b = *reinterpret_cast<const uint16_t*>(r0 + W + 2 * x);
+                const uint32_t m = __vminu4(a, b);
+                orow[x] = (uint8_t)min(min(m & 0xffu, m >> 8), (uint32_t)T);
+            }
+        } else {
+            const int y0 = y * g.Sh - g.Ph;
+            const int i0 = max(0, -y0), i1 = min(g.Lh, H - y0);
+            for (int x = lane; x < Wo; x += 32) {
+                const int x0 = x * g.Sw - g.Pw;
+                const int j0 = max(0, -x0), j1 = min(g.Lw, W - x0);
+                int m = T;
+                for (int i = i0; i < i1; ++i)
+                    for (int j = j0; j < j1; ++j) m = min(m, (int)r0[i * W + x0 + j]);
+                orow[x] = (uint8_t)min(m, T);
+            }
+        }
+    }
+    if (BULK) {  // TMA bulk store of the run of output planes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + bc0 * HWo),
+                         "r"((uint32_t)__cvta_generic_to_shared(sout)), "r"((uint32_t)n)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+    } else {
+        __syncthreads();
+        copy_bytes(out + bc0 * HWo, sout, (size_t)n);
+    }
+}
+
 // ---------------------------------------------------------------- inhibit
 // One CTA per (sample, chunk of <= kInhPix pixels); threads stride over the
 // chunk's (channel, pixel) cells so that a sample with few pixels and many maps
@@ -88,6 +199,55 @@ __global__ void __launch_bounds__(kT) inhibit_kernel(uint8_t* __restrict__ lat, 
             L[o] = (uint8_t)T;
             P[o] = 0.0f;
         }
+    }
+}
+
+
+// Large maps (HW >= 4096, HW % 4 == 0: C4): a thread owns 4 adjacent pixels of one sample
+// and walks every channel twice — first keeping the 4 least keys in registers (4-byte
+// latency loads, P* read only where something fired), then writing "never" to every
+// other firing cell.  Latencies are read once from HBM (the second walk hits L2),
+// potentials once where alive.
+__global__ void __launch_bounds__(kT) inhibit_wide_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar,
+                                                          int C, int HW, int T) {
+    const int b = blockIdx.y;
+    const int p = 4 * (blockIdx.x * kT + threadIdx.x);
+    if (p >= HW) return;
+    uint8_t* L = lat + (size_t)b * C * HW + p;
+    float* P = pstar + (size_t)b * C * HW + p;
+    unsigned long long best[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+    const uint32_t tt = 0x01010101u * (uint32_t)T;
+#pragma unroll 4
+    for (int c = 0; c < C; ++c) {
+        const uint32_t l4 = *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW);
+        if (__vcmpltu4(l4, tt) == 0u) continue;  // nothing fired at these 4 pixels
+        const float4 p4 = *reinterpret_cast<const float4*>(P + (size_t)c * HW);
+        const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t l = (l4 >> (8 * j)) & 0xffu;
+            if (l < (uint32_t)T) {
+                const uint32_t pd = ~spk_float_order_u32(pv[j] + 0.0f);  // -0 -> +0: equal potentials tie on c
+                const unsigned long long key = ((unsigned long long)l << 56) | ((unsigned long long)pd << 24) | (unsigned)c;
+                best[j] = key < best[j] ? key : best[j];
+            }
+        }
+    }
+    const uint32_t wc[4] = {(uint32_t)(best[0] & 0xFFFFFFu), (uint32_t)(best[1] & 0xFFFFFFu),
+                            (uint32_t)(best[2] & 0xFFFFFFu), (uint32_t)(best[3] & 0xFFFFFFu)};
+#pragma unroll 4
+    for (int c = 0; c < C; ++c) {
+        const uint32_t l4 = *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW);
+        uint32_t kill = __vcmpltu4(l4, tt);  // 0xff per firing byte
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (wc[j] == (uint32_t)c) kill &= ~(0xffu << (8 * j));
+        if (kill == 0u) continue;
+        *reinterpret_cast<uint32_t*>(L + (size_t)c * HW) = (l4 & ~kill) | (tt & kill);
+        float* pp = P + (size_t)c * HW;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (kill & (0xffu << (8 * j))) pp[j] = 0.0f;
     }
 }
 
@@ -169,6 +329,29 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
     SPK_CHECK((long long)Ho * Wo <= (1 << 30), SPK_ERR_SHAPE, "output plane too large");
     const long long BC = (long long)B * C;
     const int plane_out = Ho * Wo;
+    const size_t per_plane = (size_t)H * W + (size_t)plane_out;
+    // large planes (C4, C5): whole planes through shared memory, by TMA bulk copies when
+    // every run is 16-byte aligned; small planes (C1-C3, L2-resident) take the direct kernel
+    if ((long long)H * W >= 2048 && per_plane + 256 <= (size_t)kPoolSmem) {
+        const int ppc = (int)std::min<long long>(BC, std::max<long long>(1, (24 * 1024) / (long long)per_plane));  // ~24 KB per CTA
+        const size_t smem = (((size_t)ppc * H * W + 127) & ~(size_t)127) + (size_t)ppc * plane_out;
+        const long long nblk = (BC + ppc - 1) / ppc;
+        SPK_CHECK(nblk < (1ll << 31), SPK_ERR_SHAPE, "B*C too large");
+        const bool bulk = ((H * W) % 16 == 0) && (plane_out % 16 == 0) &&
+                          ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(pool_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPoolSmem);
+            cudaFuncSetAttribute(pool_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPoolSmem);
+            attr = true;
+        }
+        if (bulk) {
+            pool_smem_kernel<true><<<(unsigned)nblk, kT, smem, spk::as_cuda(stream)>>>(lat, BC, ppc, H, W, T, *p, Ho, Wo, out);
+            return spk::launched("pool_smem_kernel<bulk>");
+        }
+        pool_smem_kernel<false><<<(unsigned)nblk, kT, smem, spk::as_cuda(stream)>>>(lat, BC, ppc, H, W, T, *p, Ho, Wo, out);
+        return spk::launched("pool_smem_kernel");
+    }
     const long long ppy = std::min<long long>(BC, std::max(1, (1 << 30) / plane_out));
     const long long gy = (BC + ppy - 1) / ppy;
     SPK_CHECK(gy <= 65535, SPK_ERR_SHAPE, "B*C too large");
@@ -188,6 +371,11 @@ extern "C" spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int 
     SPK_CHECK((long long)H * W < (1ll << 31) && (long long)C * kInhPix < (1ll << 31), SPK_ERR_SHAPE, "map too large");
     SPK_CHECK(B <= 65535, SPK_ERR_SHAPE, "B=%d > 65535", B);
     const int HW = H * W;
+    if (HW >= 4096 && (HW & 3) == 0 && ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(pstar)) & 15) == 0) {
+        const dim3 grid(spk::ceil_div((size_t)HW / 4, kT), (unsigned)B);
+        inhibit_wide_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
+        return spk::launched("inhibit_wide_kernel");
+    }
     const dim3 grid(spk::ceil_div((size_t)HW, kInhPix), (unsigned)B);
     inhibit_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
     return spk::launched("inhibit_kernel");

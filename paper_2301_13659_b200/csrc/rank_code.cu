@@ -54,14 +54,8 @@ __device__ __forceinline__ unsigned int block_sum(unsigned int v, unsigned int* 
 }
 
 template <bool STAGED, int kThreads>
-__global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __restrict__ y, int N, int T,
-                                                            float thresh, int sort,
-                                                            uint8_t* __restrict__ lat) {
-    extern __shared__ __align__(16) unsigned char dyn[];
-    __shared__ RankSmem sm;
-    unsigned int* vals = reinterpret_cast<unsigned int*>(dyn);
-    const float* ys = y + (size_t)blockIdx.x * N;
-    uint8_t* out = lat + (size_t)blockIdx.x * N;
+__device__ __forceinline__ void rank_code_body(const float* __restrict__ ys, int N, int T, float thresh, int sort,
+                                               uint8_t* __restrict__ out, RankSmem& sm, unsigned int* vals) {
 
     auto U = [&](int i) -> unsigned int { return STAGED ? vals[i] : thr_bits(__ldg(ys + i), thresh); };
 
@@ -199,6 +193,16 @@ __global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __rest
     }
 }
 
+template <bool STAGED, int kThreads>
+__global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __restrict__ y, int N, int T,
+                                                            float thresh, int sort,
+                                                            uint8_t* __restrict__ lat) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    __shared__ RankSmem sm;
+    rank_code_body<STAGED, kThreads>(y + (size_t)blockIdx.x * N, N, T, thresh, sort, lat + (size_t)blockIdx.x * N, sm,
+                                     reinterpret_cast<unsigned int*>(dyn));
+}
+
 // Small samples (N <= kSortMax), sort mode: the unique keys of the positive values
 // are compacted into shared memory and bitonic-sorted descending; the value at
 // sorted position r gets bin floor(r T / n) (R-BINS) — the same ranks as the
@@ -252,6 +256,176 @@ __global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const floa
     }
 }
 
+
+// Large samples, sort mode (C4, C5: N = 160,000 / 301,056 values per sample): one
+// CTA per sample, TWO reads of the sample and no radix passes.
+//  pass 1: histogram of the positive values over 32768 buckets = the top 15 bits of
+//          the float (exponent + 7 mantissa bits; positive floats order like their
+//          bits, so buckets are ordered key ranges of width <= 2^-7 relative).
+//  scan:   for every bucket, above = #values in higher buckets, so its values hold
+//          ranks [above, above + cnt); when floor(r T / n) is the same at both ends
+//          every value of the bucket gets that bin (R-BINS) — all but the <= T-1
+//          buckets that straddle a bin boundary.
+//  pass 2: values of ordinary buckets are written at once; values of boundary
+//          buckets are compacted as unique keys (value bits << 32 | ~index, R-TIE),
+//          bitonic-sorted descending, and get rank = above + (position inside their
+//          bucket).  Exactly the ranks of the full sort.
+// More boundary-bucket values than fit shared memory (massive exact ties) -> the
+// sample falls back to the multi-target radix select above (exact, slower).
+constexpr int kBkt = 32768, kCand = 8192, kHT = 1024, kMaxBnd = 256;
+constexpr size_t kHistSmem = (size_t)kBkt * 4 + (size_t)kCand * 8;
+
+__global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __restrict__ y, int N, int T, float thresh,
+                                                            uint8_t* __restrict__ lat) {
+    extern __shared__ __align__(16) unsigned char dyn[];
+    unsigned int* tab = reinterpret_cast<unsigned int*>(dyn);                         // [kBkt]
+    unsigned long long* cand = reinterpret_cast<unsigned long long*>(dyn + (size_t)kBkt * 4);  // [kCand]
+    __shared__ unsigned int red[32];
+    __shared__ unsigned int bnd_b[kMaxBnd], bnd_c[kMaxBnd];
+    __shared__ unsigned int s_nbnd, s_ncand, s_n;
+    const float* ys = y + (size_t)blockIdx.x * N;
+    uint8_t* out = lat + (size_t)blockIdx.x * N;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool vec = (N & 3) == 0;  // float4 / uchar4 access (sample bases stay aligned)
+
+    for (int q = tid; q < kBkt; q += kHT) tab[q] = 0u;
+    if (tid == 0) {
+        s_nbnd = 0;
+        s_ncand = 0;
+    }
+    __syncthreads();
+    // pass 1: bucket histogram
+    if (vec) {
+        const float4* y4 = reinterpret_cast<const float4*>(ys);
+        for (int q = tid; q < (N >> 2); q += kHT) {
+            const float4 v = __ldg(y4 + q);
+            const unsigned int u0 = thr_bits(v.x, thresh), u1 = thr_bits(v.y, thresh), u2 = thr_bits(v.z, thresh),
+                               u3 = thr_bits(v.w, thresh);
+            if (u0) atomicAdd(&tab[u0 >> 16], 1u);
+            if (u1) atomicAdd(&tab[u1 >> 16], 1u);
+            if (u2) atomicAdd(&tab[u2 >> 16], 1u);
+            if (u3) atomicAdd(&tab[u3 >> 16], 1u);
+        }
+    } else {
+        for (int i = tid; i < N; i += kHT) {
+            const unsigned int u = thr_bits(__ldg(ys + i), thresh);
+            if (u) atomicAdd(&tab[u >> 16], 1u);
+        }
+    }
+    __syncthreads();
+    // scan from the top bucket down: thread tid owns buckets [32 tid, 32 tid + 32)
+    constexpr int kPer = kBkt / kHT;
+    unsigned int loc = 0;
+#pragma unroll 8
+    for (int j = 0; j < kPer; ++j) loc += tab[tid * kPer + j];
+    // exclusive scan over threads in DEScending tid order: above_start(tid) = sum_{tid' > tid}
+    unsigned int incl = loc;  // inclusive suffix within the warp (lanes > lane)
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int v = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += v;
+    }
+    if (lane == 0) red[wid] = incl;  // warp total
+    __syncthreads();
+    if (wid == 0) {
+        const unsigned int wt = red[lane];
+        unsigned int ws = wt;  // inclusive suffix over warps
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int v = __shfl_down_sync(0xffffffffu, ws, o);
+            if (lane + o < 32) ws += v;
+        }
+        if (lane == 0) s_n = ws;
+        __syncwarp();
+        red[lane] = ws - wt;  // sum over warps above this one
+    }
+    __syncthreads();
+    const unsigned int n = s_n;
+    if (n == 0) {
+        for (int i = tid; i < N; i += kHT) out[i] = (uint8_t)T;
+        return;
+    }
+    unsigned int run = red[wid] + (incl - loc);  // values in buckets above this thread's range
+    for (int j = kPer - 1; j >= 0; --j) {
+        const int B = tid * kPer + j;
+        const unsigned int c = tab[B];
+        unsigned int tag = 0;
+        if (c) {
+            const unsigned int lo = (unsigned int)(((unsigned long long)run * T) / n),
+                               hi = (unsigned int)(((unsigned long long)(run + c - 1) * T) / n);
+            if (lo == hi) {
+                tag = lo;
+            } else {
+                tag = 255;
+                const unsigned int slot = atomicAdd(&s_nbnd, 1u);  // <= T-1 < kMaxBnd boundary buckets
+                bnd_b[slot] = (unsigned int)B;
+                bnd_c[slot] = c;
+            }
+        }
+        tab[B] = run | (tag << 24);
+        run += c;
+    }
+    __syncthreads();
+    // pass 2: ordinary buckets are final; boundary-bucket values become candidates
+    auto one = [&](unsigned int u, int i) -> unsigned int {
+        if (!u) return (unsigned int)T;
+        const unsigned int tag = tab[u >> 16] >> 24;
+        if (tag != 255u) return tag;
+        const unsigned int pos = atomicAdd(&s_ncand, 1u);
+        if (pos < (unsigned)kCand) cand[pos] = ((unsigned long long)u << 32) | (0xffffffffu - (unsigned)i);
+        return 0u;  // placeholder, rewritten below
+    };
+    if (vec) {
+        const float4* y4 = reinterpret_cast<const float4*>(ys);
+        uchar4* o4 = reinterpret_cast<uchar4*>(out);
+        for (int q = tid; q < (N >> 2); q += kHT) {
+            const float4 v = __ldg(y4 + q);
+            uchar4 r;
+            r.x = (uint8_t)one(thr_bits(v.x, thresh), 4 * q);
+            r.y = (uint8_t)one(thr_bits(v.y, thresh), 4 * q + 1);
+            r.z = (uint8_t)one(thr_bits(v.z, thresh), 4 * q + 2);
+            r.w = (uint8_t)one(thr_bits(v.w, thresh), 4 * q + 3);
+            o4[q] = r;
+        }
+    } else {
+        for (int i = tid; i < N; i += kHT) out[i] = (uint8_t)one(thr_bits(__ldg(ys + i), thresh), i);
+    }
+    __syncthreads();
+    const int nc = (int)s_ncand;
+    if (nc > kCand) {  // massive exact ties: exact radix select over the sample (global reads)
+        RankSmem& sm = *reinterpret_cast<RankSmem*>(dyn);
+        rank_code_body<false, kHT>(ys, N, T, thresh, 1, out, sm, nullptr);
+        return;
+    }
+    int P = 1;
+    while (P < nc) P <<= 1;
+    for (int q = nc + tid; q < P; q += kHT) cand[q] = 0ull;  // sorts last
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = tid; t < (P >> 1); t += kHT) {
+                const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1)), b = a + j;
+                const unsigned long long ka = cand[a], kb = cand[b];
+                const bool desc = (a & k) == 0;
+                if ((ka < kb) == desc) {
+                    cand[a] = kb;
+                    cand[b] = ka;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const int nb = (int)s_nbnd;
+    for (int j = tid; j < nc; j += kHT) {
+        const unsigned long long key = cand[j];
+        const unsigned int u = (unsigned int)(key >> 32), B = u >> 16;
+        const unsigned int idx = 0xffffffffu - (unsigned int)(key & 0xffffffffull);
+        unsigned int sB = 0;  // candidates in higher boundary buckets
+        for (int q = 0; q < nb; ++q)
+            if (bnd_b[q] > B) sB += bnd_c[q];
+        const unsigned int rank = (tab[B] & 0xffffffu) + ((unsigned int)j - sB);
+        out[idx] = (uint8_t)(((unsigned long long)rank * T) / n);
+    }
+}
+
 }  // namespace
 
 extern "C" size_t spk_rank_code_workspace(int, int, int, int) { return 0; }
@@ -281,6 +455,15 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         }
         rank_code_sort_kernel<<<B, kSortThreads, smem, s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_sort_kernel");
+    }
+    if (sort) {  // larger samples: bucket histogram + boundary-bucket sort
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(rank_code_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHistSmem);
+            attr = true;
+        }
+        rank_code_hist_kernel<<<B, kHT, kHistSmem, s>>>(y, N, T, thresh, lat);
+        return spk::launched("rank_code_hist_kernel");
     }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
         const size_t smem = sizeof(unsigned int) * (size_t)N;

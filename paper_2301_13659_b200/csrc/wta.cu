@@ -1,20 +1,42 @@
 // wta.cu — a7: convolutional k-winners-take-all (convwta(array, radius, count)).
 //
-// One CTA per sample; the live neurons' keys are compacted into shared memory
-// once (when they fit).  Each live neuron carries the unique 64-bit key
+// Every live neuron (lat < T) carries the unique 64-bit key
 //   lat (8 bits) | ~order(P*) (32 bits) | flat (c,y,x) index (24 bits)
 // so "earliest, then higher potential, then lower index" is a plain unsigned
-// minimum.  Each of the k greedy rounds is one pass over the sample's records
-// with a warp-shuffle + shared-memory min reduction; suppression (whole
-// channel + |dy|,|dx| <= radius square in every channel, R-WTA-FOOTPRINT) is
-// evaluated against the winners picked so far.
+// minimum.  Greedy rounds pick the least key that no earlier winner suppresses
+// (its whole channel + the |dy|,|dx| <= radius square in every channel,
+// R-WTA-FOOTPRINT).
+//
+// One thread-block CLUSTER per sample (1..8 CTAs, grid = CS x B).  CTA r of the
+// cluster owns the pixel slice [r HW/CS, (r+1) HW/CS) of every channel:
+//  phase 1 (one HBM pass over the records): its slice's candidate keys are
+//    compacted into shared memory.  When the slice is too large to keep every
+//    live key, each pixel keeps only its min(k, C) least keys — EXACT: a winner
+//    at pixel (y,x) suppresses that pixel in every channel, so before it is picked
+//    every smaller key at (y,x) must be dead by CHANNEL suppression, and at most
+//    k-1 channels are dead; hence every winner is among the k least keys of its
+//    pixel, and the greedy minimum over the reduced set equals the one over all
+//    live neurons at every round.
+//  phase 2 (k rounds, on chip): each CTA takes the least unsuppressed key of its
+//    slice (warp shuffles + smem), the cluster's minimum is read through
+//    distributed shared memory (one cluster barrier per round, parity-buffered
+//    slots), and every CTA appends the same winner.
+// A slice whose candidates overflow the shared buffer re-reads its records from
+// HBM each round (exact, slow; not hit by C1-C4).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxK = 64;
-constexpr int kCap = 2048;  // live neurons kept in shared memory (else re-read each round)
+constexpr int kMaxCS = 8;
+constexpr int kCapKeys = 12288;  // 96 KB of keys per CTA
 
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) {
     return a < b ? a : b;
@@ -27,57 +49,130 @@ __device__ __forceinline__ unsigned long long wta_key(const uint8_t* L, const fl
     return ((unsigned long long)l << 56) | ((unsigned long long)po << 24) | (unsigned long long)i;
 }
 
-__global__ void __launch_bounds__(kThreads) wta_kernel(const uint8_t* __restrict__ lat,
-                                                      const float* __restrict__ pstar, int C, int H,
-                                                      int W, int T, int k, int radius,
-                                                      spk_winner* __restrict__ win,
-                                                      int32_t* __restrict__ nwin) {
-    __shared__ unsigned long long keys[kCap];
-    __shared__ int pc[kMaxK], py[kMaxK], px[kMaxK];
+struct WtaArgs {
+    const uint8_t* lat;
+    const float* pstar;
+    int C, H, W, T, k, radius, cs;
+    int mode;  // 0: emit every live key of the slice, 1: per-pixel top-KK, 2: overflow (re-read)
+    unsigned cap;  // keys the shared buffer holds
+    spk_winner* win;
+    int32_t* nwin;
+};
+
+// KK = per-pixel keep count (>= min(k, C)) for mode 1
+template <int KK>
+__global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) {
+    extern __shared__ unsigned long long keys[];  // [kCapKeys]
     __shared__ unsigned long long red[kThreads / 32];
-    __shared__ int npicked;
-    __shared__ unsigned int nlive;
-    const int b = blockIdx.x;
-    const int HW = H * W;
-    const int N = C * HW;
+    __shared__ unsigned long long cmin[2];
+    __shared__ int pc[kMaxK], py[kMaxK], px[kMaxK];
+    __shared__ unsigned int nkeys;
+    __shared__ int overflow;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int b = blockIdx.y;
+    const int HW = a.H * a.W, N = a.C * HW, T = a.T;
     const int lane = threadIdx.x & 31;
-    const uint8_t* L = lat + (size_t)b * N;
-    const float* P = pstar + (size_t)b * N;
+    const uint8_t* L = a.lat + (size_t)b * N;
+    const float* P = a.pstar + (size_t)b * N;
+    const int p_lo = (int)((long long)HW * rank / a.cs), p_hi = (int)((long long)HW * (rank + 1) / a.cs);
+    const int np_slice = p_hi - p_lo;
     if (threadIdx.x == 0) {
-        npicked = 0;
-        nlive = 0;
+        nkeys = 0;
+        overflow = a.mode == 2;
     }
     __syncthreads();
-    // compact the live neurons' keys (order irrelevant: keys are unique)
-    for (int i0 = 0; i0 < N; i0 += kThreads) {
-        const int i = i0 + threadIdx.x;
-        const unsigned long long key = i < N ? wta_key(L, P, i, T) : ~0ull;
-        const unsigned m = __ballot_sync(0xffffffffu, key != ~0ull);
+
+    auto emit = [&](unsigned long long key, bool valid) {
+        const unsigned m = __ballot_sync(0xffffffffu, valid);
         unsigned base = 0;
-        if (lane == 0 && m) base = atomicAdd(&nlive, (unsigned)__popc(m));
+        if (lane == 0 && m) base = atomicAdd(&nkeys, (unsigned)__popc(m));
         base = __shfl_sync(0xffffffffu, base, 0);
         const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
-        if (key != ~0ull && pos < kCap) keys[pos] = key;
+        if (valid) {
+            if (pos < a.cap) keys[pos] = key;
+            else overflow = 1;
+        }
+    };
+
+    if (a.mode == 0) {
+        const int n = a.C * np_slice;
+        for (int q0 = 0; q0 < n; q0 += kThreads) {
+            const int q = q0 + threadIdx.x;
+            unsigned long long key = ~0ull;
+            if (q < n) {
+                const int c = q / np_slice, p = p_lo + (q - c * np_slice);
+                key = wta_key(L, P, c * HW + p, T);
+            }
+            emit(key, key != ~0ull);
+        }
+    } else if (a.mode == 1) {
+        for (int q0 = 0; q0 < np_slice; q0 += kThreads) {
+            const int p = p_lo + q0 + threadIdx.x;
+            unsigned long long top[KK];
+#pragma unroll
+            for (int j = 0; j < KK; ++j) top[j] = ~0ull;
+            if (p < p_hi) {
+                int c = 0;
+                for (; c + 8 <= a.C; c += 8) {
+                    int l[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) l[u] = __ldg(L + (size_t)(c + u) * HW + p);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (l[u] < T) {
+                            const int i = (c + u) * HW + p;
+                            unsigned long long key = ((unsigned long long)l[u] << 56) |
+                                                     ((unsigned long long)(~spk_float_order_u32(__ldg(P + i))) << 24) |
+                                                     (unsigned long long)i;
+#pragma unroll
+                            for (int j = 0; j < KK; ++j) {  // sorted insertion, registers only
+                                const unsigned long long lo = umin64(top[j], key);
+                                key = top[j] < key ? key : top[j];
+                                top[j] = lo;
+                            }
+                        }
+                    }
+                }
+                for (; c < a.C; ++c) {
+                    unsigned long long key = wta_key(L, P, c * HW + p, T);
+                    if (key != ~0ull) {
+#pragma unroll
+                        for (int j = 0; j < KK; ++j) {
+                            const unsigned long long lo = umin64(top[j], key);
+                            key = top[j] < key ? key : top[j];
+                            top[j] = lo;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < KK; ++j) emit(top[j], top[j] != ~0ull);
+        }
     }
     __syncthreads();
-    const int nl = (int)nlive;
-    const bool cached = nl <= kCap;
-    for (int round = 0; round < k; ++round) {
-        const int np = npicked;
+    const bool cached = !overflow;
+    const int nl = cached ? (int)nkeys : 0;
+
+    int npicked = 0;
+    for (int round = 0; round < a.k; ++round) {
         unsigned long long best = ~0ull;
-        const int n = cached ? nl : N;
-        for (int q = threadIdx.x; q < n; q += kThreads) {
-            const unsigned long long key = cached ? keys[q] : wta_key(L, P, q, T);
-            if (key == ~0ull) continue;
+        auto consider = [&](unsigned long long key) {
             const int i = (int)(key & 0xffffffull);
-            const int c = i / HW, r = i - c * HW, y = r / W, x = r - y * W;
-            bool dead = false;
-            for (int t = 0; t < np; ++t)
-                if (pc[t] == c || (abs(py[t] - y) <= radius && abs(px[t] - x) <= radius)) {
-                    dead = true;
-                    break;
-                }
-            if (!dead) best = umin64(best, key);
+            const int c = i / HW, r = i - c * HW, y = r / a.W, x = r - y * a.W;
+            for (int t = 0; t < npicked; ++t)
+                if (pc[t] == c || (abs(py[t] - y) <= a.radius && abs(px[t] - x) <= a.radius)) return;
+            best = umin64(best, key);
+        };
+        if (cached) {
+            for (int q = threadIdx.x; q < nl; q += kThreads) consider(keys[q]);
+        } else {
+            const int n = a.C * np_slice;
+            for (int q = threadIdx.x; q < n; q += kThreads) {
+                const int c = q / np_slice, p = p_lo + (q - c * np_slice);
+                const unsigned long long key = wta_key(L, P, c * HW + p, T);
+                if (key != ~0ull) consider(key);
+            }
         }
         for (int o = 16; o; o >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, o));
         if (lane == 0) red[threadIdx.x >> 5] = best;
@@ -85,25 +180,60 @@ __global__ void __launch_bounds__(kThreads) wta_kernel(const uint8_t* __restrict
         if (threadIdx.x < 32) {
             best = lane < kThreads / 32 ? red[lane] : ~0ull;
             for (int o = 16; o; o >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, o));
-            if (threadIdx.x == 0) {
-                spk_winner w;
-                if (best != ~0ull) {
-                    const int i = (int)(best & 0xffffffull);
-                    const int c = i / HW, r = i - c * HW, y = r / W, x = r - y * W;
-                    w = {b, (int)(best >> 56), c, y, x, 0};
-                    pc[np] = c;
-                    py[np] = y;
-                    px[np] = x;
-                    npicked = np + 1;
-                } else {
-                    w = {-1, -1, -1, -1, -1, -1};
-                }
-                win[(size_t)b * k + round] = w;
-            }
+            if (lane == 0) cmin[round & 1] = best;
+        }
+        cluster.sync();  // every CTA's slice minimum of this round is visible
+        if (threadIdx.x == 0) {
+            unsigned long long g = ~0ull;
+            for (int r = 0; r < a.cs; ++r) g = umin64(g, *cluster.map_shared_rank(&cmin[round & 1], r));
+            red[0] = g;
         }
         __syncthreads();
+        const unsigned long long g = red[0];
+        if (g == ~0ull) break;  // nothing live and unsuppressed anywhere in the sample
+        const int i = (int)(g & 0xffffffull);
+        const int c = i / HW, r = i - c * HW, y = r / a.W, x = r - y * a.W;
+        if (threadIdx.x == 0) {
+            pc[npicked] = c;
+            py[npicked] = y;
+            px[npicked] = x;
+            if (rank == 0) a.win[(size_t)b * a.k + round] = spk_winner{b, (int)(g >> 56), c, y, x, 0};
+        }
+        ++npicked;
+        __syncthreads();
     }
-    if (threadIdx.x == 0) nwin[b] = npicked;
+    if (rank == 0 && threadIdx.x == 0) {
+        for (int r = npicked; r < a.k; ++r) a.win[(size_t)b * a.k + r] = spk_winner{-1, -1, -1, -1, -1, -1};
+        a.nwin[b] = npicked;
+    }
+    // no CTA may exit while a peer can still read its cmin slot
+    cluster.sync();
+}
+
+template <int KK>
+spk_status launch_wta(const WtaArgs& a, int B, size_t cap, cudaStream_t s) {
+    auto kern = wta_cluster_kernel<KK>;
+    const size_t smem = cap * 8;  // shared key buffer sized to the slice's candidate bound
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kCapKeys * 8) != cudaSuccess)
+            return spk::launched("wta_cluster_kernel(attr)");
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.cs, (unsigned)B, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a);
+    return spk::launched("wta_cluster_kernel");
 }
 
 }  // namespace
@@ -117,9 +247,32 @@ extern "C" spk_status spk_wta(const uint8_t* lat, const float* pstar, int B, int
     SPK_CHECK_PTR(nwin);
     SPK_CHECK(B >= 1 && C >= 1 && H >= 1 && W >= 1, SPK_ERR_SHAPE, "non-positive size");
     SPK_CHECK((long long)C * H * W <= (1 << 24), SPK_ERR_UNSUPPORTED, "C*H*W > 2^24 per sample");
+    SPK_CHECK(B <= 65535, SPK_ERR_UNSUPPORTED, "B=%d > 65535", B);
     SPK_CHECK(T >= 1 && T <= 254, SPK_ERR_UNSUPPORTED, "T=%d outside 1..254", T);
     SPK_CHECK(k >= 1 && k <= kMaxK, SPK_ERR_ARG, "k=%d outside 1..%d", k, kMaxK);
     SPK_CHECK(radius >= 0, SPK_ERR_ARG, "radius < 0");
-    wta_kernel<<<B, kThreads, 0, spk::as_cuda(stream)>>>(lat, pstar, C, H, W, T, k, radius, win, nwin);
-    return spk::launched("wta_kernel");
+    WtaArgs a{lat, pstar, C, H, W, T, k, radius, 1, 0, 0u, win, nwin};
+    const long long N = (long long)C * H * W, HW = (long long)H * W;
+    // cluster size: about 16K neurons per CTA, at most 8 CTAs and at most one pixel... per CTA
+    a.cs = (int)std::min<long long>(std::min<long long>(kMaxCS, (N + 16383) / 16384), HW);
+    if (a.cs < 1) a.cs = 1;
+    const long long slice_n = C * ((HW + a.cs - 1) / a.cs);
+    const int keep = std::min(k, C);
+    int KK = 1;
+    while (KK < keep) KK <<= 1;
+    const long long slice_p = (HW + a.cs - 1) / a.cs;
+    long long cap = 1;
+    if (slice_n <= kCapKeys) a.mode = 0, cap = slice_n;
+    else if (KK <= 16 && slice_p * KK <= kCapKeys) a.mode = 1, cap = slice_p * KK;
+    else a.mode = 2;
+    a.cap = (unsigned)cap;
+    const cudaStream_t s = spk::as_cuda(stream);
+    if (a.mode != 1) return launch_wta<1>(a, B, (size_t)cap, s);
+    switch (KK) {
+        case 1: return launch_wta<1>(a, B, (size_t)cap, s);
+        case 2: return launch_wta<2>(a, B, (size_t)cap, s);
+        case 4: return launch_wta<4>(a, B, (size_t)cap, s);
+        case 8: return launch_wta<8>(a, B, (size_t)cap, s);
+        default: return launch_wta<16>(a, B, (size_t)cap, s);
+    }
 }

@@ -76,6 +76,22 @@ def test_rank_code_large_sample_global_path(spk):
         np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, sort)), oracle.rank_code(y, T, 0.01, sort))
 
 
+@pytest.mark.parametrize("T", [1, 15, 30, 254])
+def test_rank_code_large_sample_histogram_path(spk, T):
+    """N > 8192, sort on: bucket histogram + boundary-bucket sort, and its radix-select
+    fallback when a boundary bucket holds more exact ties than shared memory."""
+    cfg = synth.load_config("c4")
+    imgs = synth.images(cfg, 0, 2)
+    y = oracle.filter_apply(imgs, opipe.filter_bank(cfg), 3)   # C4-shaped Gabor responses
+    y = np.concatenate([y.reshape(2, -1), RNG.normal(0, 1, (4, y[0].size)).astype(np.float32)])
+    y[2, : y.shape[1] // 2] = 0.5                              # 80,000 exact ties -> fallback
+    y[3] = np.round(y[3], 2)                                   # ties across many buckets
+    y[4] = -1.0
+    y[4, 12345] = 3.0                                          # a single positive
+    y[5, 1::3] = np.float32(2.0) ** RNG.integers(-6, 6, y[5, 1::3].shape)  # bucket edges
+    np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, True)), oracle.rank_code(y, T, 0.01, True))
+
+
 # ------------------------------------------------------------------------- a3 conv
 CONV_CASES = [
     # B, T, Ci, Hi, Wi, Co, K, stride, pad
@@ -198,6 +214,18 @@ def test_pool_exact(spk, L, s, p):
     np.testing.assert_array_equal(host(spk.pool(cu(lat), T, L, s, p)), ref)
 
 
+# plane shapes of the large configs: C5 conv1 (16-byte rows), C4 conv1 (2-byte rows),
+# many small planes per CTA, and a plane too large for shared memory (global path)
+@pytest.mark.parametrize("shape,L,s,p", [((2, 3, 224, 224), 2, 2, 0), ((1, 5, 160, 250), 2, 2, 0),
+                                          ((3, 250, 14, 14), 3, 3, 0), ((1, 1, 300, 330), 2, 2, 1),
+                                          ((2, 4, 50, 45), 3, 2, 1)])
+def test_pool_exact_large_planes(spk, shape, L, s, p):
+    T = 15
+    lat = RNG.integers(0, T + 1, shape).astype(np.uint8)
+    ref = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(lat, T), (L, L), (s, s), (p, p)))
+    np.testing.assert_array_equal(host(spk.pool(cu(lat), T, L, s, p)), ref)
+
+
 # ----------------------------------------------------------------- a6 inhibit, a7 wta
 def _records(B, T, C, H, W, dens=0.4, ties=False):
     P = np.cumsum(RNG.uniform(0, 1, (B, T, C, H, W)) * (RNG.random((B, 1, C, H, W)) < dens), axis=1)
@@ -220,6 +248,18 @@ def test_inhibit_exact(spk, ties):
     np.testing.assert_array_equal(host(gps), rps.astype(np.float32))
 
 
+@pytest.mark.parametrize("ties", [False, True])
+def test_inhibit_exact_large_maps(spk, ties):
+    """HW >= 4096: the 4-pixels-per-thread register kernel (C4 shapes)."""
+    T = 10
+    Q, lat, ps = _records(2, T, 9, 64, 80, 0.5, ties)
+    ref = oracle.inhibit(Q)
+    rlat, rps = lat_and_pstar(ref, 0.0)
+    glat, gps = spk.inhibit(cu(lat), cu(ps.astype(np.float32)), T)
+    np.testing.assert_array_equal(host(glat), rlat)
+    np.testing.assert_array_equal(host(gps), rps.astype(np.float32))
+
+
 @pytest.mark.parametrize("k,r", [(5, 3), (8, 1), (1, 0), (3, 10), (20, 0)])
 @pytest.mark.parametrize("ties", [False, True])
 def test_wta_exact(spk, k, r, ties):
@@ -232,6 +272,23 @@ def test_wta_exact(spk, k, r, ties):
     for b in range(4):
         np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
         assert (gw[b, nwin[b]:] == -1).all()
+
+
+# (C, H, W, k, r): a 2-CTA cluster keeping every live key; 8-CTA clusters with the
+# per-pixel top-k pre-reduction (k=5 -> 8 kept, k=8 with a C4-like slice); a slice
+# that overflows shared memory and re-reads its records every round (k=20)
+@pytest.mark.parametrize("C,H,W,k,r", [(8, 50, 50, 5, 3), (40, 60, 70, 5, 3), (128, 40, 50, 8, 1),
+                                       (40, 60, 70, 20, 2)])
+@pytest.mark.parametrize("ties", [False, True])
+def test_wta_exact_large_samples(spk, C, H, W, k, r, ties):
+    T = 15
+    Q, lat, ps = _records(2, T, C, H, W, 0.3, ties)
+    win, nwin = oracle.wta(Q, k, r)
+    gw, gn = spk.wta(cu(lat), cu(ps.astype(np.float32)), T, k, r)
+    gw, gn = host(gw), host(gn)
+    np.testing.assert_array_equal(gn, nwin)
+    for b in range(2):
+        np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
 
 
 # ------------------------------------------------------------------------- a8 stdp
