@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--prec", default="auto", choices=["auto", "exact", "event", "fp32"],
                     help="conv engine: auto = event form for small-N layers, tcgen05 otherwise (bit-identical)")
+    ap.add_argument("--dp", action="store_true",
+                    help="training configs under torchrun: one model, data-parallel mini-batch STDP (SURVEY NEXT-2): "
+                         "per-GPU batch fixed, winners + input maps all-gathered, same update on every rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8, help="images in the oracle cpu_baseline sample")
     return ap.parse_args()
@@ -189,6 +192,11 @@ def main():
     labels = synth.labels(cfg, start, B)
     Ws = synth.layer_weights(cfg)
     net = Network(cfg, B, device=dev, prec=args.prec)
+    dp = args.dp and not forward
+    if dp:
+        net.enable_dp(start, B * world, parallel.allgather_equal)
+    # NCCL collectives stay outside CUDA graphs: a data-parallel step at N > 1 runs eagerly
+    use_graph = not (dp and world > 1)
     net.img.copy_(torch.from_numpy(imgs))
     net.labels.copy_(torch.from_numpy(labels))
     net.set_weights([torch.from_numpy(w) for w in Ws])
@@ -220,7 +228,8 @@ def main():
         e.record(torch.cuda.current_stream(dev))
         gmarks.append((name, e))
 
-    net.capture(warmup=1, mark=gmark)
+    if use_graph:
+        net.capture(warmup=1, mark=gmark)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     for _ in range(args.warmup):
         net.replay()
@@ -238,7 +247,11 @@ def main():
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        net.replay()
+        if use_graph:
+            net.replay()
+        else:
+            gmarks.clear()
+            net.step_marked(gmark)
         e1.record(stream)
         evs.append((e0, e1))
         e1.synchronize()  # the graph's stage events are reused by the next replay
@@ -315,8 +328,11 @@ def main():
                        "T": T, "precision": args.prec,
                        "conv_engines": {f"conv{i}": rec["prec"] for i, rec in enumerate(net.layers)},
                        "parallelism": (f"dp{world}: image shards, NCCL weight broadcast ({bcast_ms:.3f} ms, untimed)"
-                                       if forward else f"replicas x{world} (no data-path collective)"),
-                       "l2": "flushed between timed steps (256 MiB write)", "cuda_graph": True},
+                                       if forward else
+                                       f"dp{world}: one model, mini-batch STDP over {world * B} images, all-gather of "
+                                       "winners + trained-layer input maps (NCCL), identical update on every rank"
+                                       if dp else f"replicas x{world} (no data-path collective)"),
+                       "l2": "flushed between timed steps (256 MiB write)", "cuda_graph": use_graph},
             "e2e": {"value": total_imgs / (e2e_ms * 1e-3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches_per_step * args.steps),

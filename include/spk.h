@@ -57,7 +57,7 @@ typedef enum {
 SPK_API const char* spk_last_error(void);
 /* ABI version of this header (bumped on any signature change). */
 SPK_API int spk_abi_version(void);
-#define SPK_ABI_VERSION 1
+#define SPK_ABI_VERSION 2
 /* Name of the last kernel launched by this thread (diagnostics). */
 SPK_API const char* spk_last_kernel(void);
 /* Number of kernels this process launched through the library. */
@@ -280,6 +280,16 @@ SPK_API spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* lat
  * Errors: SPK_ERR_ARG. */
 SPK_API spk_status spk_rstdp_route(spk_winner* win, const int32_t* nwin, int B, int k,
                            const int32_t* labels, int maps_per_class, spk_stream stream);
+
+/* spk_winners_rebase — data-parallel mini-batch STDP:
+ * a rank that forwarded the samples [b0, b0 + B) of a global mini-batch adds b0 to
+ * the sample index of each of its valid winners (slots < nwin[b]; empty slots stay
+ * -1), so that after an all-gather every replica applies the same winners, in the
+ * same (global sample, pick) order, to the global batch's input latency maps (R-BATCH).
+ *   win [dev] spk_winner [B][k] (in place), nwin [dev] i32 [B].
+ * Errors: SPK_ERR_ARG (B < 1, k < 1, b0 < 0). */
+SPK_API spk_status spk_winners_rebase(spk_winner* win, const int32_t* nwin, int B, int k, int b0,
+                              spk_stream stream);
 
 /* ========================================================================
  * a9  gather + boundary conversions

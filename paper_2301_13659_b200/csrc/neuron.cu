@@ -297,6 +297,15 @@ __global__ void rstdp_route_kernel(spk_winner* __restrict__ win, const int32_t* 
     w.cfg = (w.c / mpc == labels[w.b]) ? 0 : 1;  // reward : punish (R-CLASSMAP)
 }
 
+// ---------------------------------------------------------------- data-parallel STDP
+__global__ void winners_rebase_kernel(spk_winner* __restrict__ win, const int32_t* __restrict__ nwin, int B, int k,
+                                      int b0) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= B * k) return;
+    const int b = q / k, s = q % k;
+    if (s < nwin[b]) win[q].b += b0;  // local sample index -> index in the global mini-batch
+}
+
 }  // namespace
 
 extern "C" spk_status spk_fire(const float* pot, int B, int T, int C, int H, int W, float theta,
@@ -432,4 +441,15 @@ extern "C" spk_status spk_rstdp_route(spk_winner* win, const int32_t* nwin, int 
     rstdp_route_kernel<<<spk::ceil_div((size_t)B * k, kT), kT, 0, spk::as_cuda(stream)>>>(win, nwin, B, k, labels,
                                                                                         maps_per_class);
     return spk::launched("rstdp_route_kernel");
+}
+
+extern "C" spk_status spk_winners_rebase(spk_winner* win, const int32_t* nwin, int B, int k, int b0,
+                                         spk_stream stream) {
+    spk::clear_error();
+    SPK_CHECK_PTR(win);
+    SPK_CHECK_PTR(nwin);
+    SPK_CHECK(B >= 1 && k >= 1 && b0 >= 0, SPK_ERR_ARG, "B=%d k=%d b0=%d", B, k, b0);
+    SPK_CHECK((long long)B * k < (1ll << 31), SPK_ERR_ARG, "B*k too large");
+    winners_rebase_kernel<<<spk::ceil_div((size_t)B * k, kT), kT, 0, spk::as_cuda(stream)>>>(win, nwin, B, k, b0);
+    return spk::launched("winners_rebase_kernel");
 }

@@ -93,6 +93,28 @@ class Network:
         src = last["pooled"] if last["pooled"] is not None else last["lat"]
         self.features = torch.empty(src.shape, dtype=torch.float32, device=self.dev)
         self.graph = None
+        self.dp = None
+
+    def enable_dp(self, b0: int, batch_total: int, allgather):
+        """Data-parallel mini-batch STDP (SURVEY §8(f) NEXT-2, P:L178 / R-BATCH): this replica
+        forwards the samples [b0, b0 + B) of a global mini-batch of `batch_total` with the
+        pre-batch weights; its winners are rebased to global sample indices and
+        `allgather(dst, src)` collects every replica's winner records and trained-layer
+        input latency maps in rank order, so every replica applies the same sequential
+        update to the same weights — bit-identical to single-GPU training on the global
+        batch, with no weight broadcast."""
+        tl = self.cfg["train_layer"]
+        rec = self.layers[tl]
+        src = self.input_of(tl)
+        self.dp = dict(
+            b0=b0, Bt=batch_total, gather=allgather,
+            lat=torch.empty((batch_total,) + tuple(src.shape[1:]), dtype=torch.uint8, device=self.dev),
+            win=torch.empty((batch_total, self.k, 6), dtype=torch.int32, device=self.dev),
+            nwin=torch.empty((batch_total,), dtype=torch.int32, device=self.dev))
+        g = spk.ConvGeom(batch_total, self.T, rec["geom"].Ci, rec["geom"].Hi, rec["geom"].Wi, rec["L"]["Co"],
+                         rec["L"]["K"], rec["L"]["K"], rec["L"]["stride"], rec["L"]["stride"], rec["L"]["pad"],
+                         rec["L"]["pad"])
+        self.stdp_ws = torch.empty(spk.stdp_workspace(g, self.k), dtype=torch.uint8, device=self.dev)
 
     # ------------------------------------------------------------ data in
     def set_weights(self, ws):
@@ -138,8 +160,13 @@ class Network:
 
     def train_step(self, mark=_nomark):
         """Listing 3 train_layer{l} for l = cfg['train_layer'] (R-STDP if cfg['learning'] == 'rstdp')."""
-        tl = self.cfg["train_layer"]
         mark("start")
+        self.train_forward(mark)
+        self.train_update(mark)
+
+    def train_forward(self, mark=_nomark):
+        """Forward to the trained layer's (lat, P*) record -> inhibit -> convwta (-> R-STDP routing)."""
+        tl = self.cfg["train_layer"]
         self.front(mark)
         for li in range(tl):
             self.layer(li, mark=mark)
@@ -153,7 +180,21 @@ class Network:
         if self.cfg["learning"] == "rstdp":
             spk.rstdp_route(self.win, self.nwin, self.labels, self.cfg["maps_per_class"])
             mark("rstdp_route")
-        spk.stdp(self.weights[tl], self.input_of(tl), self.win, self.nwin, None, self.T, L["stride"], L["pad"],
+
+    def train_update(self, mark=_nomark):
+        """conv.stdp with this step's winners (after the data-parallel exchange, if enabled)."""
+        tl = self.cfg["train_layer"]
+        L = self.layers[tl]["L"]
+        lat_in, win, nwin = self.input_of(tl), self.win, self.nwin
+        if self.dp is not None:  # exchange winners + receptive-field inputs (NCCL all-gather on GPUs)
+            d = self.dp
+            spk.winners_rebase(self.win, self.nwin, d["b0"])
+            d["gather"](d["win"], self.win)
+            d["gather"](d["nwin"], self.nwin)
+            d["gather"](d["lat"], lat_in)
+            lat_in, win, nwin = d["lat"], d["win"], d["nwin"]
+            mark("allgather")
+        spk.stdp(self.weights[tl], lat_in, win, nwin, None, self.T, L["stride"], L["pad"],
                  ws=self.stdp_ws, cfg_arr=self.stdp_cfg)
         mark("stdp")
 

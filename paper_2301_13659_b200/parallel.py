@@ -5,7 +5,11 @@ sample, conv / fire / pool / inhibit / WTA / gather are per sample), so a batch
 shards by contiguous image ranges with no data-path collective.  The only
 collectives are the weight broadcast before a sharded forward and an optional
 gather of features/records after it.  STDP training is sample-sequential
-(reading R-BATCH): training ranks run independent replicas.
+(reading R-BATCH): training ranks run independent replicas, or — with
+data-parallel mini-batch STDP (`Network.enable_dp`) — one
+model whose global mini-batch is split across ranks: every rank all-gathers the
+winner records and the trained layer's input latency maps and applies the same
+sequential update, so the replicas stay bit-identical with no weight broadcast.
 """
 from __future__ import annotations
 
@@ -40,3 +44,18 @@ def gather_rows(x: torch.Tensor, n_total: int) -> torch.Tensor | None:
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad)
     return torch.cat([p[:s] for p, s in zip(parts, sizes)])
+
+
+def allgather_equal(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """dst[r * n : (r + 1) * n] = rank r's src (n = src.shape[0], equal on every rank), in rank order."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        dst.copy_(src)
+        return
+    try:
+        dist.all_gather_into_tensor(dst, src.contiguous())
+    except (RuntimeError, NotImplementedError):  # backends without the fused form (older gloo)
+        parts = list(dst.chunk(dist.get_world_size()))
+        tmp = [torch.empty_like(p) for p in parts]
+        dist.all_gather(tmp, src.contiguous())
+        for p, t in zip(parts, tmp):
+            p.copy_(t)

@@ -40,7 +40,7 @@ class StdpConfig(ctypes.Structure):
 EXPORTS = [
     "spk_last_error", "spk_abi_version", "spk_last_kernel", "spk_launch_count", "spk_dog", "spk_gabor",
     "spk_rank_code_workspace", "spk_rank_code", "spk_conv_workspace", "spk_conv", "spk_fire", "spk_pool",
-    "spk_inhibit", "spk_wta", "spk_stdp_workspace", "spk_stdp", "spk_rstdp_route", "spk_gather",
+    "spk_inhibit", "spk_wta", "spk_stdp_workspace", "spk_stdp", "spk_rstdp_route", "spk_winners_rebase", "spk_gather",
     "spk_lat_to_dense", "spk_dense_to_lat", "spk_conv_status", "spk_conv_fire_pool_supported", "spk_conv_fire_pool",
 ]
 
@@ -72,6 +72,7 @@ def lib():
             "spk_stdp_workspace": ([ctypes.POINTER(ConvGeom), I], Z),
             "spk_stdp": ([V, ctypes.POINTER(ConvGeom), V, V, V, I, ctypes.POINTER(StdpConfig), I, V, Z, V], I),
             "spk_rstdp_route": ([V, V, I, I, V, I, V], I),
+            "spk_winners_rebase": ([V, V, I, I, I, V], I),
             "spk_gather": ([V, Z, I, V, V], I),
             "spk_lat_to_dense": ([V, I, I, Z, V, V], I),
             "spk_dense_to_lat": ([V, I, I, Z, V, V, V], I),
@@ -309,6 +310,13 @@ def stdp(w: torch.Tensor, lat_in: torch.Tensor, win: torch.Tensor, nwin: torch.T
 def rstdp_route(win: torch.Tensor, nwin: torch.Tensor, labels: torch.Tensor, maps_per_class: int):
     B, k, _ = win.shape
     _check("spk_rstdp_route", lib().spk_rstdp_route(_p(win), _p(nwin), B, k, _p(labels), maps_per_class, _s()))
+    return win
+
+
+def winners_rebase(win: torch.Tensor, nwin: torch.Tensor, b0: int):
+    """Local -> global sample index of every valid winner (data-parallel mini-batch STDP)."""
+    B, k, _ = win.shape
+    _check("spk_winners_rebase", lib().spk_winners_rebase(_p(win), _p(nwin), B, k, int(b0), _s()))
     return win
 
 

@@ -526,3 +526,42 @@ def test_conv_fire_pool_fused(spk, case):
     got = spk.conv_fire_pool(cu(lat), cu(w), T, s, p, prec="event", theta=theta, pool_kernel=L, pool_stride=ps,
                              pool_pad=pp)
     np.testing.assert_array_equal(host(got), host(ref))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_data_parallel_stdp_shards_equal_whole_batch(spk, name):
+    """NEXT-2 on one GPU: two shards forwarded separately with the pre-batch weights, winners
+    rebased to global sample indices (spk_winners_rebase) and concatenated in shard order,
+    then one STDP over the global batch == the whole-batch train step, bit for bit (R-BATCH);
+    and Network.enable_dp's exchange path (identity gather at world size 1) == train_step."""
+    from paper_2301_13659_b200.network import Network
+    cfg = synth.load_config(name)
+    tl = cfg["train_layer"]
+    n, half = 64, 32
+    imgs, lab = synth.images(cfg, 0, n), synth.labels(cfg, 0, n)
+    Ws = [torch.from_numpy(w) for w in synth.layer_weights(cfg)]
+
+    def make(lo, hi):
+        net = Network(cfg, hi - lo, prec="auto")
+        net.img.copy_(torch.from_numpy(imgs[lo:hi]))
+        net.labels.copy_(torch.from_numpy(lab[lo:hi]))
+        net.set_weights(Ws)
+        return net
+    whole = make(0, n)
+    whole.train_step()
+    shards = [make(0, half), make(half, n)]
+    for s, net in enumerate(shards):
+        net.train_forward()
+        spk.winners_rebase(net.win, net.nwin, s * half)
+    g_win = torch.cat([net.win for net in shards])
+    g_nwin = torch.cat([net.nwin for net in shards])
+    g_lat = torch.cat([net.input_of(tl) for net in shards])
+    L = cfg["layers"][tl]
+    W = Ws[tl].clone().cuda()
+    spk.stdp(W, g_lat, g_win, g_nwin, None, cfg["T"], L["stride"], L["pad"], cfg_arr=spk.stdp_configs(cfg["stdp"]))
+    np.testing.assert_array_equal(host(W), host(whole.weights[tl]))
+    assert int(host(g_nwin).sum()) == int(host(whole.nwin).sum()) > 0
+    dp = make(0, n)
+    dp.enable_dp(0, n, lambda dst, src: dst.copy_(src))
+    dp.train_step()
+    np.testing.assert_array_equal(host(dp.weights[tl]), host(whole.weights[tl]))

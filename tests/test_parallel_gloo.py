@@ -76,3 +76,42 @@ def test_sharded_forward_equals_single_process(tmp_path, world):
     cfg["layers"][0]["pool"] = {"kernel": 2, "stride": 2, "pad": 0}
     ref = opipe.infer(cfg, synth.images(cfg, 0, 5), synth.layer_weights(cfg), event=True)
     np.testing.assert_array_equal(np.load(out), ref)
+
+
+def _dp_worker(rank, world, port, out_path, n):
+    """Data-parallel mini-batch STDP: each rank forwards its shard with the
+    pre-batch weights, rebases its winners to global sample indices, all-gathers winners and
+    the trained layer's input trains, and applies the global sequential update."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.load_config("c1")
+    start, count = parallel.shard_range(n, world, rank)
+    Ws = synth.layer_weights(cfg)
+    r = opipe.train_step(cfg, synth.images(cfg, start, count), Ws, event=True)
+    win = r["win"].copy()
+    for b in range(count):  # the product does this on the GPU (spk_winners_rebase)
+        win[b, : r["nwin"][b], 0] += start
+    g_win = torch.empty((n,) + win.shape[1:], dtype=torch.int32)
+    g_nwin = torch.empty((n,), dtype=torch.int32)
+    S_in = r["S_in"]
+    g_S = torch.empty((n,) + S_in.shape[1:], dtype=torch.uint8)
+    parallel.allgather_equal(g_win, torch.from_numpy(win))
+    parallel.allgather_equal(g_nwin, torch.from_numpy(r["nwin"].astype(np.int32)))
+    parallel.allgather_equal(g_S, torch.from_numpy(S_in.astype(np.uint8)))
+    L = cfg["layers"][0]
+    W = oracle.stdp(Ws[0], g_S.numpy(), g_win.numpy(), g_nwin.numpy(), [tuple(c) for c in cfg["stdp"]],
+                    (L["stride"],) * 2, (L["pad"],) * 2)
+    np.save(out_path.replace(".npy", f"_{rank}.npy"), W)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_data_parallel_stdp_equals_single_process(tmp_path):
+    world, n = 2, 4
+    out = str(tmp_path / "w.npy")
+    mp.spawn(_dp_worker, args=(world, _free_port(), out, n), nprocs=world, join=True)
+    cfg = synth.load_config("c1")
+    ref = opipe.train_step(cfg, synth.images(cfg, 0, n), synth.layer_weights(cfg), event=True)
+    assert ref["nwin"].sum() > 0
+    for r in range(world):  # every replica holds the single-process batch-trained weights, bit for bit
+        np.testing.assert_array_equal(np.load(out.replace(".npy", f"_{r}.npy")), ref["W_new"])
