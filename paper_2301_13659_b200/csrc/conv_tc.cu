@@ -48,7 +48,8 @@
 
 #ifndef SPK_EXP
 #define SPK_EXP 0  // timing experiments only: 1 no wait::st, 2 no gather, 4 no tcgen05.st, 8 no epilogue stores,
-                   // 16 no epilogue tcgen05.ld, 32 no MMA
+                   // 16 no epilogue tcgen05.ld, 32 no MMA, 512 no fire-epilogue TMEM loads,
+                   // 1024 fire epilogue without threshold work
 #endif
 
 namespace {
@@ -759,9 +760,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 // and the accumulator is released as soon as its last load has landed
                 uint32_t ra[24], rb[24];
                 auto ld8 = [&](int n0, uint32_t* r) {
+#if (SPK_EXP & 512)  // timing experiment: fire epilogue without TMEM loads (synthetic digits)
+#pragma unroll
+                    for (int q = 0; q < 24; ++q) r[q] = (uint32_t)(n0 * 7 + q + lane);
+#else
                     tmem_ld8(tbase + n0, r);
                     tmem_ld8(tbase + a.Nt + n0, r + 8);
                     tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
+#endif
                 };
                 uint32_t mine = 0;
                 // P*: the lane holding a (pixel, map)'s first crossing (its bit set, the previous
@@ -769,6 +775,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 const unsigned segstart = (TP == 16) ? 0x00010001u : 0x1u;
                 float* ps_tile = ob_ps + ob * a.Nt * PPT + pix;
                 auto half = [&](const uint32_t* r, int j0, int c0) {  // c0: tile column of r[0]
+#if (SPK_EXP & 1024)  // timing experiment: TMEM loads kept, threshold work reduced to one ballot
+                    {
+                        const unsigned bal = __ballot_sync(0xffffffffu, (r[0] ^ r[8] ^ r[16] ^ r[23]) > 7u);
+                        if (j0 == own_col) mine = bal;
+                        return;
+                    }
+#endif
                     if (a.small_x) {  // 32-bit form of X > theta_q (see TcArgs)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {

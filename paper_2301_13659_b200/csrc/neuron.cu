@@ -217,10 +217,9 @@ __global__ void __launch_bounds__(kT) inhibit_wide_kernel(uint8_t* __restrict__ 
     float* P = pstar + (size_t)b * C * HW + p;
     unsigned long long best[4] = {~0ull, ~0ull, ~0ull, ~0ull};
     const uint32_t tt = 0x01010101u * (uint32_t)T;
-#pragma unroll 4
-    for (int c = 0; c < C; ++c) {
-        const uint32_t l4 = *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW);
-        if (__vcmpltu4(l4, tt) == 0u) continue;  // nothing fired at these 4 pixels
+    constexpr int U = 8;  // channels whose latency words are loaded before any is used
+    auto consider = [&](int c, uint32_t l4) {
+        if (__vcmpltu4(l4, tt) == 0u) return;  // nothing fired at these 4 pixels
         const float4 p4 = *reinterpret_cast<const float4*>(P + (size_t)c * HW);
         const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
@@ -232,23 +231,38 @@ __global__ void __launch_bounds__(kT) inhibit_wide_kernel(uint8_t* __restrict__ 
                 best[j] = key < best[j] ? key : best[j];
             }
         }
+    };
+    int c = 0;
+    for (; c + U <= C; c += U) {
+        uint32_t l4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) l4[u] = *reinterpret_cast<const uint32_t*>(L + (size_t)(c + u) * HW);
+#pragma unroll
+        for (int u = 0; u < U; ++u) consider(c + u, l4[u]);
     }
+    for (; c < C; ++c) consider(c, *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW));
     const uint32_t wc[4] = {(uint32_t)(best[0] & 0xFFFFFFu), (uint32_t)(best[1] & 0xFFFFFFu),
                             (uint32_t)(best[2] & 0xFFFFFFu), (uint32_t)(best[3] & 0xFFFFFFu)};
-#pragma unroll 4
-    for (int c = 0; c < C; ++c) {
-        const uint32_t l4 = *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW);
+    auto suppress = [&](int c, uint32_t l4) {
         uint32_t kill = __vcmpltu4(l4, tt);  // 0xff per firing byte
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (wc[j] == (uint32_t)c) kill &= ~(0xffu << (8 * j));
-        if (kill == 0u) continue;
+        if (kill == 0u) return;
         *reinterpret_cast<uint32_t*>(L + (size_t)c * HW) = (l4 & ~kill) | (tt & kill);
         float* pp = P + (size_t)c * HW;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (kill & (0xffu << (8 * j))) pp[j] = 0.0f;
+    };
+    for (c = 0; c + U <= C; c += U) {
+        uint32_t l4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) l4[u] = *reinterpret_cast<const uint32_t*>(L + (size_t)(c + u) * HW);
+#pragma unroll
+        for (int u = 0; u < U; ++u) suppress(c + u, l4[u]);
     }
+    for (; c < C; ++c) suppress(c, *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW));
 }
 
 // ---------------------------------------------------------------- gather

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const floa
 //          bucket).  Exactly the ranks of the full sort.
 // More boundary-bucket values than fit shared memory (massive exact ties) -> the
 // sample falls back to the multi-target radix select above (exact, slower).
-constexpr int kBkt = 32768, kCand = 8192, kHT = 1024, kMaxBnd = 256;
+constexpr int kBkt = 32768, kCand = 8192, kHT = 1024, kMaxBnd = 256, kUnroll = 4;
 constexpr size_t kHistSmem = (size_t)kBkt * 4 + (size_t)kCand * 8;
 
 __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __restrict__ y, int N, int T, float thresh,
@@ -297,14 +297,23 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
     // pass 1: bucket histogram
     if (vec) {
         const float4* y4 = reinterpret_cast<const float4*>(ys);
-        for (int q = tid; q < (N >> 2); q += kHT) {
-            const float4 v = __ldg(y4 + q);
-            const unsigned int u0 = thr_bits(v.x, thresh), u1 = thr_bits(v.y, thresh), u2 = thr_bits(v.z, thresh),
-                               u3 = thr_bits(v.w, thresh);
-            if (u0) atomicAdd(&tab[u0 >> 16], 1u);
-            if (u1) atomicAdd(&tab[u1 >> 16], 1u);
-            if (u2) atomicAdd(&tab[u2 >> 16], 1u);
-            if (u3) atomicAdd(&tab[u3 >> 16], 1u);
+        const int n4 = N >> 2;
+        for (int q0 = tid; q0 < n4; q0 += kUnroll * kHT) {  // kUnroll 16-byte loads in flight per thread
+            float4 v[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int q = q0 + u * kHT;
+                v[u] = q < n4 ? __ldg(y4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const unsigned int u0 = thr_bits(v[u].x, thresh), u1 = thr_bits(v[u].y, thresh),
+                                   u2 = thr_bits(v[u].z, thresh), u3 = thr_bits(v[u].w, thresh);
+                if (u0) atomicAdd(&tab[u0 >> 16], 1u);
+                if (u1) atomicAdd(&tab[u1 >> 16], 1u);
+                if (u2) atomicAdd(&tab[u2 >> 16], 1u);
+                if (u3) atomicAdd(&tab[u3 >> 16], 1u);
+            }
         }
     } else {
         for (int i = tid; i < N; i += kHT) {
@@ -376,14 +385,26 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
     if (vec) {
         const float4* y4 = reinterpret_cast<const float4*>(ys);
         uchar4* o4 = reinterpret_cast<uchar4*>(out);
-        for (int q = tid; q < (N >> 2); q += kHT) {
-            const float4 v = __ldg(y4 + q);
-            uchar4 r;
-            r.x = (uint8_t)one(thr_bits(v.x, thresh), 4 * q);
-            r.y = (uint8_t)one(thr_bits(v.y, thresh), 4 * q + 1);
-            r.z = (uint8_t)one(thr_bits(v.z, thresh), 4 * q + 2);
-            r.w = (uint8_t)one(thr_bits(v.w, thresh), 4 * q + 3);
-            o4[q] = r;
+        const int n4 = N >> 2;
+        for (int q0 = tid; q0 < n4; q0 += kUnroll * kHT) {
+            float4 v[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int q = q0 + u * kHT;
+                v[u] = q < n4 ? __ldg(y4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int q = q0 + u * kHT;
+                if (q < n4) {
+                    uchar4 r;
+                    r.x = (uint8_t)one(thr_bits(v[u].x, thresh), 4 * q);
+                    r.y = (uint8_t)one(thr_bits(v[u].y, thresh), 4 * q + 1);
+                    r.z = (uint8_t)one(thr_bits(v[u].z, thresh), 4 * q + 2);
+                    r.w = (uint8_t)one(thr_bits(v[u].w, thresh), 4 * q + 3);
+                    o4[q] = r;
+                }
+            }
         }
     } else {
         for (int i = tid; i < N; i += kHT) out[i] = (uint8_t)one(thr_bits(__ldg(ys + i), thresh), i);

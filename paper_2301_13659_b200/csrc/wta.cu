@@ -62,6 +62,7 @@ struct WtaArgs {
 // KK = per-pixel keep count (>= min(k, C)) for mode 1
 template <int KK>
 __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) {
+    constexpr int kChan = KK >= 4 ? 16 : 8;  // channels read per batch in the per-pixel pre-reduction
     extern __shared__ unsigned long long keys[];  // [kCapKeys]
     __shared__ unsigned long long red[kThreads / 32];
     __shared__ unsigned long long cmin[2];
@@ -114,12 +115,12 @@ __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) 
             for (int j = 0; j < KK; ++j) top[j] = ~0ull;
             if (p < p_hi) {
                 int c = 0;
-                for (; c + 8 <= a.C; c += 8) {
-                    int l[8];
+                for (; c + kChan <= a.C; c += kChan) {  // kChan independent loads in flight
+                    int l[kChan];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) l[u] = __ldg(L + (size_t)(c + u) * HW + p);
+                    for (int u = 0; u < kChan; ++u) l[u] = __ldg(L + (size_t)(c + u) * HW + p);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int u = 0; u < kChan; ++u) {
                         if (l[u] < T) {
                             const int i = (c + u) * HW + p;
                             unsigned long long key = ((unsigned long long)l[u] << 56) |
