@@ -1230,7 +1230,13 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
         return e ? std::atoi(e) : 1;
     }();
     p.retain = (retain_ok && p.nks <= 4 && g.Co > 64) ? 1 : 0;
-    if (p.retain) {
+    static const int nt_force = [] {
+        const char* e = std::getenv("SPK_CONV_NT");  // tuning knob: force the N tile (multiple of 16)
+        return e ? std::atoi(e) : 0;
+    }();
+    if (nt_force >= 16 && nt_force % 16 == 0 && nt_force <= 128) {
+        p.Nt = nt_force;
+    } else if (p.retain) {
         p.Nt = 64;
     } else if (g.Co <= 64) {
         p.Nt = ((g.Co + 15) / 16) * 16;

@@ -38,31 +38,51 @@ void unit_gaussian(double sigma, int r, std::vector<double>& g) {
 // bit-identical.
 constexpr int TX = 32, TY = 8;
 
-template <int R>
+// KC > 0: the kernel count is a compile-time constant (every config: 2, 4 or 6), so each
+// coefficient is an immediate constant-bank operand of its FFMA and the KC independent
+// fmaf chains of a pixel interleave; KC = 0: runtime kernel count.
+template <int R, int KC>
 __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
-                                                       int K, int pad, int Ho, int Wo, float* __restrict__ out,
+                                                       int Kr, int pad, int Ho, int Wo, float* __restrict__ out,
                                                        const FilterCoef coef) {
     constexpr int E = 2 * R + 1, TW = TX + 2 * R, TH = TY + 2 * R;
     __shared__ float tile[TH][TW];
+    __shared__ float lut[256];  // u8 / 255 in fp32 (R-SCALE), one IEEE division per value
+    const int K = KC > 0 ? KC : Kr;
+    const int tid = threadIdx.y * TX + threadIdx.x;
+    lut[tid] = __fdiv_rn((float)tid, 255.0f);  // TX * TY == 256
     const int bc = blockIdx.z;  // b * C + ci
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const uint8_t* plane = img + (size_t)bc * H * W;
+    __syncthreads();
     // stage the input tile: pixel value u8 / 255 (R-SCALE), outside the image -> 0
-    for (int ty = threadIdx.y; ty < TH; ty += TY) {
-        const int iy = y0 - pad + ty;
-        for (int tx = threadIdx.x; tx < TW; tx += TX) {
-            const int ix = x0 - pad + tx;
-            float v = 0.0f;
-            if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = __fdiv_rn((float)__ldg(plane + (size_t)iy * W + ix), 255.0f);
-            tile[ty][tx] = v;
-        }
+    for (int q = tid; q < TH * TW; q += TX * TY) {
+        const int ty = q / TW, tx = q - ty * TW;
+        const int iy = y0 - pad + ty, ix = x0 - pad + tx;
+        float v = 0.0f;
+        if (iy >= 0 && iy < H && ix >= 0 && ix < W) v = lut[__ldg(plane + (size_t)iy * W + ix)];
+        tile[ty][tx] = v;
     }
     __syncthreads();
     const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     if (x >= Wo || y >= Ho) return;
     const int b = bc / C, ci = bc - b * C;
     float* o = out + (((size_t)b * C + ci) * K * Ho + y) * Wo + x;
-    if constexpr (E * E <= 81) {  // window in registers, reused by all K kernels
+    if constexpr (KC > 0) {
+        float acc[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) acc[k] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const float v = tile[threadIdx.y + i][threadIdx.x + j];
+#pragma unroll
+                for (int k = 0; k < KC; ++k) acc[k] = __fmaf_rn(coef.c[k * E * E + i * E + j], v, acc[k]);
+            }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) o[(size_t)k * Ho * Wo] = acc[k];
+    } else if constexpr (E * E <= 81) {  // window in registers, reused by all K kernels
         float v[E * E];
 #pragma unroll
         for (int i = 0; i < E; ++i)
@@ -87,6 +107,66 @@ __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restric
     }
 }
 
+// Compile-time kernel count (every config's front end: R = 3, K = 2, 4 or 6): a CTA
+// covers 32 x 32 outputs, each thread RY = 4 vertically adjacent pixels.  Every input
+// row of the thread's (RY + 2R) x E window is read from shared memory once and feeds
+// the RY outputs it overlaps; per output the taps still run i = 0..E-1, j = 0..E-1
+// (R-FILTER-ORDER), so the K fmaf chains are the oracle's, bit for bit.
+constexpr int RY = 4;
+
+template <int R, int KC>
+__global__ void __launch_bounds__(TX* TY) filter_rb_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
+                                                          int pad, int Ho, int Wo, float* __restrict__ out,
+                                                          const FilterCoef coef) {
+    constexpr int E = 2 * R + 1, OY = TY * RY, TW = TX + 2 * R, TH = OY + 2 * R;
+    __shared__ float tile[TH][TW];
+    __shared__ float lut[256];  // u8 / 255 in fp32 (R-SCALE)
+    const int tid = threadIdx.y * TX + threadIdx.x;
+    lut[tid] = __fdiv_rn((float)tid, 255.0f);
+    const int bc = blockIdx.z;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * OY;
+    const uint8_t* plane = img + (size_t)bc * H * W;
+    __syncthreads();
+    for (int ty = threadIdx.y; ty < TH; ty += TY) {
+        const int iy = y0 - pad + ty;
+        const bool rowin = iy >= 0 && iy < H;
+        for (int tx = threadIdx.x; tx < TW; tx += TX) {
+            const int ix = x0 - pad + tx;
+            tile[ty][tx] = (rowin && ix >= 0 && ix < W) ? lut[__ldg(plane + (size_t)iy * W + ix)] : 0.0f;
+        }
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x, yb = y0 + threadIdx.y * RY;
+    if (x >= Wo || yb >= Ho) return;
+    float acc[RY][KC];
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int k = 0; k < KC; ++k) acc[r][k] = 0.0f;
+#pragma unroll
+    for (int iy = 0; iy < RY + 2 * R; ++iy) {
+        float v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = tile[threadIdx.y * RY + iy][threadIdx.x + j];
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+            const int i = iy - r;  // kernel row of this input row for output row r
+            if (i < 0 || i >= E) continue;
+#pragma unroll
+            for (int j = 0; j < E; ++j)
+#pragma unroll
+                for (int k = 0; k < KC; ++k) acc[r][k] = __fmaf_rn(coef.c[k * E * E + i * E + j], v[j], acc[r][k]);
+        }
+    }
+    const int b = bc / C, ci = bc - b * C;
+    float* o = out + (((size_t)b * C + ci) * KC * Ho + yb) * Wo + x;
+#pragma unroll
+    for (int r = 0; r < RY; ++r)
+        if (yb + r < Ho)
+#pragma unroll
+            for (int k = 0; k < KC; ++k) o[(size_t)k * Ho * Wo + (size_t)r * Wo] = acc[r][k];
+}
+
 spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std::vector<float>& coef,
                       int K, int radius, int pad, float* y, spk_stream stream) {
     const int e = 2 * radius + 1;
@@ -99,15 +179,34 @@ spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std:
     SPK_CHECK(grid.z <= 65535u, SPK_ERR_SHAPE, "B*C=%d > 65535", B * C);
     cudaStream_t s = spk::as_cuda(stream);
     const dim3 blk(TX, TY);
+    if (radius == 3 && (K == 1 || K == 2 || K == 4 || K == 6) && Ho * Wo < 64 * 64) {  // small maps (C1-C3)
+        switch (K) {
+            case 1: filter_kernel<3, 1><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 2: filter_kernel<3, 2><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 4: filter_kernel<3, 4><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            default: filter_kernel<3, 6><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        }
+        return spk::launched("filter_kernel");
+    }
+    if (radius == 3 && (K == 1 || K == 2 || K == 4 || K == 6)) {  // large maps (C4, C5)
+        const dim3 g4(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY * RY), (unsigned)(B * C));
+        switch (K) {
+            case 1: filter_rb_kernel<3, 1><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 2: filter_rb_kernel<3, 2><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 4: filter_rb_kernel<3, 4><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            default: filter_rb_kernel<3, 6><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+        }
+        return spk::launched("filter_rb_kernel");
+    }
     switch (radius) {
-        case 0: filter_kernel<0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 1: filter_kernel<1><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 2: filter_kernel<2><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 3: filter_kernel<3><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 4: filter_kernel<4><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 5: filter_kernel<5><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 6: filter_kernel<6><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        default: filter_kernel<7><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 0: filter_kernel<0, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 1: filter_kernel<1, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 2: filter_kernel<2, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 3: filter_kernel<3, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 4: filter_kernel<4, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 5: filter_kernel<5, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 6: filter_kernel<6, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        default: filter_kernel<7, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
     }
     return spk::launched("filter_kernel");
 }

@@ -273,6 +273,23 @@ __global__ void gather_kernel(const uint8_t* __restrict__ lat, size_t n, int T, 
     f[q] = __fdiv_rn((float)(T - l), (float)T);
 }
 
+// 16 latencies per thread (one 16-byte load, four 16-byte stores); the T+1 possible
+// features come from a shared table of the same IEEE divisions (R-GATHER)
+__global__ void __launch_bounds__(kT) gather16_kernel(const uint4* __restrict__ lat, size_t n16, int T,
+                                                      float4* __restrict__ f) {
+    __shared__ float tab[256];
+    tab[threadIdx.x] = __fdiv_rn((float)(T - min((int)threadIdx.x, T)), (float)T);
+    __syncthreads();
+    for (size_t q = (size_t)blockIdx.x * kT + threadIdx.x; q < n16; q += (size_t)gridDim.x * kT) {
+        const uint4 v = __ldg(lat + q);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            f[4 * q + j] = make_float4(tab[w[j] & 0xffu], tab[(w[j] >> 8) & 0xffu], tab[(w[j] >> 16) & 0xffu],
+                                       tab[w[j] >> 24]);
+    }
+}
+
 // ---------------------------------------------------------------- boundary conversions
 __global__ void lat_to_dense_kernel(const uint8_t* __restrict__ lat, int B, int T, size_t N,
                                     uint8_t* __restrict__ dense) {
@@ -410,6 +427,13 @@ extern "C" spk_status spk_gather(const uint8_t* lat, size_t n, int T, float* fea
     SPK_CHECK_PTR(feat);
     SPK_CHECK(T >= 1 && T <= 254, SPK_ERR_UNSUPPORTED, "T=%d outside 1..254", T);
     if (n == 0) return SPK_OK;
+    if (n % 16 == 0 && ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(feat)) & 15) == 0) {
+        const size_t n16 = n / 16;
+        const unsigned blocks = (unsigned)std::min<size_t>(spk::ceil_div(n16, kT), 148 * 16);
+        gather16_kernel<<<blocks, kT, 0, spk::as_cuda(stream)>>>(reinterpret_cast<const uint4*>(lat), n16, T,
+                                                                 reinterpret_cast<float4*>(feat));
+        return spk::launched("gather16_kernel");
+    }
     gather_kernel<<<spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream)>>>(lat, n, T, feat);
     return spk::launched("gather_kernel");
 }

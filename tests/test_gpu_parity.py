@@ -26,7 +26,7 @@ def host(t):
 
 
 # ------------------------------------------------------------------------- a1 filters
-@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
 def test_filter_bit_identical(spk, name):
     cfg = synth.load_config(name)
     imgs = synth.images(cfg, 0, 3)
@@ -342,6 +342,15 @@ def test_gather_and_conversions(spk):
         S2[1, 6, 2, 3, 4] = 1
     _, bad = spk.dense_to_lat(cu(S2))
     assert int(host(bad)[0]) == 1 * 120 + 2 * 30 + 3 * 6 + 4
+
+
+@pytest.mark.parametrize("T", [1, 15, 30, 254])
+def test_gather_vectorised(spk, T):
+    """16-byte path (n % 16 == 0, aligned): every latency 0..T and out-of-range values."""
+    lat = RNG.integers(0, 256, (5, 8, 28, 28)).astype(np.uint8)
+    lat[0, 0, 0, :T + 1] = np.arange(T + 1) if T < 28 else lat[0, 0, 0, :T + 1]
+    ref = oracle.gather(oracle.lat_to_dense(np.minimum(lat, T), T))
+    np.testing.assert_array_equal(host(spk.gather(cu(lat), T)), ref)
 
 
 # ------------------------------------------------------------------ pipelines end to end
