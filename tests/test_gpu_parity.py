@@ -470,6 +470,104 @@ def test_c2_full_batch_sampled(spk):
     np.testing.assert_array_equal(host(net.weights[2]), W)
 
 
+def _check_rows_train(cfg, net, imgs, rows, Ws):
+    """Rows of a full-batch GPU training step against the oracle, stage by stage and
+    teacher-forced (every layer is per sample): the front end must be bit-exact; each
+    layer's output must equal the oracle applied to the GPU's own input of that layer
+    outside the near-threshold set; the trained layer's inhibited record and winners must
+    equal the oracle's threshold -> inhibit -> convwta on the GPU's input (samples with an
+    explained near-threshold mismatch in that layer are counted, not compared)."""
+    T, tl = cfg["T"], cfg["train_layer"]
+    lat0, gw, gn = host(net.lat0), host(net.win), host(net.nwin)
+    excluded = 0
+    for b in rows:
+        _, rl0 = opipe.front_end(cfg, imgs[b:b + 1])
+        np.testing.assert_array_equal(lat0[b:b + 1], rl0)
+        for li in range(tl):
+            L = cfg["layers"][li]
+            P = oracle.conv_event(host(net.input_of(li)[b:b + 1]), T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
+            rlat, _ = lat_and_pstar(P, L["theta"])
+            rec = dict(net.layers[li])
+            for key in ("lat", "pooled"):
+                if rec.get(key) is not None:
+                    rec[key] = rec[key][b:b + 1]
+            _layer_out_diff(rec, L, rlat, near_threshold(P, L["theta"]), np.zeros(1, bool), T)
+        L = cfg["layers"][tl]
+        P = oracle.conv_event(host(net.input_of(tl)[b:b + 1]), T, Ws[tl], (L["stride"],) * 2, (L["pad"],) * 2)
+        Qi = oracle.inhibit(oracle.threshold(P, L["theta"]))
+        win, nwin = oracle.wta(Qi, L["wta"]["count"], L["wta"]["radius"])
+        rlat, _ = lat_and_pstar(Qi, 0.0)
+        diff = host(net.layers[tl]["lat"][b:b + 1]) != rlat
+        assert not (diff & ~near_threshold(P, L["theta"])).any(), "trained layer: unexplained mismatches"
+        del P, Qi
+        if diff.any():
+            excluded += 1
+            continue
+        assert gn[b] == nwin[0]
+        got = gw[b, :gn[b]].copy()
+        got[:, 0] = 0
+        np.testing.assert_array_equal(got, win[0, :gn[b]])
+    return excluded
+
+
+def test_c4_full_batch_sampled(spk):
+    """BASELINE configs[3] (C4) at full size — batch 256, T = 30 — launched as bench.py does
+    (auto engines, CUDA graph replay); sampled images checked against the oracle one by one."""
+    from paper_2301_13659_b200.network import Network
+
+    cfg = synth.load_config("c4")
+    B = cfg["batch"]
+    imgs = synth.images_parallel(cfg, 0, B)
+    Ws = synth.layer_weights(cfg)
+    net = Network(cfg, B, prec="auto")
+    net.img.copy_(cu(imgs))
+    net.set_weights([cu(w) for w in Ws])
+    net.capture(warmup=1)
+    net.set_weights([cu(w) for w in Ws])  # the capture warm-up ran one training step
+    net.replay()
+    torch.cuda.synchronize()
+    assert _check_rows_train(cfg, net, imgs, [0, 137, B - 1], Ws) <= 1
+
+
+@pytest.mark.slow
+def test_c5_full_batch_sampled(spk):
+    """BASELINE configs[4] (C5) at full size — batch 4096 forward, as bench.py runs it at N = 1 —
+    with the first and last image checked against the oracle (features bit-exact outside the
+    near-threshold set)."""
+    from paper_2301_13659_b200.network import Network
+
+    cfg = synth.load_config("c5")
+    B, T = cfg["batch"], cfg["T"]
+    Ws = synth.layer_weights(cfg)
+    net = Network(cfg, B, prec="auto")
+    net.img.copy_(cu(synth.images_parallel(cfg, 0, B)))
+    net.set_weights([cu(w) for w in Ws])
+    net.capture(warmup=1)
+    net.replay()
+    torch.cuda.synchronize()
+    for b in [0, B - 1]:
+        img = synth.images(cfg, b, 1)
+        _, lat = opipe.front_end(cfg, img)
+        np.testing.assert_array_equal(host(net.lat0[b:b + 1]), lat)
+        excluded = np.zeros(1, bool)
+        for li, L in enumerate(cfg["layers"]):
+            P = oracle.conv_event(lat, T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
+            rlat, _ = lat_and_pstar(P, L["theta"])
+            excl = near_threshold(P, L["theta"])
+            del P
+            rec = dict(net.layers[li])
+            for key in ("lat", "pooled"):
+                if rec.get(key) is not None:
+                    rec[key] = rec[key][b:b + 1]
+            excluded |= _layer_out_diff(rec, L, rlat, excl, excluded, T)
+            p = L["pool"]
+            lat = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(rlat, T), (p["kernel"],) * 2,
+                                                  (p["stride"],) * 2, (p["pad"],) * 2))
+        if not excluded[0]:
+            feats = oracle.gather(oracle.lat_to_dense(lat, T))
+            np.testing.assert_array_equal(host(net.features[b:b + 1]), feats)
+
+
 def test_pipeline_c4_train_t30(spk):
     """Caltech-shaped C4 (Gabor front end, T = 30 -> 32-row time tiles), layer-2 training step, 1 image."""
     assert _check_pipeline(synth.load_config("c4"), 1) <= 1
