@@ -11,6 +11,8 @@
 // memory), after which  lat = #{t : key <= K_t}.  Deterministic, exact, one
 // read of the sample per radix pass (values staged in shared memory when they
 // fit).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -272,14 +274,24 @@ __global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const floa
 //          bucket).  Exactly the ranks of the full sort.
 // More boundary-bucket values than fit shared memory (massive exact ties) -> the
 // sample falls back to the multi-target radix select above (exact, slower).
-constexpr int kBkt = 32768, kCand = 8192, kHT = 1024, kMaxBnd = 256, kUnroll = 4;
-constexpr size_t kHistSmem = (size_t)kBkt * 4 + (size_t)kCand * 8;
+constexpr int kMaxBnd = 256, kUnroll = 4;
+// Two instantiations: C4/C5 samples (32768 buckets = exponent + 7 mantissa bits, 1024
+// threads, values read twice from global memory) and C1-C3 samples (<= 8192 values:
+// 4096 buckets = exponent + 4 mantissa bits, 256 threads, values staged in smem).
+template <int SHIFT, int kHT, int kCand, bool STAGE>
+struct HistCfg {
+    static constexpr int kBkt = 1 << (31 - SHIFT);
+    static size_t smem(int N) { return (size_t)kBkt * 4 + (size_t)kCand * 8 + (STAGE ? (size_t)N * 4 : 0); }
+};
 
+template <int SHIFT, int kHT, int kCand, bool STAGE>
 __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __restrict__ y, int N, int T, float thresh,
                                                             uint8_t* __restrict__ lat) {
+    constexpr int kBkt = HistCfg<SHIFT, kHT, kCand, STAGE>::kBkt, kNW = kHT / 32;
     extern __shared__ __align__(16) unsigned char dyn[];
     unsigned int* tab = reinterpret_cast<unsigned int*>(dyn);                         // [kBkt]
     unsigned long long* cand = reinterpret_cast<unsigned long long*>(dyn + (size_t)kBkt * 4);  // [kCand]
+    unsigned int* vals = reinterpret_cast<unsigned int*>(dyn + (size_t)kBkt * 4 + (size_t)kCand * 8);  // STAGE: [N]
     __shared__ unsigned int red[32];
     __shared__ unsigned int bnd_b[kMaxBnd], bnd_c[kMaxBnd];
     __shared__ unsigned int s_nbnd, s_ncand, s_n;
@@ -307,22 +319,25 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
+                if (q0 + u * kHT >= n4) break;
                 const unsigned int u0 = thr_bits(v[u].x, thresh), u1 = thr_bits(v[u].y, thresh),
                                    u2 = thr_bits(v[u].z, thresh), u3 = thr_bits(v[u].w, thresh);
-                if (u0) atomicAdd(&tab[u0 >> 16], 1u);
-                if (u1) atomicAdd(&tab[u1 >> 16], 1u);
-                if (u2) atomicAdd(&tab[u2 >> 16], 1u);
-                if (u3) atomicAdd(&tab[u3 >> 16], 1u);
+                if (STAGE) reinterpret_cast<uint4*>(vals)[q0 + u * kHT] = make_uint4(u0, u1, u2, u3);
+                if (u0) atomicAdd(&tab[u0 >> SHIFT], 1u);
+                if (u1) atomicAdd(&tab[u1 >> SHIFT], 1u);
+                if (u2) atomicAdd(&tab[u2 >> SHIFT], 1u);
+                if (u3) atomicAdd(&tab[u3 >> SHIFT], 1u);
             }
         }
     } else {
         for (int i = tid; i < N; i += kHT) {
             const unsigned int u = thr_bits(__ldg(ys + i), thresh);
-            if (u) atomicAdd(&tab[u >> 16], 1u);
+            if (STAGE) vals[i] = u;
+            if (u) atomicAdd(&tab[u >> SHIFT], 1u);
         }
     }
     __syncthreads();
-    // scan from the top bucket down: thread tid owns buckets [32 tid, 32 tid + 32)
+    // scan from the top bucket down: thread tid owns buckets [kPer tid, kPer tid + kPer)
     constexpr int kPer = kBkt / kHT;
     unsigned int loc = 0;
 #pragma unroll 8
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
     if (lane == 0) red[wid] = incl;  // warp total
     __syncthreads();
     if (wid == 0) {
-        const unsigned int wt = red[lane];
+        const unsigned int wt = lane < kNW ? red[lane] : 0u;
         unsigned int ws = wt;  // inclusive suffix over warps
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned int v = __shfl_down_sync(0xffffffffu, ws, o);
@@ -376,13 +391,23 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
     // pass 2: ordinary buckets are final; boundary-bucket values become candidates
     auto one = [&](unsigned int u, int i) -> unsigned int {
         if (!u) return (unsigned int)T;
-        const unsigned int tag = tab[u >> 16] >> 24;
+        const unsigned int tag = tab[u >> SHIFT] >> 24;
         if (tag != 255u) return tag;
         const unsigned int pos = atomicAdd(&s_ncand, 1u);
         if (pos < (unsigned)kCand) cand[pos] = ((unsigned long long)u << 32) | (0xffffffffu - (unsigned)i);
         return 0u;  // placeholder, rewritten below
     };
-    if (vec) {
+    if (STAGE && vec) {
+        const uint4* v4 = reinterpret_cast<const uint4*>(vals);
+        uchar4* o4 = reinterpret_cast<uchar4*>(out);
+        for (int q = tid; q < (N >> 2); q += kHT) {
+            const uint4 w = v4[q];
+            o4[q] = make_uchar4((uint8_t)one(w.x, 4 * q), (uint8_t)one(w.y, 4 * q + 1), (uint8_t)one(w.z, 4 * q + 2),
+                                (uint8_t)one(w.w, 4 * q + 3));
+        }
+    } else if (STAGE) {
+        for (int i = tid; i < N; i += kHT) out[i] = (uint8_t)one(vals[i], i);
+    } else if (vec) {
         const float4* y4 = reinterpret_cast<const float4*>(ys);
         uchar4* o4 = reinterpret_cast<uchar4*>(out);
         const int n4 = N >> 2;
@@ -437,7 +462,7 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
     const int nb = (int)s_nbnd;
     for (int j = tid; j < nc; j += kHT) {
         const unsigned long long key = cand[j];
-        const unsigned int u = (unsigned int)(key >> 32), B = u >> 16;
+        const unsigned int u = (unsigned int)(key >> 32), B = u >> SHIFT;
         const unsigned int idx = 0xffffffffu - (unsigned int)(key & 0xffffffffull);
         unsigned int sB = 0;  // candidates in higher boundary buckets
         for (int q = 0; q < nb; ++q)
@@ -464,6 +489,21 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
     SPK_CHECK(T <= 254, SPK_ERR_UNSUPPORTED, "T=%d > 254 (u8 latency)", T);
     SPK_CHECK(B <= 0x7fffffff, SPK_ERR_SHAPE, "B too large");
     cudaStream_t s = spk::as_cuda(stream);
+    static const int old_sort = [] {
+        const char* e = std::getenv("SPK_RANK_SORT");  // A/B knob: 1 = bitonic sort kernel for small samples
+        return e ? std::atoi(e) : 0;
+    }();
+    if (sort && N <= kSortMax && !old_sort) {  // small samples: staged values, 4096-bucket histogram
+        using Cfg = HistCfg<19, 256, 1024, true>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(rank_code_hist_kernel<19, 256, 1024, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(kSortMax));
+            attr = true;
+        }
+        rank_code_hist_kernel<19, 256, 1024, true><<<B, 256, Cfg::smem(N), s>>>(y, N, T, thresh, lat);
+        return spk::launched("rank_code_hist_kernel<small>");
+    }
     if (sort && N <= kSortMax) {
         int cap = 1;
         while (cap < N) cap <<= 1;
@@ -478,12 +518,14 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         return spk::launched("rank_code_sort_kernel");
     }
     if (sort) {  // larger samples: bucket histogram + boundary-bucket sort
+        using Cfg = HistCfg<16, 1024, 8192, false>;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(rank_code_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHistSmem);
+            cudaFuncSetAttribute(rank_code_hist_kernel<16, 1024, 8192, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(0));
             attr = true;
         }
-        rank_code_hist_kernel<<<B, kHT, kHistSmem, s>>>(y, N, T, thresh, lat);
+        rank_code_hist_kernel<16, 1024, 8192, false><<<B, 1024, Cfg::smem(0), s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel");
     }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
