@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const int32
 // byte; phase 2 — one thread per weight — runs the sequential fp32 chain of
 // Eq. 4-6 from shared memory only.  The gathers are thus fully parallel and the
 // order-dependent part is a few dependent flops per winner.
-constexpr int kUpdW = 64, kUpdThreads = 256, kWinChunk = 256;
+constexpr int kUpdW = 32, kUpdThreads = 256, kWinChunk = 256;  // tuned on C2 layer 3 (scripts/ab_stdp.sh)
 
 __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restrict__ w, spk_conv_geom g,
                                                                   const uint8_t* __restrict__ lat_in,
