@@ -72,10 +72,11 @@ extern "C" int spk_conv_fire_pool_supported(const spk_conv_geom* g, spk_precisio
     if (!g || !pool || prec != SPK_PREC_EVENT) return 0;
     EvPlan e;
     if (!ev_plan(*g, e)) return 0;
-    return e.stage && e.pch == e.Ho * e.Wo && pool->Lh >= 1 && pool->Lw >= 1 && pool->Sh >= 1 && pool->Sw >= 1 &&
-                   pool->Ph >= 0 && pool->Pw >= 0 && e.Ho + 2 * pool->Ph >= pool->Lh && e.Wo + 2 * pool->Pw >= pool->Lw
-               ? 1
-               : 0;
+    const bool geom_ok = pool->Lh >= 1 && pool->Lw >= 1 && pool->Sh >= 1 && pool->Sw >= 1 && pool->Ph >= 0 &&
+                         pool->Pw >= 0 && e.Ho + 2 * pool->Ph >= pool->Lh && e.Wo + 2 * pool->Pw >= pool->Lw;
+    // a whole sample per CTA, or chunks of whole output rows that no pooling window straddles
+    const bool chunk_ok = e.stage || (pool->Ph == 0 && pool->Lh == pool->Sh && e.rpc % pool->Sh == 0);
+    return geom_ok && chunk_ok ? 1 : 0;
 }
 
 extern "C" spk_status spk_conv_fire_pool(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
@@ -92,7 +93,7 @@ extern "C" spk_status spk_conv_fire_pool(const uint8_t* lat_in, const float* w, 
     SPK_CHECK(std::isfinite(theta) && theta >= 0.0f, SPK_ERR_ARG, "theta must be finite and >= 0");
     SPK_CHECK(std::isfinite(w_max) && w_max > 0.0f, SPK_ERR_ARG, "w_max must be finite and > 0");
     SPK_CHECK(spk_conv_fire_pool_supported(g, prec, pool), SPK_ERR_UNSUPPORTED,
-              "fused fire+pool needs prec=EVENT with a whole sample per CTA and a valid pool geometry (Eq. 3)");
+              "fused fire+pool needs prec=EVENT, a valid pool geometry (Eq. 3) and CTA row chunks no window straddles");
     EvPlan e;
     ev_plan(*g, e);
     SPK_CHECK(ws != nullptr && ws_bytes >= e.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,

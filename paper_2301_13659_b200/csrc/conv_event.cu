@@ -282,20 +282,24 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     }
     if (EPI == SPK_EPI_POTENTIAL) return;
     __syncthreads();
-    if (a.pool) {  // whole sample staged: window minimum of latencies (Eq. 3), padding never fires
-        const int HWp = a.Hp * a.Wp;
+    if (a.pool) {  // window minimum of latencies (Eq. 3), padding never fires; this CTA's output
+                   // rows [ya, ya + rows) hold whole windows (whole sample, or Ph = 0, Lh = Sh | rpc)
+        const int rows = npix / a.Wo;
+        const int py0 = a.rpc >= a.Ho ? 0 : ya / a.pg.Sh;
+        const int py1 = a.rpc >= a.Ho ? a.Hp : min(a.Hp, (ya + rows) / a.pg.Sh);
+        const int nq = (py1 - py0) * a.Wp;
         for (int r = warp; r < kMB; r += kEvWarps) {
             const int om = m0 + r;
             if (om >= g.Co) continue;
-            uint8_t* dl = static_cast<uint8_t*>(a.out0) + ((size_t)b * g.Co + om) * HWp;
+            uint8_t* dl = static_cast<uint8_t*>(a.out0) + ((size_t)b * g.Co + om) * a.Hp * a.Wp + py0 * a.Wp;
             const uint8_t* ml = olat + r * a.pch;
-            for (int q = lane; q < HWp; q += 32) {
-                const int py = q / a.Wp, px = q - py * a.Wp;
+            for (int q = lane; q < nq; q += 32) {
+                const int py = py0 + q / a.Wp, px = q % a.Wp;
                 const int y0 = py * a.pg.Sh - a.pg.Ph, x0 = px * a.pg.Sw - a.pg.Pw;
                 int m = T;
                 for (int i = max(0, -y0); i < a.pg.Lh && y0 + i < a.Ho; ++i)
                     for (int j = max(0, -x0); j < a.pg.Lw && x0 + j < a.Wo; ++j)
-                        m = min(m, (int)ml[(y0 + i) * a.Wo + x0 + j]);
+                        m = min(m, (int)ml[(y0 + i - ya) * a.Wo + x0 + j]);
                 dl[q] = (uint8_t)m;
             }
         }

@@ -617,8 +617,11 @@ def test_forward_c2_all_layers(spk, prec):
     assert _check_forward(synth.load_config("c2"), 6, prec) <= 1
 
 
+# whole samples per CTA (overlapping and padded windows), and row chunks of a large map
+# (fused when no window straddles a chunk)
 @pytest.mark.parametrize("case", [(3, 15, 6, 28, 28, 30, 5, 1, 2, 2, 2, 0), (2, 15, 6, 28, 28, 30, 5, 1, 2, 3, 2, 1),
-                                  (2, 30, 4, 20, 23, 40, 5, 1, 2, 2, 2, 0), (2, 7, 3, 9, 11, 20, 3, 2, 0, 3, 3, 0)])
+                                  (2, 30, 4, 20, 23, 40, 5, 1, 2, 2, 2, 0), (2, 7, 3, 9, 11, 20, 3, 2, 0, 3, 3, 0),
+                                  (5, 15, 6, 27, 27, 30, 5, 1, 2, 2, 2, 0), (2, 30, 4, 160, 250, 64, 5, 1, 2, 2, 2, 0)])
 def test_conv_fire_pool_fused(spk, case):
     """spk_conv_fire_pool == spk_pool(spk_conv(FIRE)) bit for bit (EVENT engine)."""
     B, T, Ci, Hi, Wi, Co, K, s, p, L, ps, pp = case
@@ -626,7 +629,7 @@ def test_conv_fire_pool_fused(spk, case):
     g = spk.conv_geom(cu(lat), cu(w), T, s, p)
     if not spk.conv_fire_pool_supported(g, "event", L, ps, pp):
         pytest.skip("fused fire+pool not supported for this geometry")
-    P = oracle.conv_event(lat, T, w, (s, s), (p, p))
+    P = oracle.conv_event(lat[:2], T, w, (s, s), (p, p))
     theta = float(np.percentile(P[:, -1], 60)) + 0.123
     flat, _ = spk.conv(cu(lat), cu(w), T, s, p, prec="event", epi="fire", theta=theta)
     ref = spk.pool(flat, T, L, ps, pp)
