@@ -287,20 +287,50 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
         const int rows = npix / a.Wo;
         const int py0 = a.rpc >= a.Ho ? 0 : ya / a.pg.Sh;
         const int py1 = a.rpc >= a.Ho ? a.Hp : min(a.Hp, (ya + rows) / a.pg.Sh);
-        const int nq = (py1 - py0) * a.Wp;
-        for (int r = warp; r < kMB; r += kEvWarps) {
+        const bool p2 = a.pg.Lh == 2 && a.pg.Lw == 2 && a.pg.Sh == 2 && a.pg.Sw == 2 && a.pg.Ph == 0 && a.pg.Pw == 0 &&
+                        (a.Wo & 1) == 0 && (a.pch & 1) == 0;
+        if (p2 && a.Wp < 32) {  // short rows (C2): lanes over the map's pooled outputs
+            const int nq = (py1 - py0) * a.Wp;
+            for (int r = warp; r < kMB; r += kEvWarps) {
+                const int om = m0 + r;
+                if (om >= g.Co) continue;
+                uint8_t* dl = static_cast<uint8_t*>(a.out0) + (((size_t)b * g.Co + om) * a.Hp + py0) * a.Wp;
+                const uint8_t* ml = olat + r * a.pch;
+                for (int q = lane; q < nq; q += 32) {
+                    const int pr = q / a.Wp, px = q - pr * a.Wp;
+                    const uint8_t* r0 = ml + (2 * (py0 + pr) - ya) * a.Wo + 2 * px;
+                    const uint32_t m = __vminu4(*reinterpret_cast<const uint16_t*>(r0),
+                                                *reinterpret_cast<const uint16_t*>(r0 + a.Wo));
+                    dl[q] = (uint8_t)min(m & 0xffu, m >> 8);
+                }
+            }
+            return;
+        }
+        // one (map, pooled row) per warp iteration: lanes run along the row (no divisions)
+        for (int item = warp; item < kMB * (py1 - py0); item += kEvWarps) {
+            const int r = item / (py1 - py0), py = py0 + item % (py1 - py0);
             const int om = m0 + r;
             if (om >= g.Co) continue;
-            uint8_t* dl = static_cast<uint8_t*>(a.out0) + ((size_t)b * g.Co + om) * a.Hp * a.Wp + py0 * a.Wp;
+            uint8_t* dl = static_cast<uint8_t*>(a.out0) + (((size_t)b * g.Co + om) * a.Hp + py) * a.Wp;
             const uint8_t* ml = olat + r * a.pch;
-            for (int q = lane; q < nq; q += 32) {
-                const int py = py0 + q / a.Wp, px = q % a.Wp;
-                const int y0 = py * a.pg.Sh - a.pg.Ph, x0 = px * a.pg.Sw - a.pg.Pw;
+            const int y0 = py * a.pg.Sh - a.pg.Ph;
+            if (p2) {  // 2x2/2: two 2-byte reads, byte-SIMD minimum
+                const uint8_t* r0 = ml + (y0 - ya) * a.Wo;
+                for (int px = lane; px < a.Wp; px += 32) {
+                    const uint32_t m = __vminu4(*reinterpret_cast<const uint16_t*>(r0 + 2 * px),
+                                                *reinterpret_cast<const uint16_t*>(r0 + a.Wo + 2 * px));
+                    dl[px] = (uint8_t)min(m & 0xffu, m >> 8);
+                }
+                continue;
+            }
+            const int i0 = max(0, -y0), i1 = min(a.pg.Lh, a.Ho - y0);
+            for (int px = lane; px < a.Wp; px += 32) {
+                const int x0 = px * a.pg.Sw - a.pg.Pw;
                 int m = T;
-                for (int i = max(0, -y0); i < a.pg.Lh && y0 + i < a.Ho; ++i)
+                for (int i = i0; i < i1; ++i)
                     for (int j = max(0, -x0); j < a.pg.Lw && x0 + j < a.Wo; ++j)
                         m = min(m, (int)ml[(y0 + i - ya) * a.Wo + x0 + j]);
-                dl[q] = (uint8_t)m;
+                dl[px] = (uint8_t)m;
             }
         }
         return;
