@@ -530,6 +530,12 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
     }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
         const size_t smem = sizeof(unsigned int) * (size_t)N;
+        static bool attr = false;  // up to 32 KB of staged values next to the static RankSmem
+        if (!attr) {
+            cudaFuncSetAttribute(rank_code_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(unsigned int) * 8192));
+            attr = true;
+        }
         rank_code_kernel<true, 256><<<B, 256, smem, s>>>(y, N, T, thresh, sort, lat);
         return spk::launched("rank_code_kernel<staged,256>");
     }

@@ -92,6 +92,18 @@ def test_rank_code_large_sample_histogram_path(spk, T):
     np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, True)), oracle.rank_code(y, T, 0.01, True))
 
 
+@pytest.mark.parametrize("N", [1, 3, 4705, 8192, 8193, 50_001])
+@pytest.mark.parametrize("T", [1, 15, 30])
+def test_rank_code_odd_sizes(spk, N, T):
+    """Sample sizes around every dispatch edge (small staged histogram <= 8192 < large
+    histogram), N % 4 != 0 (scalar paths), a single value, heavy ties."""
+    y = RNG.normal(0, 1, (3, N)).astype(np.float32)
+    y[1] = np.round(y[1], 1)
+    y[2, : N // 2] = 0.25
+    for sort in (True, False):
+        np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, sort)), oracle.rank_code(y, T, 0.01, sort))
+
+
 # ------------------------------------------------------------------------- a3 conv
 CONV_CASES = [
     # B, T, Ci, Hi, Wi, Co, K, stride, pad
@@ -289,6 +301,21 @@ def test_wta_exact_large_samples(spk, C, H, W, k, r, ties):
     np.testing.assert_array_equal(gn, nwin)
     for b in range(2):
         np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
+
+
+@pytest.mark.parametrize("C,H,W,k,r", [(1, 1, 1, 3, 0), (1000, 2, 2, 4, 1), (3, 1, 9000, 6, 2), (64, 3, 5, 64, 0)])
+def test_wta_degenerate_shapes(spk, C, H, W, k, r):
+    """Single neuron, many channels on a tiny map, one long row (8-CTA cluster with thin
+    slices), k larger than the live count."""
+    T = 9
+    Q, lat, ps = _records(2, T, C, H, W, 0.4, True)
+    win, nwin = oracle.wta(Q, k, r)
+    gw, gn = spk.wta(cu(lat), cu(ps.astype(np.float32)), T, k, r)
+    gw, gn = host(gw), host(gn)
+    np.testing.assert_array_equal(gn, nwin)
+    for b in range(2):
+        np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
+        assert (gw[b, nwin[b]:] == -1).all()
 
 
 # ------------------------------------------------------------------------- a8 stdp
