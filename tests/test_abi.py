@@ -75,6 +75,11 @@ def test_host_validation_before_launch():
     assert L.spk_stdp(dummy, ctypes.byref(g), dummy, dummy, dummy, 2, good, 1, dummy, 4, NULL) == 4
     pg = spk.PoolGeom(5, 5, 1, 1, 0, 0)
     assert L.spk_pool(dummy, 1, 1, 3, 3, 15, ctypes.byref(pg), dummy, NULL) == 2
+    assert L.spk_winners_rebase(dummy, dummy, 4, 5, -1, NULL) == 1   # negative base
+    assert L.spk_winners_rebase(NULL, dummy, 4, 5, 0, NULL) == 1
+    assert L.spk_inhibit(dummy, dummy, 1, 2, 3, 3, 300, NULL) == 3    # T > 254
+    assert L.spk_wta(dummy, dummy, 1, 2, 4, 4, 15, 65, 1, dummy, dummy, NULL) == 1  # k > 64
+    assert L.spk_gather(dummy, 10, 0, dummy, NULL) == 3               # T < 1
 
 
 def test_binding_refuses_cpu_tensors():
