@@ -22,10 +22,10 @@ def _nomark(name: str) -> None:
 
 class Network:
     def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "exact"):
-        """prec: "exact" (tcgen05 EXACT_I8 for every conv), "event" (latency-histogram
-        form on CUDA cores where its weight block fits), "auto" (event for small-N
-        layers, Co <= 64, tensor cores otherwise) or "fp32".  exact/event/auto give
-        bit-identical outputs."""
+        """prec: "exact" (tcgen05 EXACT_I8 for every conv), "event" (latency-sorted form
+        on CUDA cores where its weight block fits), "auto" (event for the first layer and
+        for narrow layers, Co <= 64; tensor cores otherwise) or "fp32".  exact/event/auto
+        give bit-identical outputs."""
         self.cfg = cfg
         self.B = batch
         self.T = cfg["T"]
@@ -57,7 +57,10 @@ class Network:
             lp = prec
             if prec in ("auto", "event"):
                 ok = spk.conv_workspace(geom, "event") > 0
-                lp = "event" if ok and (prec == "event" or L["Co"] <= 64) else "exact"
+                # event form where its per-active-synapse cost wins: narrow layers, and the first
+                # layer, whose rank-coded input is sparse (C5 conv0: 11 % of inputs fire,
+                # 304 vs 436 ms on tcgen05; C2 conv1, 46 % dense and 250 maps: 2.0 vs 1.04 ms)
+                lp = "event" if ok and (prec == "event" or L["Co"] <= 64 or li == 0) else "exact"
             rec = dict(
                 L=L, geom=geom, Ho=Ho, Wo=Wo, prec=lp,
                 lat=torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.uint8, device=self.dev),
