@@ -19,7 +19,7 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p);
 
 // Geometry of the event (latency-histogram) path (see conv_event.cu).
 struct EvPlan {
-    int Ho, Wo, K, MB, n_mb, Co_pad, acc64, stage, pch, nw, rpc, Wq;  // stage: whole sample per CTA
+    int Ho, Wo, K, MB, n_mb, Co_pad, acc64, stage, pch, nw, rpc, Wq, mpl;  // stage: whole sample per CTA
     size_t band;
     size_t smem_bytes, ws_bytes;
 };

@@ -21,12 +21,13 @@
 // is written (POTENTIAL).  Weights of the map block live in shared memory, transposed
 // [k][map] so a warp's 32 lanes read one 128-byte row.
 #include <cmath>
+#include <cstdlib>
 
 #include "conv.cuh"
 
 namespace {
 
-constexpr int kMB = 32;  // maps per CTA (one per lane); warps per CTA NW = 16, or 8 for large footprints
+constexpr int kMB = 32;  // maps per CTA per map-per-lane (MB = 32 MPL); warps per CTA NW = 16, or 8 for large footprints
 constexpr int kStageMax = 48 * 1024;  // input samples up to this many bytes are staged in smem
 constexpr int kPchMax = 4096;         // output pixels per CTA (a whole sample when it fits)
 
@@ -38,6 +39,7 @@ struct EvArgs {
     spk_conv_geom g;
     int Ho, Wo, HWo, K, Co_pad, pch, nw;
     int rpc, Wq, band;  // output rows per CTA, staged row length, staged band bytes
+    int mpl;            // output maps per lane (1 or 2): a CTA covers MB = 32 mpl maps
     int pool, Hp, Wp;   // fused pooling (Eq. 3) of the latency map in the write-out: out0 = pooled lat
     spk_pool_geom pg;
     uint32_t th;          // fire iff S > th  (S = sum of q; th = floor(theta 2^30 / s) >> 7)
@@ -67,16 +69,16 @@ struct EvSmem {
 __host__ __device__ inline size_t ev_al(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ inline int ev_list_len(int K) { return (K + 3) & ~3; }   // padded to whole uint4 batches
 __host__ __device__ inline int ev_cnt_len(int T) { return (T + 32) & ~31; }  // T bins, 32-lane chunks
-__host__ __device__ inline EvSmem ev_smem(int K, int T, int pch, size_t in_bytes, bool pstar, int nw) {
+__host__ __device__ inline EvSmem ev_smem(int K, int T, int pch, size_t in_bytes, bool pstar, int nw, int mb) {
     EvSmem m;
     m.sq = 0;
-    m.koff = ev_al(m.sq + (size_t)(K + 1) * kMB * 4);  // + one zero row for list padding
+    m.koff = ev_al(m.sq + (size_t)(K + 1) * mb * 4);  // + one zero row for list padding
     m.in = ev_al(m.koff + (size_t)K * 4);
     m.lists = ev_al(m.in + in_bytes);
     m.cnt = ev_al(m.lists + (size_t)nw * ev_list_len(K) * 4);
     m.olat = ev_al(m.cnt + (size_t)nw * ev_cnt_len(T) * 4);
-    m.ops = ev_al(m.olat + (size_t)kMB * pch);
-    m.total = ev_al(m.ops + (pstar ? (size_t)kMB * pch * 4 : 0));
+    m.ops = ev_al(m.olat + (size_t)mb * pch);
+    m.total = ev_al(m.ops + (pstar ? (size_t)mb * pch * 4 : 0));
     return m;
 }
 
@@ -97,15 +99,16 @@ __device__ __forceinline__ int lds_u8(uint32_t addr) {
 }
 
 // NCH = ceil(K / 32) synapse chunks held in registers (1..8), or 0 for large receptive fields
-template <typename ACC, int EPI, bool PSTAR, int NCH, int NW>
+template <typename ACC, int EPI, bool PSTAR, int NCH, int NW, int MPL>
 __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     constexpr bool SMALLK = NCH > 0;
+    constexpr int MB = 32 * MPL, LOGM = MPL == 4 ? 2 : MPL == 2 ? 1 : 0;  // maps per CTA; entry = k << (15 + LOGM) | lat
     constexpr int kEvThreads = NW * 32, kEvWarps = NW;
     extern __shared__ __align__(16) unsigned char sm[];
     const spk_conv_geom& g = a.g;
     const int K = a.K, T = g.T;
     const size_t HWi = (size_t)g.Hi * g.Wi;
-    const EvSmem ms = ev_smem(K, T, a.pch, (size_t)a.band, PSTAR, NW);
+    const EvSmem ms = ev_smem(K, T, a.pch, (size_t)a.band, PSTAR, NW, MB);
     uint32_t* sq = reinterpret_cast<uint32_t*>(sm + ms.sq);        // [K+1][32] weight rows (row K = 0)
     int* koff = reinterpret_cast<int*>(sm + ms.koff);              // [K] c*Hi*Wi + i*Wi + j
     uint8_t* sin = sm + ms.in;                                     // staged input band [Ci][rows][Wq]
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     float* ops = reinterpret_cast<float*>(sm + ms.ops);            // [32][pch] (P*)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.z, m0 = blockIdx.y * kMB;
+    const int b = blockIdx.z, m0 = blockIdx.y * MB;
     const int ya = blockIdx.x * a.rpc;                 // first output row of this CTA's chunk
     const int p0 = ya * a.Wo;
     const int npix = min(a.rpc, a.Ho - ya) * a.Wo;
@@ -125,8 +128,8 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
 
     // stage this map block's weight rows, the synapse table and the input band with its
     // zero-padding halo written as "never fires", so synapse reads need no bounds test
-    for (int q = threadIdx.x; q < K * kMB; q += kEvThreads) sq[q] = a.qT[(size_t)(q >> 5) * a.Co_pad + m0 + (q & 31)];
-    if (threadIdx.x < kMB) sq[K * kMB + threadIdx.x] = 0u;
+    for (int q = threadIdx.x; q < K * MB; q += kEvThreads) sq[q] = a.qT[(size_t)(q / MB) * a.Co_pad + m0 + (q % MB)];
+    if (threadIdx.x < MB) sq[K * MB + threadIdx.x] = 0u;
     const int KhKw = g.Kh * g.Kw;
     for (int k = threadIdx.x; k < K; k += kEvThreads) {
         const int c = k / KhKw, r = k - c * KhKw, i = r / g.Kw, j = r - i * g.Kw;
@@ -147,11 +150,27 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     for (int q = threadIdx.x; q < kEvWarps * ncnt; q += kEvThreads) cnts[q] = 0u;
     __syncthreads();
 
-    const int o = m0 + lane;  // this lane's output map
+    const int o0 = m0 + lane * MPL;  // this lane's first output map
     uint32_t* list = lists + (size_t)warp * ev_list_len(K);  // 16-byte aligned per warp
     uint32_t* cnt = cnts + (size_t)warp * ncnt;
-    const unsigned char* wrow = reinterpret_cast<const unsigned char*>(sq + lane);
-    const uint32_t pad_entry = ((uint32_t)K << 15) | (uint32_t)T;  // zero weight row, never a crossing
+    const unsigned char* wrow = reinterpret_cast<const unsigned char*>(sq + lane * MPL);
+    const uint32_t pad_entry = ((uint32_t)K << (15 + LOGM)) | (uint32_t)T;  // zero weight row, never a crossing
+    // this lane's MPL weights of the synapse whose list entry is v (row byte offset = v >> 8)
+    auto ldw = [&](uint32_t v, ACC (&w)[MPL]) {
+        if (MPL == 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(wrow + (v >> 8));
+            w[0] = (ACC)q.x;
+            w[1 % MPL] = (ACC)q.y;
+            w[2 % MPL] = (ACC)q.z;
+            w[3 % MPL] = (ACC)q.w;
+        } else if (MPL == 2) {
+            const uint2 q = *reinterpret_cast<const uint2*>(wrow + (v >> 8));
+            w[0] = (ACC)q.x;
+            w[MPL - 1] = (ACC)q.y;
+        } else {
+            w[0] = (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v >> 8));
+        }
+    };
     // small receptive fields: this lane's synapse offsets stay in registers
     constexpr int kRegChunks = SMALLK ? NCH : 1;
     int rko[kRegChunks];
@@ -228,49 +247,67 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
 #pragma unroll
             for (int c = 0; c < kRegChunks; ++c)
                 if (lr[c] < T)
-                    list[atomicAdd(cnt + lr[c], 1u)] = ((uint32_t)(c * 32 + lane) << 15) | (uint32_t)lr[c];
+                    list[atomicAdd(cnt + lr[c], 1u)] = ((uint32_t)(c * 32 + lane) << (15 + LOGM)) | (uint32_t)lr[c];
         } else {
             for (int k0 = 0; k0 < K; k0 += 32) {
                 const int l = lat_of(k0 + lane, 0);
-                if (l < T) list[atomicAdd(cnt + l, 1u)] = ((uint32_t)(k0 + lane) << 15) | (uint32_t)l;
+                if (l < T) list[atomicAdd(cnt + l, 1u)] = ((uint32_t)(k0 + lane) << (15 + LOGM)) | (uint32_t)l;
             }
         }
         __syncwarp();
-        // (2) running sums over the latency-sorted list
+        // (2) running sums over the latency-sorted list (MPL maps per lane)
         if (EPI == SPK_EPI_POTENTIAL) {
-            ACC S = 0;
+            ACC S[MPL] = {};
             int e = 0;
             for (int t = 0; t < T; ++t) {
                 const int end = (int)cnt[t];
-                for (; e < end; ++e) S += (ACC)*reinterpret_cast<const uint32_t*>(wrow + (list[e] >> 8));
-                if (o < g.Co)
-                    static_cast<float*>(a.out0)[(((size_t)b * T + t) * g.Co + o) * a.HWo + p] =
-                        __fmul_rn(__ll2float_rn((long long)S * 128ll), a.out_scale);
+                for (; e < end; ++e) {
+                    ACC w[MPL];
+                    ldw(list[e], w);
+#pragma unroll
+                    for (int m = 0; m < MPL; ++m) S[m] += w[m];
+                }
+#pragma unroll
+                for (int m = 0; m < MPL; ++m)
+                    if (o0 + m < g.Co)
+                        static_cast<float*>(a.out0)[(((size_t)b * T + t) * g.Co + o0 + m) * a.HWo + p] =
+                            __fmul_rn(__ll2float_rn((long long)S[m] * 128ll), a.out_scale);
             }
         } else {
             const ACC th = (ACC)a.th;
-            ACC S = 0, Sps = 0;
-            int lo = T;             // output latency (first crossing)
-            int pe = 0x7fffffff;    // PSTAR: end index of the crossing's latency group
+            ACC S[MPL] = {}, Sps[MPL] = {};
+            int lo[MPL], pe[MPL];  // output latency (first crossing); PSTAR: end index of its latency group
+#pragma unroll
+            for (int m = 0; m < MPL; ++m) lo[m] = T, pe[m] = 0x7fffffff;
             for (int e = 0; e < n4; e += 4) {
                 const uint4 v = *reinterpret_cast<const uint4*>(list + e);
-                const ACC s0 = S + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.x >> 8));
-                const ACC s1 = s0 + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.y >> 8));
-                const ACC s2 = s1 + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.z >> 8));
-                const ACC s3 = s2 + (ACC)*reinterpret_cast<const uint32_t*>(wrow + (v.w >> 8));
-                if (lo == T && s3 > th) {  // this lane crosses inside the batch (once per lane)
-                    lo = (int)((s0 > th ? v.x : s1 > th ? v.y : s2 > th ? v.z : v.w) & 255u);
-                    if (PSTAR) pe = (int)cnt[lo];
+                ACC w0[MPL], w1[MPL], w2[MPL], w3[MPL];
+                ldw(v.x, w0);
+                ldw(v.y, w1);
+                ldw(v.z, w2);
+                ldw(v.w, w3);
+#pragma unroll
+                for (int m = 0; m < MPL; ++m) {
+                    const ACC s0 = S[m] + w0[m], s1 = s0 + w1[m], s2 = s1 + w2[m], s3 = s2 + w3[m];
+                    if (lo[m] == T && s3 > th) {  // this map crosses inside the batch (once)
+                        lo[m] = (int)((s0 > th ? v.x : s1 > th ? v.y : s2 > th ? v.z : v.w) & 255u);
+                        if (PSTAR) pe[m] = (int)cnt[lo[m]];
+                    }
+                    if (PSTAR && pe[m] <= e + 4) {  // the crossing's group ends inside this batch
+                        const int j = pe[m] - e;     // 1..4 (pe > e: groups end after their crossing)
+                        Sps[m] = j == 1 ? s0 : j == 2 ? s1 : j == 3 ? s2 : s3;
+                        pe[m] = 0x7fffffff;
+                    }
+                    S[m] = s3;
                 }
-                if (PSTAR && pe <= e + 4) {  // the crossing's group ends inside this batch
-                    const int j = pe - e;     // 1..4 (pe > e: groups end after their crossing)
-                    Sps = j == 1 ? s0 : j == 2 ? s1 : j == 3 ? s2 : s3;
-                    pe = 0x7fffffff;
-                }
-                S = s3;
             }
-            olat[lane * a.pch + pl] = (uint8_t)lo;
-            if (PSTAR) ops[lane * a.pch + pl] = lo < T ? __fmul_rn(__ll2float_rn((long long)Sps * 128ll), a.out_scale) : 0.0f;
+#pragma unroll
+            for (int m = 0; m < MPL; ++m) {
+                olat[(lane * MPL + m) * a.pch + pl] = (uint8_t)lo[m];
+                if (PSTAR)
+                    ops[(lane * MPL + m) * a.pch + pl] =
+                        lo[m] < T ? __fmul_rn(__ll2float_rn((long long)Sps[m] * 128ll), a.out_scale) : 0.0f;
+            }
         }
         __syncwarp();
         if (T <= 32) {  // counters for the next pixel
@@ -291,7 +328,7 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
                         (a.Wo & 1) == 0 && (a.pch & 1) == 0;
         if (p2 && a.Wp < 32) {  // short rows (C2): lanes over the map's pooled outputs
             const int nq = (py1 - py0) * a.Wp;
-            for (int r = warp; r < kMB; r += kEvWarps) {
+            for (int r = warp; r < MB; r += kEvWarps) {
                 const int om = m0 + r;
                 if (om >= g.Co) continue;
                 uint8_t* dl = static_cast<uint8_t*>(a.out0) + (((size_t)b * g.Co + om) * a.Hp + py0) * a.Wp;
@@ -307,7 +344,7 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
             return;
         }
         // one (map, pooled row) per warp iteration: lanes run along the row (no divisions)
-        for (int item = warp; item < kMB * (py1 - py0); item += kEvWarps) {
+        for (int item = warp; item < MB * (py1 - py0); item += kEvWarps) {
             const int r = item / (py1 - py0), py = py0 + item % (py1 - py0);
             const int om = m0 + r;
             if (om >= g.Co) continue;
@@ -336,7 +373,7 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
         return;
     }
     // coalesced write-out: one run of npix latencies (and P*) per map
-    for (int r = warp; r < kMB; r += kEvWarps) {
+    for (int r = warp; r < MB; r += kEvWarps) {
         const int om = m0 + r;
         if (om >= g.Co) continue;
         const size_t base = ((size_t)b * g.Co + om) * a.HWo + p0;
@@ -347,32 +384,38 @@ __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
     }
 }
 
-template <typename ACC, int EPI, bool PSTAR, int NCH, int NW>
+template <typename ACC, int EPI, bool PSTAR, int NCH, int NW, int MPL>
 spk_status launch_ev1(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
-    auto k = conv_event_kernel<ACC, EPI, PSTAR, NCH, NW>;
+    auto k = conv_event_kernel<ACC, EPI, PSTAR, NCH, NW, MPL>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return spk::launched("conv_event_kernel(attr)");
     k<<<grid, NW * 32, smem, s>>>(a);
     return spk::launched("conv_event_kernel");
 }
 
-template <typename ACC, int EPI, bool PSTAR>
-spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
-    if (a.nw == 8) return launch_ev1<ACC, EPI, PSTAR, 0, 8>(a, grid, smem, s);
+template <typename ACC, int EPI, bool PSTAR, int MPL>
+spk_status launch_ev_m(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+    if (a.nw == 8) return launch_ev1<ACC, EPI, PSTAR, 0, 8, MPL>(a, grid, smem, s);
     if constexpr (sizeof(ACC) == 4) {  // K <= 256 always sums in 32 bits
         switch ((a.K + 31) / 32) {
-            case 1: return launch_ev1<ACC, EPI, PSTAR, 1, 16>(a, grid, smem, s);
-            case 2: return launch_ev1<ACC, EPI, PSTAR, 2, 16>(a, grid, smem, s);
-            case 3: return launch_ev1<ACC, EPI, PSTAR, 3, 16>(a, grid, smem, s);
-            case 4: return launch_ev1<ACC, EPI, PSTAR, 4, 16>(a, grid, smem, s);
-            case 5: return launch_ev1<ACC, EPI, PSTAR, 5, 16>(a, grid, smem, s);
-            case 6: return launch_ev1<ACC, EPI, PSTAR, 6, 16>(a, grid, smem, s);
-            case 7: return launch_ev1<ACC, EPI, PSTAR, 7, 16>(a, grid, smem, s);
-            case 8: return launch_ev1<ACC, EPI, PSTAR, 8, 16>(a, grid, smem, s);
+            case 1: return launch_ev1<ACC, EPI, PSTAR, 1, 16, MPL>(a, grid, smem, s);
+            case 2: return launch_ev1<ACC, EPI, PSTAR, 2, 16, MPL>(a, grid, smem, s);
+            case 3: return launch_ev1<ACC, EPI, PSTAR, 3, 16, MPL>(a, grid, smem, s);
+            case 4: return launch_ev1<ACC, EPI, PSTAR, 4, 16, MPL>(a, grid, smem, s);
+            case 5: return launch_ev1<ACC, EPI, PSTAR, 5, 16, MPL>(a, grid, smem, s);
+            case 6: return launch_ev1<ACC, EPI, PSTAR, 6, 16, MPL>(a, grid, smem, s);
+            case 7: return launch_ev1<ACC, EPI, PSTAR, 7, 16, MPL>(a, grid, smem, s);
+            case 8: return launch_ev1<ACC, EPI, PSTAR, 8, 16, MPL>(a, grid, smem, s);
             default: break;
         }
     }
-    return launch_ev1<ACC, EPI, PSTAR, 0, 16>(a, grid, smem, s);
+    return launch_ev1<ACC, EPI, PSTAR, 0, 16, MPL>(a, grid, smem, s);
+}
+
+template <typename ACC, int EPI, bool PSTAR>
+spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+    if (a.mpl == 4) return launch_ev_m<ACC, EPI, PSTAR, 4>(a, grid, smem, s);
+    return a.mpl == 2 ? launch_ev_m<ACC, EPI, PSTAR, 2>(a, grid, smem, s) : launch_ev_m<ACC, EPI, PSTAR, 1>(a, grid, smem, s);
 }
 
 }  // namespace
@@ -381,14 +424,27 @@ bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
     p.Ho = (g.Hi + 2 * g.Ph - g.Kh) / g.Sh + 1;
     p.Wo = (g.Wi + 2 * g.Pw - g.Kw) / g.Sw + 1;
     p.K = g.Ci * g.Kh * g.Kw;
-    if (g.Kh > 255 || g.Kw > 255 || g.T > 254 || p.K >= (1 << 17)) return false;  // list entry k << 15
+    if (g.Kh > 255 || g.Kw > 255 || g.T > 254) return false;
+    // several output maps per lane (64 or 128 per CTA) divide the per-pixel sort and list
+    // work per map for wide layers; one for narrow ones (Co <= 32)
+    static const int mpl_env = [] {
+        const char* e = std::getenv("SPK_EV_MPL");  // tuning knob: 1, 2 or 4
+        return e ? std::atoi(e) : 0;
+    }();
+    // (measured: two maps per lane win on every wide layer — C4 conv0 5.26 -> 3.51 ms, C5 conv0
+    // 304 -> 236 ms; four lose: the 128-map output staging shrinks the row chunks)
+    p.mpl = (mpl_env == 1 || mpl_env == 2 || mpl_env == 4) ? mpl_env : g.Co > 32 ? 2 : 1;
+    // the weight rows of a CTA's map block must leave room for the rest (at most 128 KB)
+    while (p.mpl > 1 && (size_t)(p.K + 1) * kMB * p.mpl * 4 > 128 * 1024 && mpl_env == 0) p.mpl >>= 1;
+    if ((long long)p.K << (15 + (p.mpl == 4 ? 2 : p.mpl == 2 ? 1 : 0)) >= (1ll << 32)) return false;  // list entry
+    const int mb = kMB * p.mpl;
     if ((double)g.Ci * g.Hi * g.Wi >= 2147483647.0) return false;
     p.acc64 = (double)p.K * 8388608.0 >= 4294967296.0 ? 1 : 0;
     p.Wq = g.Wi + 2 * g.Pw;
     // whole output rows per CTA: the staged band (with halo) and the output staging must fit;
     // a whole sample per CTA when possible (enables the fused pooling write-out)
     auto band = [&](int r) { return (size_t)g.Ci * (size_t)((r - 1) * g.Sh + g.Kh) * p.Wq; };
-    auto smem = [&](int r, int nw) { return ev_smem(p.K, g.T, r * p.Wo, band(r), true, nw).total; };
+    auto smem = [&](int r, int nw) { return ev_smem(p.K, g.T, r * p.Wo, band(r), true, nw, mb).total; };
     int r = std::max(1, std::min(p.Ho, kPchMax / std::max(1, p.Wo)));
     while (r > 1 && (band(r) > (size_t)kStageMax || smem(r, 16) > 200 * 1024)) --r;
     p.nw = 16;
@@ -399,9 +455,9 @@ bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
     p.band = band(r);
     p.stage = r >= p.Ho ? 1 : 0;  // whole sample in one CTA
     p.smem_bytes = smem(r, p.nw);
-    p.n_mb = (g.Co + kMB - 1) / kMB;
-    p.Co_pad = p.n_mb * kMB;
-    p.MB = kMB;
+    p.n_mb = (g.Co + mb - 1) / mb;
+    p.Co_pad = p.n_mb * mb;
+    p.MB = mb;
     p.ws_bytes = 256 + (size_t)p.K * p.Co_pad * 4;
     return true;
 }
@@ -438,6 +494,7 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     a.rpc = p.rpc;
     a.Wq = p.Wq;
     a.band = (int)p.band;
+    a.mpl = p.mpl;
     if (pool) {  // caller checked: FIRE, whole sample in one CTA
         a.pool = 1;
         a.pg = *pool;
@@ -450,7 +507,7 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     const dim3 grid((unsigned)((p.Ho + p.rpc - 1) / p.rpc), (unsigned)p.n_mb, (unsigned)g.B);
     const bool ps = out1 != nullptr && epi == SPK_EPI_FIRE;
     a.nw = p.nw;
-    const size_t smem = ev_smem(p.K, g.T, p.pch, p.band, ps, p.nw).total;
+    const size_t smem = ev_smem(p.K, g.T, p.pch, p.band, ps, p.nw, p.MB).total;
     if (epi == SPK_EPI_POTENTIAL)
         return p.acc64 ? launch_ev<unsigned long long, SPK_EPI_POTENTIAL, false>(a, grid, smem, s)
                        : launch_ev<uint32_t, SPK_EPI_POTENTIAL, false>(a, grid, smem, s);
