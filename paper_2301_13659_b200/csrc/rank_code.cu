@@ -518,14 +518,16 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         return spk::launched("rank_code_sort_kernel");
     }
     if (sort) {  // larger samples: bucket histogram + boundary-bucket sort
-        using Cfg = HistCfg<16, 1024, 8192, false>;
+        // 16384 buckets (exponent + 6 mantissa bits) and 4096 candidates: 96 KB, two CTAs per
+        // SM (C5 samples have 2-3K boundary-bucket values; more falls back to the radix select)
+        using Cfg = HistCfg<17, 1024, 4096, false>;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(rank_code_hist_kernel<16, 1024, 8192, false>,
+            cudaFuncSetAttribute(rank_code_hist_kernel<17, 1024, 4096, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(0));
             attr = true;
         }
-        rank_code_hist_kernel<16, 1024, 8192, false><<<B, 1024, Cfg::smem(0), s>>>(y, N, T, thresh, lat);
+        rank_code_hist_kernel<17, 1024, 4096, false><<<B, 1024, Cfg::smem(0), s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel");
     }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
