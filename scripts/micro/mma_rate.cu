@@ -55,7 +55,7 @@ int main() {
     double tops = 2.0 * macs_per * iters * 148 / (ms * 1e-3) / 1e12;
     printf("%-22s N=%3d  cycles/MMA %7.1f   chip %7.1f TOPS  (err %s)\n", name, N, cyc, tops, cudaGetErrorString(cudaGetLastError()));
   };
-  for (int N : {32, 64, 112, 128, 256}) {
+  for (int N : {32, 64, 96, 112, 128, 144, 192, 224, 256}) {
     run(k<0, true>, "i8  A=tmem  B=smem", N, 128.0 * N * 32);
     run(k<0, false>, "i8  A=smem  B=smem", N, 128.0 * N * 32);
     run(k<1, true>, "f16 A=tmem  B=smem", N, 128.0 * N * 16);
