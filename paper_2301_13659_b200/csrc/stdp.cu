@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restr
         __syncthreads();
         // phase 1: gathers, kUpdThreads / kUpdW winners per pass, several passes in flight
         if (valid1) {
-            constexpr int kStep = kUpdThreads / kUpdW, kBatch = 16;  // kBatch independent loads in flight
+            constexpr int kStep = kUpdThreads / kUpdW, kBatch = 32;  // kBatch independent loads in flight
             for (int e0b = e_lane; e0b < m; e0b += kStep * kBatch) {
                 int tj[kBatch];
 #pragma unroll
