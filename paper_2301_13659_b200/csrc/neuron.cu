@@ -265,6 +265,46 @@ __global__ void __launch_bounds__(kT) inhibit_wide_kernel(uint8_t* __restrict__ 
     for (; c < C; ++c) suppress(c, *reinterpret_cast<const uint32_t*>(L + (size_t)c * HW));
 }
 
+// Small maps (HW <= 32: C2 layer 3, 200 maps of 4 x 4): one CTA per sample, thread
+// (pixel, channel group) keeps its least key in a register, groups reduced through shared
+// memory — no 200-way atomics on one pixel's slot.
+__global__ void __launch_bounds__(kT) inhibit_small_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar,
+                                                           int C, int HW, int T) {
+    __shared__ unsigned long long part[kT];
+    __shared__ uint32_t win_c[32];
+    const int b = blockIdx.x;
+    const int ngrp = kT / HW, p = threadIdx.x % HW, grp = threadIdx.x / HW;
+    uint8_t* L = lat + (size_t)b * C * HW;
+    float* P = pstar + (size_t)b * C * HW;
+    unsigned long long best = ~0ull;
+    if (grp < ngrp)
+        for (int c = grp; c < C; c += ngrp) {
+            const int l = L[c * HW + p];
+            if (l >= T) continue;
+            const uint32_t pd = ~spk_float_order_u32(P[c * HW + p] + 0.0f);  // -0 -> +0: equal potentials tie on c
+            const unsigned long long key = ((unsigned long long)l << 56) | ((unsigned long long)pd << 24) | (unsigned)c;
+            best = key < best ? key : best;
+        }
+    part[threadIdx.x] = best;
+    __syncthreads();
+    if (threadIdx.x < HW) {
+        unsigned long long m = ~0ull;
+        for (int g2 = 0; g2 < ngrp; ++g2) m = part[g2 * HW + threadIdx.x] < m ? part[g2 * HW + threadIdx.x] : m;
+        win_c[threadIdx.x] = m == ~0ull ? 0xffffffffu : (uint32_t)(m & 0xFFFFFFu);
+    }
+    __syncthreads();
+    if (grp < ngrp) {
+        const uint32_t wc = win_c[p];
+        for (int c = grp; c < C; c += ngrp) {
+            const int o = c * HW + p;
+            if (L[o] < T && (uint32_t)c != wc) {
+                L[o] = (uint8_t)T;
+                P[o] = 0.0f;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- gather
 __global__ void gather_kernel(const uint8_t* __restrict__ lat, size_t n, int T, float* __restrict__ f) {
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -411,6 +451,10 @@ extern "C" spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int 
     SPK_CHECK((long long)H * W < (1ll << 31) && (long long)C * kInhPix < (1ll << 31), SPK_ERR_SHAPE, "map too large");
     SPK_CHECK(B <= 65535, SPK_ERR_SHAPE, "B=%d > 65535", B);
     const int HW = H * W;
+    if (HW <= 32) {
+        inhibit_small_kernel<<<(unsigned)B, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
+        return spk::launched("inhibit_small_kernel");
+    }
     if (HW >= 4096 && (HW & 3) == 0 && ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(pstar)) & 15) == 0) {
         const dim3 grid(spk::ceil_div((size_t)HW / 4, kT), (unsigned)B);
         inhibit_wide_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);

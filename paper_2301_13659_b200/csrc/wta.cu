@@ -155,6 +155,31 @@ __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) 
     const bool cached = !overflow;
     const int nl = cached ? (int)nkeys : 0;
 
+    if (a.cs == 1 && cached && nl <= 32) {
+        // few candidates (C2 layer 3 after inhibition: <= 16 per sample): one warp runs every
+        // round with shuffles — each lane holds one key and drops it when a pick suppresses it
+        if (threadIdx.x >= 32) return;
+        const unsigned long long key = lane < nl ? keys[lane] : ~0ull;
+        const int i = (int)(key & 0xffffffull);
+        const int c = i / HW, r = i - c * HW, y = r / a.W, x = r - y * a.W;
+        bool alive = key != ~0ull;
+        int np = 0;
+        for (int round = 0; round < a.k; ++round) {
+            unsigned long long best = alive ? key : ~0ull;
+            for (int o = 16; o; o >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (best == ~0ull) break;
+            const int wi = (int)(best & 0xffffffull);
+            const int wc = wi / HW, wr = wi - wc * HW, wy = wr / a.W, wx = wr - wy * a.W;
+            if (lane == 0) a.win[(size_t)b * a.k + round] = spk_winner{b, (int)(best >> 56), wc, wy, wx, 0};
+            if (c == wc || (abs(y - wy) <= a.radius && abs(x - wx) <= a.radius)) alive = false;
+            ++np;
+        }
+        if (lane == 0) {
+            for (int q = np; q < a.k; ++q) a.win[(size_t)b * a.k + q] = spk_winner{-1, -1, -1, -1, -1, -1};
+            a.nwin[b] = np;
+        }
+        return;
+    }
     int npicked = 0;
     for (int round = 0; round < a.k; ++round) {
         unsigned long long best = ~0ull;

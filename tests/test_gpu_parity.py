@@ -260,6 +260,29 @@ def test_inhibit_exact(spk, ties):
     np.testing.assert_array_equal(host(gps), rps.astype(np.float32))
 
 
+@pytest.mark.parametrize("shape", [(4, 200, 4, 4), (2, 50, 5, 6), (3, 7, 1, 1)])
+@pytest.mark.parametrize("ties", [False, True])
+def test_inhibit_and_wta_small_maps(spk, shape, ties):
+    """HW <= 32 (C2 layer 3: 200 maps of 4 x 4): the per-sample register inhibition kernel, and
+    the one-warp WTA rounds on its <= HW surviving keys."""
+    B, C, H, W = shape
+    T = 15
+    Q, lat, ps = _records(B, T, C, H, W, 0.5, ties)
+    ref = oracle.inhibit(Q)
+    rlat, rps = lat_and_pstar(ref, 0.0)
+    glat, gps = spk.inhibit(cu(lat), cu(ps.astype(np.float32)), T)
+    np.testing.assert_array_equal(host(glat), rlat)
+    np.testing.assert_array_equal(host(gps), rps.astype(np.float32))
+    for k, r in [(8, 1), (5, 3), (20, 0)]:
+        win, nwin = oracle.wta(ref, k, r)
+        gw, gn = spk.wta(glat, gps, T, k, r)
+        gw, gn = host(gw), host(gn)
+        np.testing.assert_array_equal(gn, nwin)
+        for b in range(B):
+            np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
+            assert (gw[b, nwin[b]:] == -1).all()
+
+
 @pytest.mark.parametrize("ties", [False, True])
 def test_inhibit_exact_large_maps(spk, ties):
     """HW >= 4096: the 4-pixels-per-thread register kernel (C4 shapes)."""
