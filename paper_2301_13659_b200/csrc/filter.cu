@@ -41,14 +41,17 @@ constexpr int TX = 32, TY = 8;
 // KC > 0: the kernel count is a compile-time constant (every config: 2, 4 or 6), so each
 // coefficient is an immediate constant-bank operand of its FFMA and the KC independent
 // fmaf chains of a pixel interleave; KC = 0: runtime kernel count.
-template <int R, int KC>
+// PAIR: kernel 2m+1 is exactly the negation of kernel 2m (on/off DoG and LoG pairs):
+// one fmaf chain per pair, the second output is 0 - acc — bit-identical to the negated
+// chain (round-to-nearest is symmetric, and an exactly-zero sum is +0 on both sides).
+template <int R, int KC, bool PAIR = false>
 __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
                                                        int Kr, int pad, int Ho, int Wo, float* __restrict__ out,
                                                        const FilterCoef coef) {
     constexpr int E = 2 * R + 1, TW = TX + 2 * R, TH = TY + 2 * R;
     __shared__ float tile[TH][TW];
     __shared__ float lut[256];  // u8 / 255 in fp32 (R-SCALE), one IEEE division per value
-    const int K = KC > 0 ? KC : Kr;
+    const int K = KC > 0 ? (PAIR ? 2 * KC : KC) : Kr;
     const int tid = threadIdx.y * TX + threadIdx.x;
     lut[tid] = __fdiv_rn((float)tid, 255.0f);  // TX * TY == 256
     const int bc = blockIdx.z;  // b * C + ci
@@ -69,6 +72,7 @@ __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restric
     const int b = bc / C, ci = bc - b * C;
     float* o = out + (((size_t)b * C + ci) * K * Ho + y) * Wo + x;
     if constexpr (KC > 0) {
+        constexpr int KS = PAIR ? 2 : 1;  // kernel stride between chains
         float acc[KC];
 #pragma unroll
         for (int k = 0; k < KC; ++k) acc[k] = 0.0f;
@@ -78,10 +82,13 @@ __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restric
             for (int j = 0; j < E; ++j) {
                 const float v = tile[threadIdx.y + i][threadIdx.x + j];
 #pragma unroll
-                for (int k = 0; k < KC; ++k) acc[k] = __fmaf_rn(coef.c[k * E * E + i * E + j], v, acc[k]);
+                for (int k = 0; k < KC; ++k) acc[k] = __fmaf_rn(coef.c[KS * k * E * E + i * E + j], v, acc[k]);
             }
 #pragma unroll
-        for (int k = 0; k < KC; ++k) o[(size_t)k * Ho * Wo] = acc[k];
+        for (int k = 0; k < KC; ++k) {
+            o[(size_t)KS * k * Ho * Wo] = acc[k];
+            if (PAIR) o[(size_t)(KS * k + 1) * Ho * Wo] = __fsub_rn(0.0f, acc[k]);
+        }
     } else if constexpr (E * E <= 81) {  // window in registers, reused by all K kernels
         float v[E * E];
 #pragma unroll
@@ -114,7 +121,7 @@ __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restric
 // (R-FILTER-ORDER), so the K fmaf chains are the oracle's, bit for bit.
 constexpr int RY = 4;
 
-template <int R, int KC>
+template <int R, int KC, bool PAIR = false>
 __global__ void __launch_bounds__(TX* TY) filter_rb_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
                                                           int pad, int Ho, int Wo, float* __restrict__ out,
                                                           const FilterCoef coef) {
@@ -155,16 +162,21 @@ __global__ void __launch_bounds__(TX* TY) filter_rb_kernel(const uint8_t* __rest
 #pragma unroll
             for (int j = 0; j < E; ++j)
 #pragma unroll
-                for (int k = 0; k < KC; ++k) acc[r][k] = __fmaf_rn(coef.c[k * E * E + i * E + j], v[j], acc[r][k]);
+                for (int k = 0; k < KC; ++k)
+                    acc[r][k] = __fmaf_rn(coef.c[(PAIR ? 2 : 1) * k * E * E + i * E + j], v[j], acc[r][k]);
         }
     }
     const int b = bc / C, ci = bc - b * C;
-    float* o = out + (((size_t)b * C + ci) * KC * Ho + yb) * Wo + x;
+    constexpr int KO = PAIR ? 2 * KC : KC;  // output kernels
+    float* o = out + (((size_t)b * C + ci) * KO * Ho + yb) * Wo + x;
 #pragma unroll
     for (int r = 0; r < RY; ++r)
         if (yb + r < Ho)
 #pragma unroll
-            for (int k = 0; k < KC; ++k) o[(size_t)k * Ho * Wo + (size_t)r * Wo] = acc[r][k];
+            for (int k = 0; k < KC; ++k) {
+                o[(size_t)(PAIR ? 2 * k : k) * Ho * Wo + (size_t)r * Wo] = acc[r][k];
+                if (PAIR) o[(size_t)(2 * k + 1) * Ho * Wo + (size_t)r * Wo] = __fsub_rn(0.0f, acc[r][k]);
+            }
 }
 
 spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std::vector<float>& coef,
@@ -179,6 +191,28 @@ spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std:
     SPK_CHECK(grid.z <= 65535u, SPK_ERR_SHAPE, "B*C=%d > 65535", B * C);
     cudaStream_t s = spk::as_cuda(stream);
     const dim3 blk(TX, TY);
+    // exact negation pairs (on/off DoG, LoG): kernel 2m+1 == -kernel 2m for every coefficient
+    const int E2 = (2 * radius + 1) * (2 * radius + 1);
+    bool pairs = K % 2 == 0;
+    for (int k = 0; pairs && k < K; k += 2)
+        for (int q = 0; q < E2; ++q)
+            if (!(coef[(size_t)(k + 1) * E2 + q] == -coef[(size_t)k * E2 + q])) {
+                pairs = false;
+                break;
+            }
+    if (radius == 3 && pairs && (K == 2 || K == 4 || K == 6)) {  // every DoG / LoG front end
+        const bool small = Ho * Wo < 64 * 64;
+        const dim3 g4(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY * RY), (unsigned)(B * C));
+        switch (K / 2 + (small ? 0 : 8)) {
+            case 1: filter_kernel<3, 1, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 2: filter_kernel<3, 2, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 3: filter_kernel<3, 3, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 9: filter_rb_kernel<3, 1, true><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 10: filter_rb_kernel<3, 2, true><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            default: filter_rb_kernel<3, 3, true><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+        }
+        return spk::launched("filter_kernel<pairs>");
+    }
     if (radius == 3 && (K == 1 || K == 2 || K == 4 || K == 6) && Ho * Wo < 64 * 64) {  // small maps (C1-C3)
         switch (K) {
             case 1: filter_kernel<3, 1><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;

@@ -38,7 +38,8 @@ def test_filter_bit_identical(spk, name):
         got = spk.dog(cu(imgs), spk.log_pairs(fr["stds"]), fr["radius"], fr["pad"])
     else:
         got = spk.gabor(cu(imgs), fr["params"], fr["radius"], fr["pad"])
-    np.testing.assert_array_equal(host(got), ref)
+    # bit for bit, including the sign of zeros (on/off pairs are computed as 0 - acc)
+    np.testing.assert_array_equal(host(got).view(np.uint32), ref.astype(np.float32).view(np.uint32))
 
 
 def test_filter_odd_geometry(spk):
@@ -46,7 +47,12 @@ def test_filter_odd_geometry(spk):
     for r, pad in [(2, 0), (3, 1), (1, 4), (0, 0)]:
         pairs = [(0.8, 1.7), (2.2, 1.1)]
         ref = oracle.filter_apply(imgs, oracle.dog_bank(pairs, r), pad)
-        np.testing.assert_array_equal(host(spk.dog(cu(imgs), pairs, r, pad)), ref)
+        np.testing.assert_array_equal(host(spk.dog(cu(imgs), pairs, r, pad)).view(np.uint32),
+                                      ref.astype(np.float32).view(np.uint32))
+        onoff = [(1.0, 2.0), (2.0, 1.0), (0.7, 1.5), (1.5, 0.7)]  # exact negation pairs
+        ref = oracle.filter_apply(imgs, oracle.dog_bank(onoff, r), pad)
+        np.testing.assert_array_equal(host(spk.dog(cu(imgs), onoff, r, pad)).view(np.uint32),
+                                      ref.astype(np.float32).view(np.uint32))
         gab = [(2.0, 0.3, 0.6, 4.0, 0.5)]
         ref = oracle.filter_apply(imgs, oracle.gabor_bank(gab, r), pad)
         np.testing.assert_array_equal(host(spk.gabor(cu(imgs), gab, r, pad)), ref)
