@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const floa
 //          buckets that straddle a bin boundary.
 //  pass 2: values of ordinary buckets are written at once; values of boundary
 //          buckets are compacted as unique keys (value bits << 32 | ~index, R-TIE),
-//          bitonic-sorted descending, and get rank = above + (position inside their
+//          grouped by bucket, and get rank = above + (number of larger keys in their
 //          bucket).  Exactly the ranks of the full sort.
 // More boundary-bucket values than fit shared memory (massive exact ties) -> the
 // sample falls back to the multi-target radix select above (exact, slower).
@@ -288,6 +288,7 @@ template <int SHIFT, int kHT, int kCand, bool STAGE>
 __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __restrict__ y, int N, int T, float thresh,
                                                             uint8_t* __restrict__ lat) {
     constexpr int kBkt = HistCfg<SHIFT, kHT, kCand, STAGE>::kBkt, kNW = kHT / 32;
+    static_assert(kBkt / 2 >= kCand, "the bucket table is reused for the grouped candidates");
     extern __shared__ __align__(16) unsigned char dyn[];
     unsigned int* tab = reinterpret_cast<unsigned int*>(dyn);                         // [kBkt]
     unsigned long long* cand = reinterpret_cast<unsigned long long*>(dyn + (size_t)kBkt * 4);  // [kCand]
@@ -441,33 +442,40 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
         rank_code_body<false, kHT>(ys, N, T, thresh, 1, out, sm, nullptr);
         return;
     }
-    int P = 1;
-    while (P < nc) P <<= 1;
-    for (int q = nc + tid; q < P; q += kHT) cand[q] = 0ull;  // sorts last
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int t = tid; t < (P >> 1); t += kHT) {
-                const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1)), b = a + j;
-                const unsigned long long ka = cand[a], kb = cand[b];
-                const bool desc = (a & k) == 0;
-                if ((ka < kb) == desc) {
-                    cand[a] = kb;
-                    cand[b] = ka;
-                }
-            }
-            __syncthreads();
+    // group the candidates by boundary bucket (segments sized by the histogram), then rank
+    // each one inside its own bucket by counting the larger keys there — no sort
+    __shared__ unsigned int seg_start[kMaxBnd], seg_cur[kMaxBnd], seg_above[kMaxBnd];
+    const int nb = (int)s_nbnd;
+    if (tid == 0) {
+        unsigned int acc = 0;
+        for (int q = 0; q < nb; ++q) {
+            seg_start[q] = acc;
+            seg_cur[q] = 0;
+            seg_above[q] = tab[bnd_b[q]] & 0xffffffu;  // values in higher buckets
+            acc += bnd_c[q];
         }
     }
-    const int nb = (int)s_nbnd;
+    __syncthreads();
+    // the bucket table is no longer read: its space holds the grouped keys
+    unsigned long long* grp = reinterpret_cast<unsigned long long*>(tab);
     for (int j = tid; j < nc; j += kHT) {
         const unsigned long long key = cand[j];
-        const unsigned int u = (unsigned int)(key >> 32), B = u >> SHIFT;
+        const unsigned int B = (unsigned int)(key >> 32) >> SHIFT;
+        int q = 0;
+        while (bnd_b[q] != B) ++q;  // its boundary bucket (one of <= T-1)
+        grp[seg_start[q] + atomicAdd(&seg_cur[q], 1u)] = key;
+    }
+    __syncthreads();
+    for (int j = tid; j < nc; j += kHT) {
+        const unsigned long long key = grp[j];
+        const unsigned int B = (unsigned int)(key >> 32) >> SHIFT;
+        int q = 0;
+        while (bnd_b[q] != B) ++q;
+        const unsigned int s0 = seg_start[q], s1 = s0 + bnd_c[q];
+        unsigned int larger = 0;
+        for (unsigned int e = s0; e < s1; ++e) larger += grp[e] > key;
         const unsigned int idx = 0xffffffffu - (unsigned int)(key & 0xffffffffull);
-        unsigned int sB = 0;  // candidates in higher boundary buckets
-        for (int q = 0; q < nb; ++q)
-            if (bnd_b[q] > B) sB += bnd_c[q];
-        const unsigned int rank = (tab[B] & 0xffffffu) + ((unsigned int)j - sB);
+        const unsigned int rank = seg_above[q] + larger;
         out[idx] = (uint8_t)(((unsigned long long)rank * T) / n);
     }
 }
