@@ -346,7 +346,7 @@ def main():
             "stage_ms_note": "per-stage device time inside the timed graph replays (external event nodes)",
             "clocks": clk,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the oracle baseline is an N = 1 figure
             line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
         print(json.dumps(line), flush=True)
     if world > 1:
