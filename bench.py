@@ -97,6 +97,21 @@ def conv_flops(rec, B, T):
     return 2.0 * B * T * rec["Ho"] * rec["Wo"] * g.Co * (g.Ci * g.Kh * g.Kw)
 
 
+def event_adds(net, li):
+    """Active-synapse adds of one event-form conv launch: every output map o and output pixel
+    (y, x) adds the weight of each in-bounds input tap that fires (lat < T) once."""
+    import torch
+
+    g = net.layers[li]["geom"]
+    act = (net.input_of(li) < net.T).float().sum(dim=1, keepdim=True)  # [B][1][Hi][Wi]
+    ones = torch.ones((1, 1, g.Kh, g.Kw), device=act.device)
+    per_px = torch.nn.functional.conv2d(act, ones, stride=(g.Sh, g.Sw), padding=(g.Ph, g.Pw))
+    return float(per_px.sum().item()) * g.Co
+
+
+SMEM_WORDS_PER_CLK_SM = 32  # 128 B/clk/SM shared-memory bandwidth / 4-byte weight per add
+
+
 def cpu_baseline(cfg, n_images):
     """The oracle as it stands (oracle/, single thread) on a bounded sample of the same workload."""
     import oracle
@@ -311,6 +326,24 @@ def main():
         if tf.exists():
             traffic = json.loads(tf.read_text()).get(f"{cfg['name']}:{dom}")
         total_imgs = cfg["batch"] if forward else world * B
+        if net.layers[li]["prec"] == "event":
+            # event form on CUDA cores: one shared-memory weight read + integer add per active synapse
+            adds = event_adds(net, li)
+            sm_mhz = clk.get("sm_mhz") or 1965.0
+            peak_g = 148 * SMEM_WORDS_PER_CLK_SM * sm_mhz * 1e6 / 1e9
+            ach_g = adds / (convs[dom] * 1e-3) / 1e9
+            roof = {"bound": "alu", "kernel": f"conv_event_kernel ({dom})", "achieved": ach_g, "peak": peak_g,
+                    "unit": "Gadd/s", "frac": ach_g / peak_g, "traffic": traffic,
+                    "peak_note": "148 SMs x 32 four-byte shared-memory weight reads/clk (128 B/clk/SM) at the "
+                                 "sampled SM clock; one read + int add per active synapse (DESIGN §5.1b)",
+                    "algorithmic_adds_per_launch": adds, "launch_ms": convs[dom]}
+        else:
+            roof = {"bound": "tensor", "kernel": f"conv_tc_kernel ({dom}, incl. weight pack)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": traffic,
+                    "peak_note": f"int8 dense = {src} bf16 burst {bf16} x {INT8_OVER_BF16} (nominal 4.5/2.25); "
+                                 "the exact path issues 3 int8 MMAs per algorithmic MAC, so its ceiling is 1/3",
+                    "algorithmic_flops_per_launch": flops, "launch_ms": convs[dom]}
         line = {
             "metric": METRIC,
             "value": total_imgs / (ms * 1e-3),
@@ -336,12 +369,7 @@ def main():
             "e2e": {"value": total_imgs / (e2e_ms * 1e-3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches_per_step * args.steps),
-            "roofline": {"bound": "tensor", "kernel": f"conv_tc_kernel ({dom}, incl. weight pack)",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": traffic,
-                         "peak_note": f"int8 dense = {src} bf16 burst {bf16} x {INT8_OVER_BF16} (nominal 4.5/2.25); "
-                                      "the exact path issues 3 int8 MMAs per algorithmic MAC, so its ceiling is 1/3",
-                         "algorithmic_flops_per_launch": flops, "launch_ms": convs[dom]},
+            "roofline": roof,
             "stage_ms": live_ms,
             "stage_ms_note": "per-stage device time inside the timed graph replays (external event nodes)",
             "clocks": clk,
