@@ -54,7 +54,7 @@ extern "C" spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_
     SPK_CHECK(std::isfinite(w_max) && w_max > 0.0f, SPK_ERR_ARG, "w_max must be finite and > 0");
     if (prec == SPK_PREC_EVENT) {
         EvPlan e;
-        SPK_CHECK(ev_plan(*g, e), SPK_ERR_UNSUPPORTED, "EVENT: a 32-map weight block of K=%d synapses does not fit shared memory",
+        SPK_CHECK(ev_plan(*g, e, true), SPK_ERR_UNSUPPORTED, "EVENT: a 32-map weight block of K=%d synapses does not fit shared memory",
                   g->Ci * g->Kh * g->Kw);
         SPK_CHECK(ws != nullptr && ws_bytes >= e.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
                   e.ws_bytes);

@@ -23,7 +23,7 @@ struct EvPlan {
     size_t band;
     size_t smem_bytes, ws_bytes;
 };
-bool ev_plan(const spk_conv_geom& g, EvPlan& p);
+bool ev_plan(const spk_conv_geom& g, EvPlan& p, bool fill = false);  // fill: split rows for small grids (spk_conv)
 spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_geom& g, const EvPlan& p,
                           spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
                           cudaStream_t s, const spk_pool_geom* pool = nullptr);

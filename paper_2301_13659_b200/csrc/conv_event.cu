@@ -420,7 +420,7 @@ spk_status launch_ev(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
 
 }  // namespace
 
-bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
+bool ev_plan(const spk_conv_geom& g, EvPlan& p, bool fill) {
     p.Ho = (g.Hi + 2 * g.Ph - g.Kh) / g.Sh + 1;
     p.Wo = (g.Wi + 2 * g.Pw - g.Kw) / g.Sw + 1;
     p.K = g.Ci * g.Kh * g.Kw;
@@ -447,6 +447,14 @@ bool ev_plan(const spk_conv_geom& g, EvPlan& p) {
     auto smem = [&](int r, int nw) { return ev_smem(p.K, g.T, r * p.Wo, band(r), true, nw, mb).total; };
     int r = std::max(1, std::min(p.Ho, kPchMax / std::max(1, p.Wo)));
     while (r > 1 && (band(r) > (size_t)kStageMax || smem(r, 16) > 200 * 1024)) --r;
+    // small batches (C1: one image) would leave most SMs idle with a whole sample per CTA:
+    // split the rows until the grid covers ~two CTAs per SM (unfused launches only — the
+    // fused pooling write-out keeps its chunking)
+    const long long blocks = (long long)g.B * ((g.Co + mb - 1) / mb);
+    if (fill && blocks * ((p.Ho + r - 1) / r) < 148) {
+        const long long want = (296 + blocks - 1) / blocks;  // row chunks per (sample, map block)
+        r = std::max(1, std::min(r, (int)((p.Ho + want - 1) / want)));
+    }
     p.nw = 16;
     if (smem(r, 16) > 200 * 1024) p.nw = 8;
     if (band(r) > (size_t)kStageMax * 2 || smem(r, p.nw) > 200 * 1024 || r * p.Wo > 65535) return false;

@@ -174,10 +174,10 @@ __global__ void __launch_bounds__(kT) pool_smem_kernel(const uint8_t* __restrict
 constexpr int kInhPix = 256;
 
 __global__ void __launch_bounds__(kT) inhibit_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar, int C,
-                                                     int HW, int T) {
+                                                     int HW, int T, int pc) {
     __shared__ unsigned long long best[kInhPix];
-    const int b = blockIdx.y, p0 = blockIdx.x * kInhPix;
-    const int np = min(kInhPix, HW - p0);
+    const int b = blockIdx.y, p0 = blockIdx.x * pc;  // pc <= kInhPix pixels per CTA
+    const int np = min(pc, HW - p0);
     uint8_t* L = lat + (size_t)b * C * HW + p0;
     float* P = pstar + (size_t)b * C * HW + p0;
     for (int q = threadIdx.x; q < np; q += kT) best[q] = ~0ull;
@@ -460,8 +460,15 @@ extern "C" spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int 
         inhibit_wide_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
         return spk::launched("inhibit_wide_kernel");
     }
-    const dim3 grid(spk::ceil_div((size_t)HW, kInhPix), (unsigned)B);
-    inhibit_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
+    // fewer pixels per CTA when the grid would not cover the SMs (C1: one 28x28 sample),
+    // so each thread walks a few cells instead of a long chain of dependent loads
+    int pc = kInhPix;
+    if ((long long)B * spk::ceil_div((size_t)HW, kInhPix) < 148) {
+        const int want = (296 + B - 1) / B;  // CTAs per sample
+        pc = std::max(1, std::min(kInhPix, (HW + want - 1) / want));
+    }
+    const dim3 grid(spk::ceil_div((size_t)HW, pc), (unsigned)B);
+    inhibit_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T, pc);
     return spk::launched("inhibit_kernel");
 }
 

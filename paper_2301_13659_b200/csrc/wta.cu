@@ -280,7 +280,11 @@ extern "C" spk_status spk_wta(const uint8_t* lat, const float* pstar, int B, int
     WtaArgs a{lat, pstar, C, H, W, T, k, radius, 1, 0, 0u, win, nwin};
     const long long N = (long long)C * H * W, HW = (long long)H * W;
     // cluster size: about 16K neurons per CTA, at most 8 CTAs and at most one pixel... per CTA
-    a.cs = (int)std::min<long long>(std::min<long long>(kMaxCS, (N + 16383) / 16384), HW);
+    long long cs = std::min<long long>(kMaxCS, (N + 16383) / 16384);
+    // a few samples (C1: one) leave the GPU idle: widen the cluster so phase 1's HBM pass is
+    // spread over up to 8 SMs (about 2K neurons per CTA)
+    if ((long long)B * cs < 148) cs = std::max(cs, std::min<long long>(kMaxCS, (N + 2047) / 2048));
+    a.cs = (int)std::min<long long>(cs, HW);
     if (a.cs < 1) a.cs = 1;
     const long long slice_n = C * ((HW + a.cs - 1) / a.cs);
     const int keep = std::min(k, C);

@@ -121,6 +121,7 @@ CONV_CASES = [
     (3, 7, 3, 9, 11, 20, 3, 2, 0),        # strided, ragged tiles
     (1, 16, 5, 6, 5, 17, 4, 3, 1),        # T = TP, odd Co
     (2, 1, 2, 5, 7, 8, 2, 1, 0),          # T = 1
+    (160, 15, 2, 12, 12, 8, 5, 1, 2),     # grid >= 148 CTAs: whole sample per event CTA
 ]
 
 
@@ -287,6 +288,28 @@ def test_inhibit_and_wta_small_maps(spk, shape, ties):
         for b in range(B):
             np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
             assert (gw[b, nwin[b]:] == -1).all()
+
+
+# one C1-shaped sample (the small-grid rule: a few pixels per inhibition CTA, an 8-CTA WTA
+# cluster) and a batch large enough to keep 256 pixels per CTA and the 16K-neuron clusters
+@pytest.mark.parametrize("shape", [(1, 32, 28, 28), (2, 30, 28, 28), (160, 6, 20, 20)])
+@pytest.mark.parametrize("ties", [False, True])
+def test_inhibit_and_wta_grid_sizing(spk, shape, ties):
+    B, C, H, W = shape
+    T = 15
+    Q, lat, ps = _records(B, T, C, H, W, 0.5, ties)
+    ref = oracle.inhibit(Q)
+    rlat, rps = lat_and_pstar(ref, 0.0)
+    glat, gps = spk.inhibit(cu(lat), cu(ps.astype(np.float32)), T)
+    np.testing.assert_array_equal(host(glat), rlat)
+    np.testing.assert_array_equal(host(gps), rps.astype(np.float32))
+    for k, r in [(5, 3), (8, 1)]:
+        win, nwin = oracle.wta(ref, k, r)
+        gw, gn = spk.wta(glat, gps, T, k, r)
+        gw, gn = host(gw), host(gn)
+        np.testing.assert_array_equal(gn, nwin)
+        for b in range(B):
+            np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
 
 
 @pytest.mark.parametrize("ties", [False, True])
