@@ -3,6 +3,7 @@
 //   P:L140-149), a6 spk_inhibit, a8 spk_rstdp_route (Eq. 7),
 //   a9 spk_gather and the dense <-> latency boundary conversions.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -115,7 +116,20 @@ __global__ void __launch_bounds__(kT) pool_smem_kernel(const uint8_t* __restrict
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool p2 = g.Lh == 2 && g.Lw == 2 && g.Sh == 2 && g.Sw == 2 && g.Ph == 0 && g.Pw == 0;
     const uint32_t tt = 0x01010101u * (uint32_t)T;
-    for (int row = warp; row < np * Ho; row += kT / 32) {
+    // narrow output rows (C2 pool 2: 4 x 4 planes) would idle most lanes of a row-per-warp
+    // loop: there every thread takes whole outputs instead
+    const bool narrow = Wo < 16;
+    for (int o = narrow ? (int)threadIdx.x : n; o < n; o += kT) {
+        const int pl = o / HWo, r = o - pl * HWo, y = r / Wo, x = r - y * Wo;
+        const int y0 = y * g.Sh - g.Ph, x0 = x * g.Sw - g.Pw;
+        const int i0 = max(0, -y0), i1 = min(g.Lh, H - y0), j0 = max(0, -x0), j1 = min(g.Lw, W - x0);
+        const uint8_t* r0 = sin + pl * HW + y0 * W + x0;
+        int m = T;
+        for (int i = i0; i < i1; ++i)
+            for (int j = j0; j < j1; ++j) m = min(m, (int)r0[i * W + j]);
+        sout[o] = (uint8_t)m;
+    }
+    for (int row = warp; row < (narrow ? 0 : np * Ho); row += kT / 32) {
         const int pl = row / Ho, y = row - pl * Ho;
         const uint8_t* r0 = sin + pl * HW + (y * g.Sh - g.Ph) * W;
         uint8_t* orow = sout + row * Wo;
@@ -412,7 +426,11 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
     const size_t per_plane = (size_t)H * W + (size_t)plane_out;
     // large planes (C4, C5): whole planes through shared memory, by TMA bulk copies when
     // every run is 16-byte aligned; small planes (C1-C3, L2-resident) take the direct kernel
-    if ((long long)H * W >= 2048 && per_plane + 256 <= (size_t)kPoolSmem) {
+    static const long long smem_min = [] {  // A/B knob: smallest plane staged through smem
+        const char* e = std::getenv("SPK_POOL_SMEM_MIN");
+        return e ? std::atoll(e) : 2048ll;
+    }();
+    if ((long long)H * W >= smem_min && per_plane + 256 <= (size_t)kPoolSmem) {
         const int ppc = (int)std::min<long long>(BC, std::max<long long>(1, (24 * 1024) / (long long)per_plane));  // ~24 KB per CTA
         const size_t smem = (((size_t)ppc * H * W + 127) & ~(size_t)127) + (size_t)ppc * plane_out;
         const long long nblk = (BC + ppc - 1) / ppc;

@@ -3,7 +3,8 @@ into profiles/ncu_traffic.json from gpurun_out/<cfg>_convs.ncu-rep (launch i = c
 import csv, json, subprocess, sys
 from pathlib import Path
 
-out = Path("profiles/ncu_traffic.json")
+import os
+out = Path(os.environ.get("TRAFFIC_OUT", "profiles/ncu_traffic.json"))
 d = json.loads(out.read_text()) if out.exists() else {}
 for c in sys.argv[1:]:
     rep = Path(f"gpurun_out/{c}_convs.ncu-rep")

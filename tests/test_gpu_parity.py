@@ -234,10 +234,12 @@ def test_pool_exact(spk, L, s, p):
 
 
 # plane shapes of the large configs: C5 conv1 (16-byte rows), C4 conv1 (2-byte rows),
-# many small planes per CTA, and a plane too large for shared memory (global path)
+# many small planes per CTA, a plane too large for shared memory (global path), and
+# narrow output rows (Wo < 16: one output per thread from shared memory)
 @pytest.mark.parametrize("shape,L,s,p", [((2, 3, 224, 224), 2, 2, 0), ((1, 5, 160, 250), 2, 2, 0),
                                           ((3, 250, 14, 14), 3, 3, 0), ((1, 1, 300, 330), 2, 2, 1),
-                                          ((2, 4, 50, 45), 3, 2, 1)])
+                                          ((2, 4, 50, 45), 3, 2, 1), ((2, 3, 64, 64), 8, 8, 0),
+                                          ((2, 3, 61, 47), 5, 4, 2)])
 def test_pool_exact_large_planes(spk, shape, L, s, p):
     T = 15
     lat = RNG.integers(0, T + 1, shape).astype(np.uint8)
