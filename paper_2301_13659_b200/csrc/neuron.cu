@@ -56,6 +56,30 @@ __global__ void __launch_bounds__(kT) pool_kernel(const uint8_t* __restrict__ la
 }
 
 
+// Unpadded square windows of compile-time size L (C2 pool 2: 3x3/3): every window lies
+// inside the plane, so the L*L loads of an output are unrolled and issued together
+// instead of one dependent load per runtime loop iteration.
+template <int L>
+__global__ void __launch_bounds__(kT) pool_fixed_kernel(const uint8_t* __restrict__ lat, long long BC, int ppy, int H,
+                                                        int W, int T, int S, int Ho, int Wo,
+                                                        uint8_t* __restrict__ out) {
+    const int plane_out = Ho * Wo;
+    const int q = blockIdx.x * kT + threadIdx.x;
+    const long long bc = (long long)blockIdx.y * ppy + q / plane_out;
+    if (bc >= BC || q >= ppy * plane_out) return;
+    const int r = q % plane_out, y = r / Wo, x = r - y * Wo;
+    const uint8_t* p = lat + (size_t)bc * H * W + (size_t)(y * S) * W + x * S;
+    uint32_t v[L * L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int j = 0; j < L; ++j) v[i * L + j] = __ldg(p + (size_t)i * W + j);
+    uint32_t m = (uint32_t)T;
+#pragma unroll
+    for (int e = 0; e < L * L; ++e) m = min(m, v[e]);
+    out[(size_t)bc * plane_out + r] = (uint8_t)m;
+}
+
 // Planes that fit shared memory (every config's pooling): a CTA copies a run of
 // whole input planes — one contiguous byte range — with 16-byte loads, takes the
 // window minima from shared memory and writes its contiguous run of output planes
@@ -454,6 +478,17 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
     const long long gy = (BC + ppy - 1) / ppy;
     SPK_CHECK(gy <= 65535, SPK_ERR_SHAPE, "B*C too large");
     const dim3 grid(spk::ceil_div((size_t)ppy * plane_out, kT), (unsigned)gy);
+    static const bool fixed_ok = [] {  // A/B knob: SPK_POOL_FIXED=0 keeps the generic kernel
+        const char* e = std::getenv("SPK_POOL_FIXED");
+        return !(e && e[0] == '0');
+    }();
+    if (fixed_ok && p->Ph == 0 && p->Pw == 0 && p->Lh == p->Lw && p->Sh == p->Sw && (p->Lh == 2 || p->Lh == 3)) {
+        if (p->Lh == 2)
+            pool_fixed_kernel<2><<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, p->Sh, Ho, Wo, out);
+        else
+            pool_fixed_kernel<3><<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, p->Sh, Ho, Wo, out);
+        return spk::launched("pool_fixed_kernel");
+    }
     pool_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, *p, Ho, Wo, out);
     return spk::launched("pool_kernel");
 }
