@@ -315,13 +315,27 @@ __global__ void __launch_bounds__(kT) inhibit_small_kernel(uint8_t* __restrict__
     uint8_t* L = lat + (size_t)b * C * HW;
     float* P = pstar + (size_t)b * C * HW;
     unsigned long long best = ~0ull;
+    // four channels per trip: their latency loads (and the P* loads of those that fired)
+    // are in flight together instead of one dependent load per loop trip
     if (grp < ngrp)
-        for (int c = grp; c < C; c += ngrp) {
-            const int l = L[c * HW + p];
-            if (l >= T) continue;
-            const uint32_t pd = ~spk_float_order_u32(P[c * HW + p] + 0.0f);  // -0 -> +0: equal potentials tie on c
-            const unsigned long long key = ((unsigned long long)l << 56) | ((unsigned long long)pd << 24) | (unsigned)c;
-            best = key < best ? key : best;
+        for (int c0 = grp; c0 < C; c0 += 4 * ngrp) {
+            int l[4];
+            float pv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + u * ngrp;
+                l[u] = c < C ? (int)L[c * HW + p] : T;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pv[u] = l[u] < T ? P[(c0 + u * ngrp) * HW + p] : 0.0f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (l[u] >= T) continue;
+                const uint32_t pd = ~spk_float_order_u32(pv[u] + 0.0f);  // -0 -> +0: equal potentials tie on c
+                const unsigned long long key =
+                    ((unsigned long long)l[u] << 56) | ((unsigned long long)pd << 24) | (unsigned)(c0 + u * ngrp);
+                best = key < best ? key : best;
+            }
         }
     part[threadIdx.x] = best;
     __syncthreads();
@@ -333,11 +347,20 @@ __global__ void __launch_bounds__(kT) inhibit_small_kernel(uint8_t* __restrict__
     __syncthreads();
     if (grp < ngrp) {
         const uint32_t wc = win_c[p];
-        for (int c = grp; c < C; c += ngrp) {
-            const int o = c * HW + p;
-            if (L[o] < T && (uint32_t)c != wc) {
-                L[o] = (uint8_t)T;
-                P[o] = 0.0f;
+        for (int c0 = grp; c0 < C; c0 += 4 * ngrp) {
+            int l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + u * ngrp;
+                l[u] = c < C ? (int)L[c * HW + p] : T;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + u * ngrp;
+                if (l[u] < T && (uint32_t)c != wc) {
+                    L[c * HW + p] = (uint8_t)T;
+                    P[c * HW + p] = 0.0f;
+                }
             }
         }
     }
