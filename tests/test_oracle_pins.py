@@ -64,6 +64,39 @@ def test_gabor_closed_forms():
     np.testing.assert_allclose(g90, g0.T, atol=1e-6)
 
 
+@pytest.mark.parametrize("gamma", [0.5, 1.0, 2.0])
+@pytest.mark.parametrize("psi", [0.0, 0.4])
+def test_gabor_gamma_off_axis_closed_form(gamma, psi):
+    # at theta = 0, x' = x and y' = y, so on the column x = 0 the carrier is
+    # cos(psi) and the envelope exp(-gamma^2 y^2 / (2 sigma^2)).  This fixes gamma SQUARED on
+    # the y' term (gamma = 0.5 and 2 separate gamma from gamma^2; gamma = 1 checks the sigma),
+    # and that y runs along the kernel rows (index r + y).
+    sigma, r = 2.8, 3
+    g = oracle.gabor_kernel(sigma, 0.0, gamma, 5.0, psi, r).astype(np.float64)
+    for y in range(-r, r + 1):
+        expect = math.exp(-(gamma ** 2) * y * y / (2 * sigma ** 2)) * math.cos(psi)
+        assert abs(g[r + y, r] - expect) < 1e-6, (gamma, y)
+    # rotating by theta = pi/2 moves that column onto the row y = 0: g(x, 0) = exp(-gamma^2 x^2/2s^2) cos(psi)
+    g90 = oracle.gabor_kernel(sigma, math.pi / 2, gamma, 5.0, psi, r).astype(np.float64)
+    for x in range(-r, r + 1):
+        expect = math.exp(-(gamma ** 2) * x * x / (2 * sigma ** 2)) * math.cos(psi)
+        assert abs(g90[r, r + x] - expect) < 1e-6, (gamma, x)
+
+
+def test_log_pair_order():
+    # LoG(sigma) = (DoG(sigma*sqrt2, sigma/sqrt2), DoG(sigma/sqrt2, sigma*sqrt2)) in this
+    # order.  The first DoG subtracts the narrower Gaussian (sigma2 = sigma/sqrt2 < sigma1), so its
+    # centre is NEGATIVE (off-centre) and the second's positive (centre > 0 iff s1 < s2).
+    for s in (0.471, 1.099, 2.042):
+        k = oracle.log_kernels([s], 3)
+        assert k[0, 3, 3] < 0 < k[1, 3, 3], s
+        # the centre is the extreme of each kernel: the most negative / most positive tap
+        assert k[0, 3, 3] == k[0].min() and k[1, 3, 3] == k[1].max()
+    # list order is kept: stds [a, b] -> [pair(a), pair(b)] (R-CHORDER)
+    ka, kb = oracle.log_kernels([0.471], 3), oracle.log_kernels([2.042], 3)
+    np.testing.assert_array_equal(oracle.log_kernels([0.471, 2.042], 3), np.concatenate([ka, kb]))
+
+
 def test_log_six_channels_pairs_negate():
     # Listing 1: 3 LoG stds -> 6 channels; each pair is an exact negation.
     k = oracle.log_kernels([0.471, 1.099, 2.042], 3)
@@ -291,6 +324,28 @@ def test_inhibit_properties():
     Q[0, 1:, 1] = 5.0
     Qi = oracle.inhibit(Q)
     assert (Qi[0, :, 0] == 0).all()
+
+
+@pytest.mark.parametrize("C,survivor", [(2, 0), (3, 1), (5, 2)])
+def test_inhibit_channel_index_tie(C, survivor):
+    # R-INHIBIT-TIE: channels with the same (first-crossing step, potential at it) tie;
+    # the LOWER channel index survives, every other channel is zeroed at all steps.  Channels
+    # below `survivor` cross later (or never), channels above it tie with it exactly.
+    T = 6
+    Q = np.zeros((1, T, C, 1, 2))
+    for c in range(survivor, C):
+        Q[0, 2:, c, 0, 0] = 4.0          # cross at t=2 with P* = 4 ...
+        Q[0, 4:, c, 0, 0] = 4.0 + c       # ... and differ only after the crossing
+    for c in range(survivor):
+        Q[0, 3:, c, 0, 0] = 9.0          # later crossing, higher potential: loses on time
+    Q[0, 1:, C - 1, 0, 1] = 1.0           # the other location is untouched by location (0, 0)
+    Qi = oracle.inhibit(Q)
+    for c in range(C):
+        if c == survivor:
+            np.testing.assert_array_equal(Qi[0, :, c, 0, 0], Q[0, :, c, 0, 0])
+        else:
+            assert (Qi[0, :, c, 0, 0] == 0).all(), c
+    np.testing.assert_array_equal(Qi[0, :, :, 0, 1], Q[0, :, :, 0, 1])
 
 
 def _indep_wta(Q, count, radius):
