@@ -71,11 +71,19 @@ def _declare(L):
         "oracle_stdp": [P, I, I, I, I, I, I, I, I, P, I, I, I, I, P, P, I, P, P, I],
         "oracle_rstdp_route": [P, P, I, I, P, I],
         "oracle_gather": [P, I, I, SZ, P],
+        "oracle_rate_code": [P, I, I, I, ctypes.c_uint64, P],
+        "oracle_pool_rates": [P, P, I, I, I, I, I, I, I, I, I, I, I, P],
+        "oracle_quantize": [P, SZ, F, F, F],
+        "oracle_fc": [P, I, I, I, P, I, P],
+        "oracle_fc_stdp": [P, I, I, P, I, I, P, P, I, P, P, I],
+        "oracle_fcwta": [P, I, I, I, I, I, P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = None
+    L.oracle_splitmix64.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+    L.oracle_splitmix64.restype = ctypes.c_uint64
 
 
 def _p(a: np.ndarray):
@@ -273,3 +281,81 @@ def gather(S: np.ndarray) -> np.ndarray:
     f = np.empty((B,) + S.shape[2:], np.float32)
     lib().oracle_gather(_p(S), B, T, N, _p(f))
     return f
+
+
+# ------------------------------------------------- NEXT-3: rate coding (O14-O16)
+def splitmix64(seed: int, counter: int) -> int:
+    """Value `counter` of the counter-based stream `seed` (O14)."""
+    return int(lib().oracle_splitmix64(seed, counter))
+
+
+def rate_code(y: np.ndarray, T: int, seed: int) -> np.ndarray:
+    """Per-step Bernoulli(v / vmax) spikes of thresholded responses [B][...] -> dense
+    non-cumulative train [B][T][...]."""
+    y = _c(y, np.float32)
+    B = y.shape[0]
+    N = int(np.prod(y.shape[1:]))
+    S = np.empty((B, T) + y.shape[1:], np.uint8)
+    lib().oracle_rate_code(_p(y), B, N, T, seed, _p(S))
+    return S
+
+
+def pool_rates(S: np.ndarray, rates: np.ndarray, kernel, stride=None, pad=(0, 0)) -> np.ndarray:
+    """Rate-based max pooling: the window's highest-rate cell's whole train."""
+    S = _c(S, np.uint8)
+    rates = _c(rates, np.float32)
+    B, T, C, H, W = S.shape
+    assert rates.shape == (B, C, H, W)
+    Lh, Lw = kernel
+    Sh, Sw = stride if stride is not None else kernel
+    Ph, Pw = pad
+    Ho, Wo = (H + 2 * Ph - Lh) // Sh + 1, (W + 2 * Pw - Lw) // Sw + 1
+    out = np.empty((B, T, C, Ho, Wo), np.uint8)
+    lib().oracle_pool_rates(_p(S), _p(rates), B, T, C, H, W, Lh, Lw, Sh, Sw, Ph, Pw, _p(out))
+    return out
+
+
+# ------------------------------------------- NEXT-4: quantize, FC, fcwta (O17-O19)
+def quantize(w: np.ndarray, lower: float, mid: float, upper: float) -> np.ndarray:
+    """Listing 4 quantize(kernel, lower, mid, upper) on a copy."""
+    w = np.array(w, dtype=np.float32, order="C", copy=True)
+    lib().oracle_quantize(_p(w), w.size, lower, mid, upper)
+    return w
+
+
+def fc(S: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """Fully connected potentials: dense train [B][T][I] x W[I][O] -> fp64 [B][T][O]."""
+    S = _c(S, np.uint8)
+    W = _c(W, np.float32)
+    B, T, I_ = S.shape
+    I2, O = W.shape
+    assert I_ == I2
+    P_ = np.empty((B, T, O), np.float64)
+    lib().oracle_fc(_p(S), B, T, I_, _p(W), O, _p(P_))
+    return P_
+
+
+def fc_stdp(W: np.ndarray, S_in: np.ndarray, win, nwin, cfgs) -> np.ndarray:
+    """STDP of an FC layer (weights I x O), winners {b, t, o, 0, 0, cfg}; returns a copy."""
+    W = np.array(W, dtype=np.float32, order="C", copy=True)
+    S_in = _c(S_in, np.uint8)
+    win = _c(win, np.int32)
+    nwin = _c(nwin, np.int32)
+    I_, O = W.shape
+    B, T, I2 = S_in.shape
+    assert I2 == I_
+    cfg = _c([[c[0], c[1], c[2], c[3]] for c in cfgs], np.float32)
+    stab = _c([int(bool(c[4])) for c in cfgs], np.int32)
+    lib().oracle_fc_stdp(_p(W), I_, O, _p(S_in), B, T, _p(win), _p(nwin), win.shape[1], _p(cfg), _p(stab),
+                         len(cfgs))
+    return W
+
+
+def fcwta(Q: np.ndarray, count: int, radius: int):
+    """FC winner-take-all on thresholded potentials [B][T][O] -> (win [B][count][6], nwin [B])."""
+    Q = _c(Q, np.float64)
+    B, T, O = Q.shape
+    win = np.full((B, count, 6), -1, np.int32)
+    nwin = np.zeros(B, np.int32)
+    lib().oracle_fcwta(_p(Q), B, T, O, count, radius, _p(win), _p(nwin))
+    return win, nwin

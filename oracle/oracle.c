@@ -522,3 +522,197 @@ ORC_API void oracle_gather(const uint8_t* S, int B, int T, size_t N, float* f) {
             f[(size_t)b * N + n] = (float)cnt / (float)T;
         }
 }
+
+/* ========================================================================= */
+/* NEXT-3 / NEXT-4: rate coding, rate pooling, quantisation,   */
+/* fully connected layer and fcwta.  Same conventions as above.               */
+/* ========================================================================= */
+
+/* ------------------------------------------------------------------------- */
+/* O14  Counter-based generator for rate coding                               */
+/* ------------------------------------------------------------------------- */
+
+/* The random numbers the method draws are an input stream both sides generate
+ * from the same counter-based definition (task rule: "each side implements the
+ * same counter-based generator"): the 64-bit value number `counter` of stream
+ * `seed` is splitmix64's output for the state seed + (counter + 1) *
+ * 0x9E3779B97F4A7C15 (so seed 0, counter 0 is splitmix64's first output from
+ * state 0).  Pinned against splitmix64's published first outputs. */
+ORC_API uint64_t oracle_splitmix64(uint64_t seed, uint64_t counter) {
+    uint64_t z = seed + (counter + 1u) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* ------------------------------------------------------------------------- */
+/* O15  Rate coding ("the rate of firing is dependent on the       */
+/*      intensity of the input value ... may be modeled with a Poisson        */
+/*      distribution"; "Spyker supports rank order and rate coding")   */
+/* ------------------------------------------------------------------------- */
+
+/* Per sample b of y[B][N] (already thresholded, Listing 1): vmax = largest
+ * positive value; p_i = clamp(v_i / vmax, 0, 1) in fp32 (reading R-RATE-P); at
+ * every step t an independent Bernoulli(p_i) spike (R-RATE-BERNOULLI: discrete
+ * steps, the Poisson process of P:L109 in its per-step form): spike iff
+ * u24 * 2^-24 < p_i with u24 = the top 24 bits of value (b*T + t)*N + i of
+ * stream `seed` (O14).  Spikes are NOT cumulative.  Output: the dense BTCHW
+ * train S[B][T][N] in {0,1}.  A sample without positives never fires. */
+ORC_API void oracle_rate_code(const float* y, int B, int N, int T, uint64_t seed, uint8_t* S) {
+    for (int b = 0; b < B; ++b) {
+        const float* v = y + (size_t)b * N;
+        float vmax = 0.0f;
+        for (int i = 0; i < N; ++i)
+            if (v[i] > vmax) vmax = v[i];
+        for (int t = 0; t < T; ++t)
+            for (int i = 0; i < N; ++i) {
+                float p = 0.0f;
+                if (vmax > 0.0f && v[i] > 0.0f) {
+                    p = v[i] / vmax;
+                    if (p > 1.0f) p = 1.0f;
+                }
+                uint64_t c = ((uint64_t)b * (uint64_t)T + (uint64_t)t) * (uint64_t)N + (uint64_t)i;
+                uint32_t u24 = (uint32_t)(oracle_splitmix64(seed, c) >> 40);
+                float u = (float)u24 * 5.9604644775390625e-8f; /* 2^-24, exact */
+                S[((size_t)b * T + t) * N + i] = (uint8_t)(u < p);
+            }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* O16  Rate-based max pooling ("selects neurons that have a higher    */
+/*      firing rate when rate coding is used", `pool(array, k, s, p, rates)`) */
+/* ------------------------------------------------------------------------- */
+
+/* For every output cell (b, c, y, x) of Eq. 3's geometry: among the in-image
+ * cells of its window, the one with the largest rate[b][c][iy][ix] wins (ties:
+ * the lowest flat index iy*W + ix, reading R-RATE-POOL-TIE) and its whole
+ * spike train S[b][:][c][iy][ix] is copied to the output; a window with no
+ * in-image cell outputs no spikes (zero padding). */
+ORC_API void oracle_pool_rates(const uint8_t* S, const float* rate, int B, int T, int C, int H, int W, int Lh,
+                               int Lw, int Sh, int Sw, int Ph, int Pw, uint8_t* out) {
+    int Ho = (H + 2 * Ph - Lh) / Sh + 1, Wo = (W + 2 * Pw - Lw) / Sw + 1;
+    for (int b = 0; b < B; ++b)
+        for (int c = 0; c < C; ++c)
+            for (int y = 0; y < Ho; ++y)
+                for (int x = 0; x < Wo; ++x) {
+                    int by = -1, bx = -1;
+                    float br = 0.0f;
+                    for (int i = 0; i < Lh; ++i)
+                        for (int j = 0; j < Lw; ++j) {
+                            int iy = y * Sh - Ph + i, ix = x * Sw - Pw + j;
+                            if (iy < 0 || iy >= H || ix < 0 || ix >= W) continue;
+                            float r = rate[(((size_t)b * C + c) * H + iy) * W + ix];
+                            if (by < 0 || r > br || (r == br && iy * W + ix < by * W + bx)) {
+                                by = iy; bx = ix; br = r;
+                            }
+                        }
+                    for (int t = 0; t < T; ++t) {
+                        uint8_t s = 0;
+                        if (by >= 0) s = S[((((size_t)b * T + t) * C + c) * H + by) * W + bx];
+                        out[((((size_t)b * T + t) * C + c) * Ho + y) * Wo + x] = s;
+                    }
+                }
+}
+
+/* ------------------------------------------------------------------------- */
+/* O17  Weight quantisation (Listing 4                            */
+/*      `spyker.quantize(network.conv1.kernel, 0, 0.5, 1)`)                   */
+/* ------------------------------------------------------------------------- */
+
+/* In place: w <- lower if w < mid else upper (reading R-QUANT: the value mid
+ * itself maps to upper). */
+ORC_API void oracle_quantize(float* w, size_t n, float lower, float mid, float upper) {
+    for (size_t i = 0; i < n; ++i) w[i] = (w[i] < mid) ? lower : upper;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O18  Fully connected layer ("kernel with I x O shape ... The   */
+/*      input has B x T x I ... The output has B x T x O shape")              */
+/* ------------------------------------------------------------------------- */
+
+/* P[b][t][o] = sum_i S[b][t][i] * W[i][o], W in the paper's I x O layout,
+ * accumulated in double in i order (as O6). */
+ORC_API void oracle_fc(const uint8_t* S, int B, int T, int I, const float* W, int O, double* P) {
+    for (int b = 0; b < B; ++b)
+        for (int t = 0; t < T; ++t)
+            for (int o = 0; o < O; ++o) {
+                double acc = 0.0;
+                for (int i = 0; i < I; ++i)
+                    if (S[((size_t)b * T + t) * I + i]) acc += (double)W[(size_t)i * O + o];
+                P[((size_t)b * T + t) * O + o] = acc;
+            }
+}
+
+/* STDP of a fully connected layer (Eq. 4-6; "a function belonging to fully
+ * connected or convolution layers"): as O11 with the receptive field
+ * of output neuron o = every input i, weight W[i][o] (I x O layout). */
+ORC_API void oracle_fc_stdp(float* Wt, int I, int O, const uint8_t* S_in, int B, int T, const int32_t* win,
+                            const int32_t* nwin, int count, const float* cfg, const int32_t* stab, int ncfg) {
+    for (int b = 0; b < B; ++b)
+        for (int q = 0; q < nwin[b]; ++q) {
+            const int32_t* w = win + ((size_t)b * count + q) * 6;
+            int wb = w[0], ti = w[1], o = w[2], k = w[5];
+            if (k < 0 || k >= ncfg) continue;
+            float Ap = cfg[4 * k + 0], Am = cfg[4 * k + 1], L = cfg[4 * k + 2], U = cfg[4 * k + 3];
+            for (int i = 0; i < I; ++i) {
+                int tj = T + 1;
+                for (int t = 0; t < T; ++t)
+                    if (S_in[((size_t)wb * T + t) * I + i]) { tj = t; break; }
+                float A = (tj <= ti) ? Ap : Am;
+                float* pw = &Wt[(size_t)i * O + o];
+                float W = *pw;
+                float d;
+                if (stab[k]) {
+                    float s = (W - L) * (U - W);
+                    d = A * s;
+                } else {
+                    d = A;
+                }
+                float nw = W + d;
+                if (nw > U) nw = U;
+                if (nw < L) nw = L;
+                *pw = nw;
+            }
+        }
+}
+
+/* ------------------------------------------------------------------------- */
+/* O19  Fully connected winner-take-all (P:L198 `spyker.fcwta(array, radius,   */
+/*      count, threshold)`)                                                    */
+/* ------------------------------------------------------------------------- */
+
+/* As O10 over the output index o of thresholded FC potentials Q[B][T][O]:
+ * up to `count` greedy picks of (lat asc, potential at lat desc, o asc) among
+ * live neurons; a pick suppresses every o' with |o' - o| <= radius (reading
+ * R-FCWTA: "radius" spans output indices).  Winner {b, t, o, 0, 0, cfg=0}. */
+ORC_API void oracle_fcwta(const double* Q, int B, int T, int O, int count, int radius, int32_t* win,
+                          int32_t* nwin) {
+    uint8_t* dead = (uint8_t*)malloc(O ? O : 1);
+    int* lat = (int*)malloc(sizeof(int) * (O ? O : 1));
+    double* ps = (double*)malloc(sizeof(double) * (O ? O : 1));
+    for (int b = 0; b < B; ++b) {
+        for (int o = 0; o < O; ++o) {
+            neuron_key(Q + (size_t)b * T * O + o, T, (size_t)O, &lat[o], &ps[o]);
+            dead[o] = (uint8_t)(lat[o] >= T);
+        }
+        int got = 0;
+        for (int q = 0; q < count; ++q) {
+            int best = -1;
+            for (int o = 0; o < O; ++o) {
+                if (dead[o]) continue;
+                if (best < 0 || key_less(lat[o], ps[o], o, lat[best], ps[best], best)) best = o;
+            }
+            if (best < 0) break;
+            int32_t* w = win + ((size_t)b * count + q) * 6;
+            w[0] = b; w[1] = lat[best]; w[2] = best; w[3] = 0; w[4] = 0; w[5] = 0;
+            ++got;
+            for (int o = best - radius; o <= best + radius; ++o)
+                if (o >= 0 && o < O) dead[o] = 1;
+        }
+        nwin[b] = got;
+    }
+    free(dead);
+    free(lat);
+    free(ps);
+}

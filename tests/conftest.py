@@ -25,3 +25,12 @@ def spk():
 
     _spk.lib()  # raises if libspk.so is absent
     return _spk
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the parity report (counts of near-threshold / near-tie cases, error percentiles)
+    gathered by the GPU parity tests (tests/parity.py ParityReport)."""
+    from parity import ParityReport
+
+    path = os.environ.get("SPK_PARITY_REPORT", str(ROOT / "profiles" / "parity_report.json"))
+    ParityReport.dump(path)

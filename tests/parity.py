@@ -49,3 +49,130 @@ def lat_and_pstar(P: np.ndarray, theta: float):
     ps = np.take_along_axis(P, np.minimum(lat, T - 1)[:, None].astype(np.int64), axis=1)[:, 0]
     ps = np.where(any_, ps, 0.0)
     return lat, ps
+
+
+# ---------------------------------------------------------------------------------------
+# Parity report (SURVEY §8(c) protocol items 2 and 5; north_star "such cases are counted and
+# reported"): every GPU parity test that compares a stage adds its counts here, and the session
+# writes them to $SPK_PARITY_REPORT (default profiles/parity_report.json) — see conftest.py.
+# ---------------------------------------------------------------------------------------
+class ParityReport:
+    entries: dict = {}
+    _errs: dict = {}
+    CAP = 4_000_000  # relative errors kept per entry for the percentile (uniform subsample)
+
+    @classmethod
+    def _e(cls, key):
+        return cls.entries.setdefault(key, dict(neurons=0, near_threshold=0, mismatch_in_near_threshold=0,
+                                                mismatch_outside=0, near_ties=0, tie_decisions=0,
+                                                samples_excluded=0, potentials=0, max_rel_err=0.0,
+                                                p9999_rel_err=None))
+
+    @classmethod
+    def latency(cls, key, gpu_lat, ref_lat, excluded):
+        e = cls._e(key)
+        diff = gpu_lat != ref_lat
+        e["neurons"] += int(diff.size)
+        e["near_threshold"] += int(excluded.sum()) if excluded is not None else 0
+        if excluded is not None:
+            e["mismatch_in_near_threshold"] += int((diff & excluded).sum())
+            e["mismatch_outside"] += int((diff & ~excluded).sum())
+        else:
+            e["mismatch_outside"] += int(diff.sum())
+
+    @classmethod
+    def potentials(cls, key, gpu, ref):
+        e = cls._e(key)
+        ref = np.asarray(ref, np.float64)
+        rel = (np.abs(np.asarray(gpu, np.float64) - ref) / np.maximum(np.abs(ref), 1e-12)).ravel()
+        if rel.size == 0:
+            return
+        e["potentials"] += int(rel.size)
+        e["max_rel_err"] = max(e["max_rel_err"], float(rel.max()))
+        if rel.size > cls.CAP:
+            rel = np.random.default_rng(0).choice(rel, cls.CAP, replace=False)
+        errs = cls._errs.setdefault(key, [])
+        errs.append(rel)
+        allr = np.concatenate(errs)
+        e["p9999_rel_err"] = float(np.quantile(allr, 0.9999))
+        if allr.size > cls.CAP:
+            cls._errs[key] = [np.random.default_rng(1).choice(allr, cls.CAP, replace=False)]
+
+    @classmethod
+    def ties(cls, key, n_near, n_decisions):
+        e = cls._e(key)
+        e["near_ties"] += int(n_near)
+        e["tie_decisions"] += int(n_decisions)
+
+    @classmethod
+    def excluded_samples(cls, key, n):
+        cls._e(key)["samples_excluded"] += int(n)
+
+    @classmethod
+    def dump(cls, path):
+        import json
+        import time
+        if not cls.entries:
+            return None
+        out = {"protocol": {"REL_THR": REL_THR, "RTOL": RTOL, "ATOL": ATOL, "TIE_REL": TIE_REL,
+                            "note": "near_threshold = neurons whose oracle potential lies within REL_THR*theta of "
+                                    "theta at some step (spike-time mismatches there are counted, not failed); "
+                                    "near_ties = inhibition/WTA decisions whose two best P* (same step) lie within "
+                                    "TIE_REL relative; mismatch_outside must be 0 (the tests assert it)"},
+               "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
+               "entries": {" / ".join(k) if isinstance(k, tuple) else k: v for k, v in sorted(cls.entries.items())}}
+        with open(path, "w") as f:
+            json.dump(out, f, indent=1)
+        return path
+
+
+def _keys(Q: np.ndarray):
+    """Oracle thresholded potentials [T][C][H][W] of one sample -> (lat, P*) per neuron."""
+    T = Q.shape[0]
+    fired = Q > 0
+    anyf = fired.any(0)
+    lat = np.where(anyf, fired.argmax(0), T)
+    ps = np.take_along_axis(Q, np.minimum(lat, T - 1)[None], 0)[0]
+    return lat, np.where(anyf, ps, 0.0)
+
+
+def near_ties_inhibit(Q: np.ndarray):
+    """Inhibition decisions (locations with >= 2 firing channels) whose winner's P* is within
+    TIE_REL of another channel firing at the same step -> (near ties, decisions)."""
+    near = dec = 0
+    for b in range(Q.shape[0]):
+        lat, ps = _keys(Q[b])
+        T = Q.shape[1]
+        nf = (lat < T).sum(0)
+        m = lat.min(0)
+        for y, x in zip(*np.nonzero(nf >= 2)):
+            dec += 1
+            cand = np.sort(ps[lat[:, y, x] == m[y, x], y, x])[::-1]
+            if cand.size >= 2 and abs(cand[0] - cand[1]) <= TIE_REL * abs(cand[0]):
+                near += 1
+    return near, dec
+
+
+def near_ties_wta(Qi: np.ndarray, count: int, radius: int):
+    """k-WTA picks (R-WTA-FOOTPRINT scan, written independently of the oracle) whose P* lies
+    within TIE_REL of another live neuron of the same step -> (near ties, picks)."""
+    near = picks = 0
+    B, T, C, H, W = Qi.shape
+    for b in range(B):
+        lat, ps = _keys(Qi[b])
+        live = lat < T
+        for _ in range(count):
+            if not live.any():
+                break
+            m = lat[live].min()
+            cand = live & (lat == m)
+            best = ps[cand].max()
+            picks += 1
+            if (np.abs(ps[cand] - best) <= TIE_REL * abs(best)).sum() >= 2:
+                near += 1
+            # the oracle's pick (lowest flat index among the max-P* neurons of step m)
+            idx = np.flatnonzero((cand & (ps == best)).ravel())[0]
+            c, y, x = idx // (H * W), (idx // W) % H, idx % W
+            live[c] = False
+            live[:, max(0, y - radius):y + radius + 1, max(0, x - radius):x + radius + 1] = False
+    return near, picks

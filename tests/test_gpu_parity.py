@@ -10,7 +10,8 @@ import torch
 import oracle
 import synth
 from oracle import pipeline as opipe
-from parity import (assert_potentials, compare_latency, lat_and_pstar, near_threshold)
+from parity import (ParityReport, assert_potentials, compare_latency, lat_and_pstar, near_threshold,
+                    near_ties_inhibit, near_ties_wta)
 
 pytestmark = pytest.mark.gpu
 RNG = np.random.default_rng(2024)
@@ -145,6 +146,7 @@ def test_conv_potentials(spk, case, prec):
     _skip_unsupported(spk, lat, w, T, s, p, prec)
     ref = oracle.conv_event(lat, T, w, (s, s), (p, p))
     got = host(spk.conv(cu(lat), cu(w), T, s, p, prec=prec, epi="potential"))
+    ParityReport.potentials(("conv potentials (CONV_CASES)", prec), got, ref)
     assert_potentials(got, ref)
 
 
@@ -160,8 +162,10 @@ def test_conv_fire_epilogue(spk, case, prec):
     glat, gps = spk.conv(cu(lat), cu(w), T, s, p, prec=prec, epi="fire", theta=theta)
     glat, gps = host(glat), host(gps)
     excl = near_threshold(P, theta)
+    ParityReport.latency(("conv fire (CONV_CASES)", prec), glat, ref_lat, excl)
     compare_latency(glat, ref_lat, excl)
     ok = (glat == ref_lat) & (ref_lat < T)
+    ParityReport.potentials(("conv fire P* (CONV_CASES)", prec), gps[ok], ref_ps[ok])
     assert_potentials(gps[ok], ref_ps[ok])
     assert (gps[glat == T] == 0).all()
 
@@ -448,7 +452,7 @@ def _gpu_train(cfg, imgs, Ws, labels=None, prec="exact"):
     return net
 
 
-def _layer_out_diff(rec, L, rlat, excl, excluded, T):
+def _layer_out_diff(rec, L, rlat, excl, excluded, T, key=None):
     """GPU output of a non-trained layer vs the oracle's latencies: the latency map itself,
     or — when the layer's conv and pool run fused — the pooled map, a pooled neuron being
     excluded when a near-threshold neuron lies in its window (Eq. 3)."""
@@ -460,12 +464,16 @@ def _layer_out_diff(rec, L, rlat, excl, excluded, T):
         glat = host(rec["pooled"])
     else:
         glat = host(rec["lat"])
+    if key is not None:
+        keep = ~excluded
+        ParityReport.latency(key, glat[keep], rlat[keep], excl[keep])
     diff = (glat != rlat) & ~excluded[:, None, None, None]
     assert not (diff & ~excl).any(), "unexplained latency mismatches"
     return diff.any(axis=(1, 2, 3))
 
 
 def _check_pipeline(cfg, n, labels=False, prec="exact"):
+    name = f"{cfg['name']} train step, batch {n}, prec={prec}"
     imgs = synth.images(cfg, 0, n)
     lab = synth.labels(cfg, 0, n) if labels else None
     Ws = synth.layer_weights(cfg)
@@ -481,12 +489,20 @@ def _check_pipeline(cfg, n, labels=False, prec="exact"):
         P = oracle.conv_event(oracle.dense_to_lat(ref["inputs"][li]), T, Ws[li], (L["stride"],) * 2, (L["pad"],) * 2)
         excl = near_threshold(P, L["theta"])
         rlat, _ = lat_and_pstar(P, L["theta"])
-        excluded_samples |= _layer_out_diff(net.layers[li], L, rlat, excl, excluded_samples, T)
+        excluded_samples |= _layer_out_diff(net.layers[li], L, rlat, excl, excluded_samples, T,
+                                            key=(name, f"conv{li} fire"))
     # trained layer: (lat, P*) after inhibition, winners, weights
     L = cfg["layers"][tl]
     excl = near_threshold(ref["P"], L["theta"])
     rlat, rps = lat_and_pstar(ref["Qi"], 0.0)
     glat = host(net.layers[tl]["lat"])
+    keep = ~excluded_samples
+    ParityReport.latency((name, f"conv{tl} fire + inhibit"), glat[keep], rlat[keep], excl[keep])
+    ParityReport.ties((name, f"conv{tl} inhibit"), *near_ties_inhibit(ref["Q"]))
+    ParityReport.ties((name, f"conv{tl} wta"), *near_ties_wta(ref["Qi"], L["wta"]["count"], L["wta"]["radius"]))
+    gps = host(net.layers[tl]["pstar"])
+    okp = (glat == rlat) & (rlat < T) & keep[:, None, None, None]
+    ParityReport.potentials((name, f"conv{tl} P*"), gps[okp], rps[okp])
     diff = (glat != rlat) & ~excluded_samples[:, None, None, None]
     assert not (diff & ~excl).any(), "trained layer: unexplained mismatches after inhibition"
     excluded_samples |= diff.any(axis=(1, 2, 3))
@@ -496,6 +512,7 @@ def _check_pipeline(cfg, n, labels=False, prec="exact"):
             continue
         assert gn[b] == ref["nwin"][b]
         np.testing.assert_array_equal(gw[b, :gn[b]], ref["win"][b, :gn[b]])
+    ParityReport.excluded_samples((name, "samples"), int(excluded_samples.sum()))
     if not excluded_samples.any():
         np.testing.assert_array_equal(host(net.weights[tl]), ref["W_new"])
     else:
@@ -519,39 +536,41 @@ def test_pipeline_c3_rstdp(spk):
     assert _check_pipeline(synth.load_config("c3"), 12, labels=True) <= 1
 
 
-def test_c2_full_batch_sampled(spk):
-    """BASELINE configs[1] at full size (batch 1024), launched exactly as bench.py does
-    (CUDA graph replay): sampled images checked against the oracle one by one, the
-    STDP update checked bit-exactly with the GPU's winners teacher-forced."""
+# a 64-image parity subset of the full C2 / C3 batch, spread over the batch
+PARITY_ROWS_64 = [int(r) for r in np.linspace(0, 1023, 64)]
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_full_batch_sampled_64(spk, name):
+    """BASELINE configs[1] (C2) and configs[2] (C3, R-STDP) at full size (batch 1024), launched
+    exactly as bench.py does (auto engines, CUDA graph replay): 64 sampled images checked
+    against the oracle stage by stage (front end bit-exact; every layer, inhibition and the
+    winners outside the near-threshold set), and the STDP update of the whole batch checked
+    bit-exactly with the GPU's winners teacher-forced."""
     from paper_2301_13659_b200.network import Network
 
-    cfg = synth.load_config("c2")
-    B, T = cfg["batch"], cfg["T"]
-    imgs = synth.images(cfg, 0, B)
+    cfg = synth.load_config(name)
+    B, T, tl = cfg["batch"], cfg["T"], cfg["train_layer"]
+    imgs = synth.images_parallel(cfg, 0, B)
+    lab = synth.labels(cfg, 0, B)
     Ws = synth.layer_weights(cfg)
-    net = Network(cfg, B, prec="auto")  # bench.py's engines: event form for conv1, tcgen05 for conv2/conv3
+    net = Network(cfg, B, prec="auto")
     net.img.copy_(cu(imgs))
+    net.labels.copy_(cu(lab))
     net.set_weights([cu(w) for w in Ws])
     net.capture(warmup=1)
     net.set_weights([cu(w) for w in Ws])  # the capture warm-up ran one training step
     net.replay()
     torch.cuda.synchronize()
+    assert _check_rows_train(cfg, net, imgs, PARITY_ROWS_64, Ws, labels=lab) <= 1
     gw, gn = host(net.win), host(net.nwin)
-    lat0 = host(net.lat0)
-    for b in [0, 511, 1023]:
-        ref = opipe.train_step(cfg, imgs[b:b + 1], Ws, None, event=True)
-        np.testing.assert_array_equal(lat0[b:b + 1], ref["lat0"])
-        assert gn[b] == ref["nwin"][0]
-        got = gw[b, :gn[b]].copy()
-        got[:, 0] = 0
-        np.testing.assert_array_equal(got, ref["win"][0, :gn[b]])
-    L = cfg["layers"][2]
-    S_in = oracle.lat_to_dense(host(net.input_of(2)), T)
-    W = oracle.stdp(Ws[2], S_in, gw, gn, [tuple(c) for c in cfg["stdp"]], (1, 1), (2, 2))
-    np.testing.assert_array_equal(host(net.weights[2]), W)
+    L = cfg["layers"][tl]
+    S_in = oracle.lat_to_dense(host(net.input_of(tl)), T)
+    W = oracle.stdp(Ws[tl], S_in, gw, gn, [tuple(c) for c in cfg["stdp"]], (L["stride"],) * 2, (L["pad"],) * 2)
+    np.testing.assert_array_equal(host(net.weights[tl]), W)
 
 
-def _check_rows_train(cfg, net, imgs, rows, Ws):
+def _check_rows_train(cfg, net, imgs, rows, Ws, labels=None):
     """Rows of a full-batch GPU training step against the oracle, stage by stage and
     teacher-forced (every layer is per sample): the front end must be bit-exact; each
     layer's output must equal the oracle applied to the GPU's own input of that layer
@@ -559,6 +578,7 @@ def _check_rows_train(cfg, net, imgs, rows, Ws):
     equal the oracle's threshold -> inhibit -> convwta on the GPU's input (samples with an
     explained near-threshold mismatch in that layer are counted, not compared)."""
     T, tl = cfg["T"], cfg["train_layer"]
+    name = f"{cfg['name']} full batch {net.B} (bench launch), {len(rows)} sampled rows"
     lat0, gw, gn = host(net.lat0), host(net.win), host(net.nwin)
     excluded = 0
     for b in rows:
@@ -572,17 +592,29 @@ def _check_rows_train(cfg, net, imgs, rows, Ws):
             for key in ("lat", "pooled"):
                 if rec.get(key) is not None:
                     rec[key] = rec[key][b:b + 1]
-            _layer_out_diff(rec, L, rlat, near_threshold(P, L["theta"]), np.zeros(1, bool), T)
+            _layer_out_diff(rec, L, rlat, near_threshold(P, L["theta"]), np.zeros(1, bool), T,
+                            key=(name, f"conv{li} fire"))
         L = cfg["layers"][tl]
         P = oracle.conv_event(host(net.input_of(tl)[b:b + 1]), T, Ws[tl], (L["stride"],) * 2, (L["pad"],) * 2)
         Qi = oracle.inhibit(oracle.threshold(P, L["theta"]))
         win, nwin = oracle.wta(Qi, L["wta"]["count"], L["wta"]["radius"])
-        rlat, _ = lat_and_pstar(Qi, 0.0)
-        diff = host(net.layers[tl]["lat"][b:b + 1]) != rlat
-        assert not (diff & ~near_threshold(P, L["theta"])).any(), "trained layer: unexplained mismatches"
+        if cfg["learning"] == "rstdp":
+            win = oracle.rstdp_route(win, nwin, labels[b:b + 1], cfg["maps_per_class"])
+        rlat, rps = lat_and_pstar(Qi, 0.0)
+        glat_b = host(net.layers[tl]["lat"][b:b + 1])
+        diff = glat_b != rlat
+        excl_b = near_threshold(P, L["theta"])
+        ParityReport.latency((name, f"conv{tl} fire + inhibit"), glat_b, rlat, excl_b)
+        ParityReport.ties((name, f"conv{tl} inhibit"), *near_ties_inhibit(oracle.threshold(P, L["theta"])))
+        ParityReport.ties((name, f"conv{tl} wta"), *near_ties_wta(Qi, L["wta"]["count"], L["wta"]["radius"]))
+        gps_b = host(net.layers[tl]["pstar"][b:b + 1])
+        okp = (glat_b == rlat) & (rlat < T)
+        ParityReport.potentials((name, f"conv{tl} P*"), gps_b[okp], rps[okp])
+        assert not (diff & ~excl_b).any(), "trained layer: unexplained mismatches"
         del P, Qi
         if diff.any():
             excluded += 1
+            ParityReport.excluded_samples((name, "samples"), 1)
             continue
         assert gn[b] == nwin[0]
         got = gw[b, :gn[b]].copy()
@@ -665,6 +697,7 @@ def _check_forward(cfg, n, prec="exact"):
     net.set_weights([cu(w) for w in Ws])
     net.infer()
     torch.cuda.synchronize()
+    name = f"{cfg['name']} forward, batch {n}, prec={prec}"
     _, lat0 = opipe.front_end(cfg, imgs)
     np.testing.assert_array_equal(host(net.lat0), lat0)
     lat = lat0
@@ -674,7 +707,7 @@ def _check_forward(cfg, n, prec="exact"):
         rlat, _ = lat_and_pstar(P, L["theta"])
         excl = near_threshold(P, L["theta"])
         del P
-        excluded |= _layer_out_diff(net.layers[li], L, rlat, excl, excluded, T)
+        excluded |= _layer_out_diff(net.layers[li], L, rlat, excl, excluded, T, key=(name, f"conv{li} fire"))
         if L["pool"]:
             p = L["pool"]
             lat = oracle.dense_to_lat(oracle.pool(oracle.lat_to_dense(rlat, T), (p["kernel"],) * 2,
@@ -684,6 +717,7 @@ def _check_forward(cfg, n, prec="exact"):
             lat = rlat
     feats = oracle.gather(oracle.lat_to_dense(lat, T))
     np.testing.assert_array_equal(host(net.features)[~excluded], feats[~excluded])
+    ParityReport.excluded_samples((name, "samples"), int(excluded.sum()))
     return int(excluded.sum())
 
 
@@ -756,3 +790,104 @@ def test_data_parallel_stdp_shards_equal_whole_batch(spk, name):
     dp.enable_dp(0, n, lambda dst, src: dst.copy_(src))
     dp.train_step()
     np.testing.assert_array_equal(host(dp.weights[tl]), host(whole.weights[tl]))
+
+
+def test_data_parallel_stdp_matches_oracle_global_batch(spk):
+    """NEXT-2 (R-BATCH) against the ORACLE: two replicas forward their shards, exchange
+    winners + trained-layer inputs (Network.enable_dp with an in-process all-gather standing in
+    for NCCL), and apply one sequential update; the result equals oracle.stdp applied with the
+    oracle's own global-batch winners (bit-exact), or — when a near-threshold neuron changed a
+    sample's winners — the oracle's update with the GPU winners teacher-forced."""
+    from paper_2301_13659_b200.network import Network
+    cfg = synth.load_config("c2")
+    tl, T = cfg["train_layer"], cfg["T"]
+    L = cfg["layers"][tl]
+    n, half = 32, 16
+    imgs = synth.images(cfg, 0, n)
+    Ws = synth.layer_weights(cfg)
+    ref = opipe.train_step(cfg, imgs, Ws, None, event=True)
+    nets = []
+    for s in range(2):
+        net = Network(cfg, half, prec="auto")
+        net.img.copy_(cu(imgs[s * half:(s + 1) * half]))
+        net.set_weights([cu(w) for w in Ws])
+        nets.append(net)
+    # forward both shards with the pre-batch weights; the rank-ordered concatenation of the
+    # shards' winners and trained-layer inputs is what NCCL's all-gather hands every replica
+    for s, net in enumerate(nets):
+        net.enable_dp(s * half, n, None)
+        net.train_forward()
+        spk.winners_rebase(net.win, net.nwin, s * half)
+    g_win = torch.cat([net.win for net in nets])
+    g_nwin = torch.cat([net.nwin for net in nets])
+    g_lat = torch.cat([net.input_of(tl) for net in nets])
+    for net in nets:
+        spk.stdp(net.weights[tl], g_lat, g_win, g_nwin, None, T, L["stride"], L["pad"], ws=net.stdp_ws,
+                 cfg_arr=net.stdp_cfg)
+    w0, w1 = host(nets[0].weights[tl]), host(nets[1].weights[tl])
+    np.testing.assert_array_equal(w0, w1)  # replicas stay bit-identical with no broadcast
+    gw, gn = host(g_win), host(g_nwin)
+    bad = [b for b in range(n) if gn[b] != ref["nwin"][b] or not (gw[b, :gn[b]] == ref["win"][b, :gn[b]]).all()]
+    ParityReport.excluded_samples(("C2 data-parallel STDP (2 replicas x 16)", "samples"), len(bad))
+    assert len(bad) <= 1, f"winners differ from the oracle's global batch in samples {bad}"
+    if not bad:
+        np.testing.assert_array_equal(w0, ref["W_new"])
+    else:
+        S_in = oracle.lat_to_dense(host(g_lat), T)
+        W = oracle.stdp(Ws[tl], S_in, gw, gn, [tuple(c) for c in cfg["stdp"]], (L["stride"],) * 2, (L["pad"],) * 2)
+        np.testing.assert_array_equal(w0, W)
+
+
+def _train_outputs(net):
+    torch.cuda.synchronize()
+    outs = [host(net.lat0), host(net.win), host(net.nwin)] + [host(w) for w in net.weights]
+    for rec in net.layers:
+        for key in ("lat", "pstar", "pooled"):
+            if rec.get(key) is not None:
+                outs.append(host(rec[key]))
+    return outs
+
+
+@pytest.mark.parametrize("name,batch", [("c2", 1024), ("c3", 1024), ("c4", 8)])
+def test_run_twice_bitwise_deterministic(spk, name, batch):
+    """SURVEY §4.2 T4 / §8(b) "Determinism": the same step run twice from the same state (CUDA
+    graph replay, bench engines) gives bit-identical latencies, P*, winners and weights."""
+    from paper_2301_13659_b200.network import Network
+    cfg = synth.load_config(name)
+    imgs = synth.images_parallel(cfg, 0, batch)
+    Ws = [cu(w) for w in synth.layer_weights(cfg)]
+    net = Network(cfg, batch, prec="auto")
+    net.img.copy_(cu(imgs))
+    net.labels.copy_(cu(synth.labels(cfg, 0, batch)))
+    net.capture(warmup=1)
+    runs = []
+    for _ in range(2):
+        net.set_weights(Ws)
+        net.replay()
+        runs.append(_train_outputs(net))
+    for a, b in zip(*runs):
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,batch,shards", [("c5", 8, 2), ("c5", 12, 4), ("c2", 64, 2), ("c4", 6, 3)])
+def test_sharded_forward_bitwise_equals_whole_batch(spk, name, batch, shards):
+    """SURVEY §8(e) test: the batched forward split into contiguous image shards (rank g gets
+    parallel.shard_range) — each shard generated from its global indices and forwarded
+    separately — concatenates to exactly the whole-batch output, bit for bit."""
+    from paper_2301_13659_b200 import parallel
+    from paper_2301_13659_b200.network import Network
+    cfg = synth.load_config(name)
+    Ws = [cu(w) for w in synth.layer_weights(cfg)]
+
+    def run(start, n):
+        net = Network(cfg, n, prec="auto")
+        net.img.copy_(cu(synth.images_parallel(cfg, start, n)))
+        net.set_weights(Ws)
+        net.infer()
+        torch.cuda.synchronize()
+        return host(net.features), host(net.lat0)
+
+    whole_f, whole_l = run(0, batch)
+    parts = [run(*parallel.shard_range(batch, shards, g)) for g in range(shards)]
+    np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), whole_l)
+    np.testing.assert_array_equal(np.concatenate([p[0] for p in parts]), whole_f)
