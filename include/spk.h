@@ -57,7 +57,7 @@ typedef enum {
 SPK_API const char* spk_last_error(void);
 /* ABI version of this header (bumped on any signature change). */
 SPK_API int spk_abi_version(void);
-#define SPK_ABI_VERSION 2
+#define SPK_ABI_VERSION 3
 /* Name of the last kernel launched by this thread (diagnostics). */
 SPK_API const char* spk_last_kernel(void);
 /* Number of kernels this process launched through the library. */
@@ -165,7 +165,8 @@ SPK_API size_t spk_conv_workspace(const spk_conv_geom* g, spk_precision prec);
  *   P[b][t][o][y][x] = sum_{c,i,j} W[o][c][i][j] * [lat_in[b][c][y*Sh-Ph+i][x*Sw-Pw+j] <= t]
  * (Eq. 2; padded taps never fire), Ho = floor((Hi + 2Ph - Kh)/Sh) + 1.
  *   lat_in [dev] u8 [B][Ci][Hi][Wi] (values 0..T; > T treated as never).
- *   w      [dev] f32 [Co][Ci][Kh][Kw]; PRECONDITION 0 <= w <= w_max (weights are
+ *   w      [dev] f32 [Co][Ci][Kh][Kw], or NULL when `ws` holds the weights packed by
+ *          spk_conv_prepack (EXACT_I8 / EVENT); PRECONDITION 0 <= w <= w_max (weights are
  *          non-negative in the paper's bounded STDP, L = 0 — required for the
  *          latency map to be lossless, R-NONNEG).  EXACT_I8 clamps out-of-range
  *          weights into [0, s] and raises the device flag in the workspace
@@ -179,6 +180,15 @@ SPK_API size_t spk_conv_workspace(const spk_conv_geom* g, spk_precision prec);
 SPK_API spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_conv_geom* g,
                     spk_precision prec, spk_epilogue epi, float theta, float w_max, void* out0,
                     void* out1, void* ws, size_t ws_bytes, spk_stream stream);
+
+/* spk_conv_prepack — pack a layer's weights into `ws` once (the fixed-point digit
+ * planes of EXACT_I8 / the weight block of EVENT, as spk_conv does on every call):
+ * a later spk_conv / spk_conv_fire_pool with w == NULL, the same geometry,
+ * precision and w_max runs on the packed copy without re-packing (layers whose
+ * weights do not change between steps — every layer but the trained one).
+ * Errors: as spk_conv (SPK_ERR_ARG for FP32). */
+SPK_API spk_status spk_conv_prepack(const float* w, const spk_conv_geom* g, spk_precision prec, float w_max,
+                                    void* ws, size_t ws_bytes, spk_stream stream);
 
 /* spk_conv_fire_pool — spk_conv(FIRE) followed by spk_pool (Eq. 3) on its latency
  * map, fused (Listing 5 `fire` then `pool`): out [dev] u8 pooled lat
@@ -315,6 +325,109 @@ SPK_API spk_status spk_dense_to_lat(const uint8_t* dense, int B, int T, size_t N
  * *flag_out (host) = 1 if a weight was outside [0, s] and was clamped.
  * Synchronises `stream`. */
 SPK_API spk_status spk_conv_status(const void* ws, int* flag_out, spk_stream stream);
+
+/* ========================================================================
+ * NEXT-3  Rate coding, rate pooling, T = 300 inference (
+ *         P:L107-109)
+ * ========================================================================
+ * Rate-coded trains are NOT cumulative, so they are carried as STEP MAPS:
+ * u8 step[B][T][C][H][W] (BTCHW) with 0 where the neuron spikes at
+ * step t and 1 where it does not — one one-step latency map (T' = 1) per time
+ * step.  spk_conv / spk_conv(FIRE) / spk_pool therefore run on them unchanged
+ * with geometry B' = B*T, T' = 1: the potential of step t is the convolution
+ * of the spikes of step t (Eq. 2 "time steps independent"), fire gives the
+ * next layer's step map, and spk_pool gives the per-step window max ("no
+ * rates" pooling).  The dense spike array of P:L60 is S = 1 - step. */
+
+/* Bytes of workspace spk_rate_code needs (4 per sample). */
+SPK_API size_t spk_rate_code_workspace(int B, int N, int T);
+
+/* spk_rate_code — per sample b of y[b][0..N): v = y if y > thresh else 0
+ * (Listing 1 threshold, strict), vmax = max v; each step t independently
+ * spikes with probability p = min(1, v / vmax) (fp32 IEEE division; "the rate
+ * of firing is dependent on the intensity", "modeled with a Poisson
+ * distribution", P:L109 — per-step Bernoulli form, R-RATE-BERNOULLI):
+ * spike iff u24 * 2^-24 < p, u24 = top 24 bits of value ((b0+b)*T + t)*N + i of
+ * the counter-based stream `seed` (splitmix64 of seed + (counter+1)*0x9E3779B97F4A7C15,
+ * R-RATE-RNG); b0 = global index of sample 0, so a shard draws exactly the numbers
+ * of the same rows of the whole batch.  A sample with no value above thresh never spikes.
+ *   y [dev] f32 [B][N]; step [dev] u8 [B][T][N] (0 = spike); ws >= spk_rate_code_workspace.
+ * Errors: SPK_ERR_ARG, SPK_ERR_SHAPE, SPK_ERR_UNSUPPORTED (B or T > 65535), SPK_ERR_WORKSPACE. */
+SPK_API spk_status spk_rate_code(const float* y, int B, int N, int T, float thresh, uint64_t seed, uint64_t b0,
+                                 uint8_t* step, void* ws, size_t ws_bytes, spk_stream stream);
+
+/* spk_rate_gather — firing rate of a step map ("firing times divided
+ * by the number of time steps" in its rate form; "firing rates as
+ * output features"): rate[b][i] = #{t : step[b][t][i] == 0} / T (fp32 of the
+ * integer count / T).  step [dev] u8 [B][T][N], rate [dev] f32 [B][N]. */
+SPK_API spk_status spk_rate_gather(const uint8_t* step, int B, int T, size_t N, float* rate, spk_stream stream);
+
+/* spk_pool_rates — `spyker.pool(array, kernel, stride, pad, rates)` (P:L149:
+ * "selects neurons that have a higher firing rate when rate coding is used"):
+ * for every output cell of Eq. 3's geometry the in-image window cell with the
+ * largest rate (ties: lowest flat index y*W + x, R-RATE-POOL-TIE) is selected
+ * and its whole train copied; a window without in-image cells never spikes.
+ *   step [dev] u8 [B][T][C][H][W], rate [dev] f32 [B][C][H][W] (spk_rate_gather),
+ *   out [dev] u8 [B][T][C][Ho][Wo].  Errors: SPK_ERR_ARG, SPK_ERR_SHAPE. */
+SPK_API spk_status spk_pool_rates(const uint8_t* step, const float* rate, int B, int T, int C, int H, int W,
+                                  const spk_pool_geom* p, uint8_t* out, spk_stream stream);
+
+/* ========================================================================
+ * NEXT-4  Quantisation, fully connected layer + fcwta, ZCA (
+ *         P:L356-366)
+ * ======================================================================== */
+
+/* spk_quantize — Listing 4 `spyker.quantize(kernel, lower, mid, upper)`
+ * (P:L361): in place w = (w < mid) ? lower : upper (mid maps to upper,
+ * R-QUANT).  Binary {0, 1} weights make every potential an integer, so the
+ * EXACT_I8 conv then issues one int8 MMA per MAC (only the top digit plane is
+ * non-zero; spk_conv skips all-zero planes).  w [dev] f32 [n].
+ * Errors: SPK_ERR_ARG (null, non-finite, not lower <= mid <= upper). */
+SPK_API spk_status spk_quantize(float* w, size_t n, float lower, float mid, float upper, spk_stream stream);
+
+/* spk_fc — fully connected IF layer ("kernel with I x O shape ...
+ * input B x T x I ... output B x T x O"): the 1x1 convolution of a 1x1 map,
+ * i.e. spk_conv with geometry {B, T, Ci = I, 1, 1, Co = O, 1, 1, 1, 1, 0, 0}.
+ *   lat_in [dev] u8 [B][I] latencies; w [dev] f32 [O][I] — the paper's I x O
+ *   kernel stored output-major (its transpose, R-FC-LAYOUT) so each output
+ *   neuron's synapses are contiguous, as a conv kernel's are;
+ *   POTENTIAL: out0 f32 [B][T][O]; FIRE: out0 u8 lat [B][O], out1 f32 P* [B][O].
+ * Workspace, precisions, errors: as spk_conv.  STDP of an FC layer is spk_stdp
+ * with the same 1x1 geometry and winners {b, t, o, 0, 0, cfg} (spk_fcwta). */
+SPK_API size_t spk_fc_workspace(int B, int T, int I, int O, spk_precision prec);
+SPK_API spk_status spk_fc(const uint8_t* lat_in, const float* w, int B, int T, int I, int O, spk_precision prec,
+                          spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
+                          size_t ws_bytes, spk_stream stream);
+
+/* spk_fcwta — `spyker.fcwta(array, radius, count)`: per sample up
+ * to k greedy picks of the least key (lat asc, P* desc, o asc) among live
+ * neurons (lat < T); a pick suppresses every o' with |o' - o| <= radius
+ * (R-FCWTA).  lat [dev] u8 [B][O], pstar [dev] f32 [B][O] (spk_fc FIRE);
+ * win [dev] spk_winner [B][k] = {b, t, o, 0, 0, 0} (slots >= nwin[b]: -1),
+ * nwin [dev] i32 [B].  Errors: SPK_ERR_ARG, SPK_ERR_SHAPE,
+ * SPK_ERR_UNSUPPORTED (O >= 2^24, T > 254, O > 25600 with k > 64). */
+SPK_API spk_status spk_fcwta(const uint8_t* lat, const float* pstar, int B, int O, int T, int k, int radius,
+                             spk_winner* win, int32_t* nwin, spk_stream stream);
+
+/* spk_zca_fit — ZCA whitening fit ("fit(array, epsilon)", R-ZCA):
+ * mu = column means of x[B][F]; C = (x - mu)^T (x - mu) / (B - 1) in fp64 on
+ * the device; C = E diag(lam) E^T by a host fp64 symmetric eigensolver
+ * (Householder tridiagonalisation + implicit QL — the LAPACK symmetric route
+ * the paper names); Wz = E diag((lam + eps)^-1/2) E^T.
+ *   x [dev] f32 [B][F]; mean [dev] f32 [F]; wz [dev] f32 [F][F] (symmetric);
+ *   ws [dev] >= spk_zca_fit_workspace(B, F) bytes.
+ * SYNCHRONOUS: waits for `stream` and uses host scratch (a fit is a one-off).
+ * Errors: SPK_ERR_SHAPE (B < 2), SPK_ERR_ARG (eps < 0; eps = 0 with a singular
+ * covariance; no convergence), SPK_ERR_UNSUPPORTED (F > 8192), SPK_ERR_WORKSPACE. */
+SPK_API size_t spk_zca_fit_workspace(int B, int F);
+SPK_API spk_status spk_zca_fit(const float* x, int B, int F, double eps, float* mean, float* wz, void* ws,
+                               size_t ws_bytes, spk_stream stream);
+
+/* spk_zca_apply — the ZCA "call": y = (x - mu) Wz in fp32 (one tiled
+ * GEMM, centering fused into the operand load).  x, y [dev] f32 [B][F]
+ * (y must not alias x), mean [F], wz [F][F].  Errors: SPK_ERR_ARG, SPK_ERR_SHAPE. */
+SPK_API spk_status spk_zca_apply(const float* x, int B, int F, const float* mean, const float* wz, float* y,
+                                 spk_stream stream);
 
 #ifdef __cplusplus
 }

@@ -71,7 +71,7 @@ def _declare(L):
         "oracle_stdp": [P, I, I, I, I, I, I, I, I, P, I, I, I, I, P, P, I, P, P, I],
         "oracle_rstdp_route": [P, P, I, I, P, I],
         "oracle_gather": [P, I, I, SZ, P],
-        "oracle_rate_code": [P, I, I, I, ctypes.c_uint64, P],
+        "oracle_rate_code": [P, I, I, I, ctypes.c_uint64, ctypes.c_uint64, P],
         "oracle_pool_rates": [P, P, I, I, I, I, I, I, I, I, I, I, I, P],
         "oracle_quantize": [P, SZ, F, F, F],
         "oracle_fc": [P, I, I, I, P, I, P],
@@ -289,14 +289,14 @@ def splitmix64(seed: int, counter: int) -> int:
     return int(lib().oracle_splitmix64(seed, counter))
 
 
-def rate_code(y: np.ndarray, T: int, seed: int) -> np.ndarray:
+def rate_code(y: np.ndarray, T: int, seed: int, b0: int = 0) -> np.ndarray:
     """Per-step Bernoulli(v / vmax) spikes of thresholded responses [B][...] -> dense
-    non-cumulative train [B][T][...]."""
+    non-cumulative train [B][T][...]; b0 = global index of row 0."""
     y = _c(y, np.float32)
     B = y.shape[0]
     N = int(np.prod(y.shape[1:]))
     S = np.empty((B, T) + y.shape[1:], np.uint8)
-    lib().oracle_rate_code(_p(y), B, N, T, seed, _p(S))
+    lib().oracle_rate_code(_p(y), B, N, T, seed, b0, _p(S))
     return S
 
 

@@ -555,10 +555,11 @@ ORC_API uint64_t oracle_splitmix64(uint64_t seed, uint64_t counter) {
  * positive value; p_i = clamp(v_i / vmax, 0, 1) in fp32 (reading R-RATE-P); at
  * every step t an independent Bernoulli(p_i) spike (R-RATE-BERNOULLI: discrete
  * steps, the Poisson process of P:L109 in its per-step form): spike iff
- * u24 * 2^-24 < p_i with u24 = the top 24 bits of value (b*T + t)*N + i of
- * stream `seed` (O14).  Spikes are NOT cumulative.  Output: the dense BTCHW
+ * u24 * 2^-24 < p_i with u24 = the top 24 bits of value (g*T + t)*N + i of
+ * stream `seed` (O14), g = b0 + b the GLOBAL sample index (so a shard of a batch
+ * draws exactly the numbers of the same rows of the whole batch).  Spikes are NOT cumulative.  Output: the dense BTCHW
  * train S[B][T][N] in {0,1}.  A sample without positives never fires. */
-ORC_API void oracle_rate_code(const float* y, int B, int N, int T, uint64_t seed, uint8_t* S) {
+ORC_API void oracle_rate_code(const float* y, int B, int N, int T, uint64_t seed, uint64_t b0, uint8_t* S) {
     for (int b = 0; b < B; ++b) {
         const float* v = y + (size_t)b * N;
         float vmax = 0.0f;
@@ -571,7 +572,7 @@ ORC_API void oracle_rate_code(const float* y, int B, int N, int T, uint64_t seed
                     p = v[i] / vmax;
                     if (p > 1.0f) p = 1.0f;
                 }
-                uint64_t c = ((uint64_t)b * (uint64_t)T + (uint64_t)t) * (uint64_t)N + (uint64_t)i;
+                uint64_t c = ((b0 + (uint64_t)b) * (uint64_t)T + (uint64_t)t) * (uint64_t)N + (uint64_t)i;
                 uint32_t u24 = (uint32_t)(oracle_splitmix64(seed, c) >> 40);
                 float u = (float)u24 * 5.9604644775390625e-8f; /* 2^-24, exact */
                 S[((size_t)b * T + t) * N + i] = (uint8_t)(u < p);

@@ -100,3 +100,56 @@ def infer(cfg: dict, imgs: np.ndarray, weights, event: bool = False):
 def sig3(x: float) -> float:
     """Round to 3 significant figures (calibrated thresholds, reading R-THETA-CAL)."""
     return float(f"{x:.3g}") if x > 0 else 0.0
+
+
+# ------------------------------------------------------------------ NEXT-3 rate-coded inference
+def quantized_weights(cfg: dict, weights):
+    """Listing 4: layers with a "quantize" entry (lower, mid, upper) use
+    quantize(kernel, lower, mid, upper) of their weights."""
+    from . import quantize
+
+    out = []
+    for L, W in zip(cfg["layers"], weights):
+        q = L.get("quantize")
+        out.append(quantize(W, *q) if q else W)
+    return out
+
+
+def rate_front_end(cfg: dict, imgs: np.ndarray, start: int = 0):
+    """Listing 1 with rate coding: filter -> threshold -> rate code.
+    Returns the dense non-cumulative train [B][T][C][H][W].  `start` = global index of imgs[0]
+    (the generator's counter runs over the global sample index)."""
+    from . import rate_code
+
+    fr = cfg["front"]
+    y = threshold(filter_apply(imgs, filter_bank(cfg), fr["pad"]), fr["thresh"])
+    return rate_code(y, cfg["T"], cfg["rate_seed"], start)
+
+
+def rate_infer(cfg: dict, imgs: np.ndarray, weights, start: int = 0):
+    """Rate-coded inference: per layer conv (per step, Eq. 2) -> fire (per step,
+    P:L125) -> pool by rates or per-step max; features = firing rates.
+    Returns dict(S0, steps=[layer output trains], pooled=[...], rates=[...], features)."""
+    from . import gather, pool_rates
+
+    T = cfg["T"]
+    Ws = quantized_weights(cfg, weights)
+    S = rate_front_end(cfg, imgs, start)
+    out = dict(S0=S, steps=[], pooled=[], rates=[])
+    for li, L in enumerate(cfg["layers"]):
+        P = _conv(S, Ws[li], L, False, T)
+        Sl = fire(P, L["theta"])
+        del P
+        out["steps"].append(Sl)
+        p = L["pool"]
+        if p:
+            r = gather(Sl)
+            out["rates"].append(r)
+            if L.get("pool_rates"):
+                Sl = pool_rates(Sl, r, (p["kernel"],) * 2, (p["stride"],) * 2, (p["pad"],) * 2)
+            else:
+                Sl = pool(Sl, (p["kernel"],) * 2, (p["stride"],) * 2, (p["pad"],) * 2)
+        out["pooled"].append(Sl)
+        S = Sl
+    out["features"] = gather(S)
+    return out

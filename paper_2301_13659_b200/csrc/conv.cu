@@ -44,7 +44,7 @@ extern "C" spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_
     spk_status st = check_geom(g, Ho, Wo);
     if (st != SPK_OK) return st;
     SPK_CHECK_PTR(lat_in);
-    SPK_CHECK_PTR(w);
+    SPK_CHECK(w != nullptr || prec != SPK_PREC_FP32, SPK_ERR_ARG, "w is null (prepacked weights need EXACT_I8 or EVENT)");
     SPK_CHECK_PTR(out0);
     SPK_CHECK(epi == SPK_EPI_POTENTIAL || epi == SPK_EPI_FIRE, SPK_ERR_ARG, "unknown epilogue %d", (int)epi);
     SPK_CHECK(std::isfinite(theta) && theta >= 0.0f, SPK_ERR_ARG, "theta must be finite and >= 0");
@@ -68,6 +68,30 @@ extern "C" spk_status spk_conv(const uint8_t* lat_in, const float* w, const spk_
     return spk_conv_tc(lat_in, w, *g, p, epi, theta, w_max, out0, out1, ws, s);
 }
 
+extern "C" spk_status spk_conv_prepack(const float* w, const spk_conv_geom* g, spk_precision prec, float w_max,
+                                       void* ws, size_t ws_bytes, spk_stream stream) {
+    spk::clear_error();
+    int Ho = 0, Wo = 0;
+    spk_status st = check_geom(g, Ho, Wo);
+    if (st != SPK_OK) return st;
+    SPK_CHECK_PTR(w);
+    SPK_CHECK(std::isfinite(w_max) && w_max > 0.0f, SPK_ERR_ARG, "w_max must be finite and > 0");
+    cudaStream_t s = spk::as_cuda(stream);
+    if (prec == SPK_PREC_EVENT) {
+        EvPlan e;
+        SPK_CHECK(ev_plan(*g, e, true), SPK_ERR_UNSUPPORTED, "EVENT: weight block does not fit shared memory");
+        SPK_CHECK(ws != nullptr && ws_bytes >= e.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
+                  e.ws_bytes);
+        return spk_conv_event(nullptr, w, *g, e, SPK_EPI_FIRE, 0.0f, w_max, nullptr, nullptr, ws, s);
+    }
+    SPK_CHECK(prec == SPK_PREC_EXACT_I8, SPK_ERR_ARG, "prepacking needs EXACT_I8 or EVENT");
+    TcPlan p;
+    SPK_CHECK(tc_plan(*g, p), SPK_ERR_UNSUPPORTED, "EXACT_I8 geometry not supported");
+    SPK_CHECK(ws != nullptr && ws_bytes >= p.ws_bytes, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
+              p.ws_bytes);
+    return spk_conv_tc(nullptr, w, *g, p, SPK_EPI_FIRE, 0.0f, w_max, nullptr, nullptr, ws, s);
+}
+
 extern "C" int spk_conv_fire_pool_supported(const spk_conv_geom* g, spk_precision prec, const spk_pool_geom* pool) {
     if (!g || !pool || prec != SPK_PREC_EVENT) return 0;
     EvPlan e;
@@ -87,7 +111,6 @@ extern "C" spk_status spk_conv_fire_pool(const uint8_t* lat_in, const float* w, 
     spk_status st = check_geom(g, Ho, Wo);
     if (st != SPK_OK) return st;
     SPK_CHECK_PTR(lat_in);
-    SPK_CHECK_PTR(w);
     SPK_CHECK_PTR(pool);
     SPK_CHECK_PTR(out);
     SPK_CHECK(std::isfinite(theta) && theta >= 0.0f, SPK_ERR_ARG, "theta must be finite and >= 0");
@@ -111,6 +134,35 @@ extern "C" spk_status spk_conv_status(const void* ws, int* flag_out, spk_stream 
     if (cudaMemcpyAsync(&v, ws, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
         return spk::launched("spk_conv_status");
-    *flag_out = v;
+    *flag_out = v & 1;  // bit 0: clamped weight (bits 1-3: live digit planes, internal)
     return SPK_OK;
+}
+
+// ------------------------------------------------------------------ fully connected layer
+// "kernel with I x O shape ... input B x T x I ... output B x T x O".  An FC layer
+// is the 1x1 convolution of a 1x1 map with Ci = I input and Co = O output channels, so it runs
+// on the spk_conv engines with that geometry (weights stored output-major [O][I], R-FC-LAYOUT).
+static spk_conv_geom fc_geom(int B, int T, int I, int O) {
+    spk_conv_geom g{};
+    g.B = B;
+    g.T = T;
+    g.Ci = I;
+    g.Hi = g.Wi = 1;
+    g.Co = O;
+    g.Kh = g.Kw = 1;
+    g.Sh = g.Sw = 1;
+    g.Ph = g.Pw = 0;
+    return g;
+}
+
+extern "C" size_t spk_fc_workspace(int B, int T, int I, int O, spk_precision prec) {
+    const spk_conv_geom g = fc_geom(B, T, I, O);
+    return spk_conv_workspace(&g, prec);
+}
+
+extern "C" spk_status spk_fc(const uint8_t* lat_in, const float* w, int B, int T, int I, int O, spk_precision prec,
+                             spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
+                             size_t ws_bytes, spk_stream stream) {
+    const spk_conv_geom g = fc_geom(B, T, I, O);
+    return spk_conv(lat_in, w, &g, prec, epi, theta, w_max, out0, out1, ws, ws_bytes, stream);
 }

@@ -481,11 +481,14 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     const float inv_scale23 = (float)(8388608.0 / scale);
     int* flag = static_cast<int*>(ws);
     uint32_t* qT = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + 256);
-    if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
-    const size_t n = (size_t)p.K * p.Co_pad;
-    ev_pack_kernel<<<spk::ceil_div(n, 256), 256, 0, s>>>(w, g.Co, p.K, p.Co_pad, inv_scale23, qT, flag);
-    spk_status st = spk::launched("ev_pack_kernel");
-    if (st != SPK_OK) return st;
+    if (w) {  // w == nullptr: the workspace already holds this layer's packed weights (spk_conv_prepack)
+        if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
+        const size_t n = (size_t)p.K * p.Co_pad;
+        ev_pack_kernel<<<spk::ceil_div(n, 256), 256, 0, s>>>(w, g.Co, p.K, p.Co_pad, inv_scale23, qT, flag);
+        spk_status st = spk::launched("ev_pack_kernel");
+        if (st != SPK_OK) return st;
+    }
+    if (!lat_in) return SPK_OK;  // pack only (spk_conv_prepack)
 
     EvArgs a{};
     a.lat_in = lat_in;
@@ -512,16 +515,32 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     const long long theta_q = (long long)std::floor((double)theta * (1073741824.0 / scale));  // tensor path's
     a.th = (uint32_t)std::min<long long>(theta_q >> 7, 0xffffffffll);
     a.out_scale = (float)(scale / 1073741824.0);
-    const dim3 grid((unsigned)((p.Ho + p.rpc - 1) / p.rpc), (unsigned)p.n_mb, (unsigned)g.B);
     const bool ps = out1 != nullptr && epi == SPK_EPI_FIRE;
     a.nw = p.nw;
     const size_t smem = ev_smem(p.K, g.T, p.pch, p.band, ps, p.nw, p.MB).total;
-    if (epi == SPK_EPI_POTENTIAL)
-        return p.acc64 ? launch_ev<unsigned long long, SPK_EPI_POTENTIAL, false>(a, grid, smem, s)
-                       : launch_ev<uint32_t, SPK_EPI_POTENTIAL, false>(a, grid, smem, s);
-    if (p.acc64)
-        return ps ? launch_ev<unsigned long long, SPK_EPI_FIRE, true>(a, grid, smem, s)
-                  : launch_ev<unsigned long long, SPK_EPI_FIRE, false>(a, grid, smem, s);
-    return ps ? launch_ev<uint32_t, SPK_EPI_FIRE, true>(a, grid, smem, s)
-              : launch_ev<uint32_t, SPK_EPI_FIRE, false>(a, grid, smem, s);
+    // samples go on grid z (<= 65535 per launch): larger batches (rate-coded steps, B' = B T)
+    // run as consecutive launches over sample chunks
+    const size_t in_b = (size_t)g.Ci * g.Hi * g.Wi;
+    const size_t out_b = epi == SPK_EPI_POTENTIAL ? (size_t)g.T * g.Co * a.HWo * sizeof(float)
+                                                  : (size_t)g.Co * (a.pool ? (size_t)a.Hp * a.Wp : (size_t)a.HWo);
+    const size_t ps_b = (size_t)g.Co * a.HWo;
+    spk_status st2 = SPK_OK;
+    for (int b0 = 0; b0 < g.B && st2 == SPK_OK; b0 += 65535) {
+        EvArgs c = a;
+        c.g.B = std::min(65535, g.B - b0);
+        c.lat_in = lat_in + (size_t)b0 * in_b;
+        c.out0 = static_cast<uint8_t*>(out0) + (size_t)b0 * out_b;
+        c.out1 = a.out1 ? a.out1 + (size_t)b0 * ps_b : nullptr;
+        const dim3 grid((unsigned)((p.Ho + p.rpc - 1) / p.rpc), (unsigned)p.n_mb, (unsigned)c.g.B);
+        if (epi == SPK_EPI_POTENTIAL)
+            st2 = p.acc64 ? launch_ev<unsigned long long, SPK_EPI_POTENTIAL, false>(c, grid, smem, s)
+                          : launch_ev<uint32_t, SPK_EPI_POTENTIAL, false>(c, grid, smem, s);
+        else if (p.acc64)
+            st2 = ps ? launch_ev<unsigned long long, SPK_EPI_FIRE, true>(c, grid, smem, s)
+                     : launch_ev<unsigned long long, SPK_EPI_FIRE, false>(c, grid, smem, s);
+        else
+            st2 = ps ? launch_ev<uint32_t, SPK_EPI_FIRE, true>(c, grid, smem, s)
+                     : launch_ev<uint32_t, SPK_EPI_FIRE, false>(c, grid, smem, s);
+    }
+    return st2;
 }

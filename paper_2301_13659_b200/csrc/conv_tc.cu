@@ -88,6 +88,7 @@ __device__ long long g_trace[12][kTrace];
 struct TcArgs {
     const uint8_t* lat_in;
     const uint8_t* wpk;  // packed digit planes
+    const int* wflag;    // pack flags: bit 0 clamp, bit 1 + d = digit plane d has a non-zero digit
     void* out0;
     float* out1;
     spk_conv_geom g;
@@ -215,37 +216,28 @@ __device__ __forceinline__ void tc_stage_sep(uint32_t d0, uint32_t d1, uint32_t 
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) tc_kstep3(d0, d1, d2, a0 + 8u * kk, bdesc + inck * kk, incd, idesc, kk ? 1u : acc0);
 }
-// one k-step with planes 0-1 stacked (N = 2 Nt, accumulators d01 .. d01 + 2 Nt) and plane 2
-// alone (N = Nt): two MMAs instead of three when 3 Nt > 256 >= 2 Nt
-__device__ __forceinline__ void tc_kstep2(uint32_t d01, uint32_t d2, uint32_t a, uint64_t x0, uint64_t inc2,
-                                          uint32_t idesc01, uint32_t idesc2, uint32_t acc) {
+// One k-step of the live digit planes as one or two MMAs: MMA A covers planes [pA, pA + nA)
+// (accumulators dA, B descriptor bA, N = nA Nt in idA), MMA B (only when `two`) likewise.
+// Digit planes that are all zero for every weight of the layer are never issued (exact: they
+// would add zero) — C5's fp16-representable weights have no digit 0, binary quantized weights
+// (Listing 4) only digit 2.
+__device__ __forceinline__ void tc_kstep_gen(uint32_t dA, uint32_t dB, uint32_t a, uint64_t bA, uint64_t bB,
+                                             uint32_t idA, uint32_t idB, uint32_t acc, uint32_t two) {
     asm volatile(
-        "{\n.reg .pred p, e;\n.reg .b64 x2;\n"
+        "{\n.reg .pred p, e, q, eq;\n"
         "elect.sync _|e, 0xffffffff;\n"
-        "setp.ne.b32 p, %7, 0;\n add.s64 x2, %3, %4;\n"
+        "setp.ne.b32 p, %7, 0;\n setp.ne.b32 q, %8, 0;\n and.pred eq, e, q;\n"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%2], %3, %5, p;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%1], [%2], x2, %6, p;\n}\n" ::"r"(d01),
-        "r"(d2), "r"(a), "l"(x0), "l"(inc2), "r"(idesc01), "r"(idesc2), "r"(acc)
+        "@eq tcgen05.mma.cta_group::1.kind::i8 [%1], [%2], %4, %6, p;\n}\n" ::"r"(dA),
+        "r"(dB), "r"(a), "l"(bA), "l"(bB), "r"(idA), "r"(idB), "r"(acc), "r"(two)
         : "memory");
 }
 template <int NK>
-__device__ __forceinline__ void tc_stage_pair(uint32_t d01, uint32_t d2, uint32_t a0, uint64_t bdesc, uint64_t inck,
-                                              uint64_t inc2, uint32_t idesc01, uint32_t idesc2, uint32_t acc0) {
+__device__ __forceinline__ void tc_stage_gen(uint32_t dA, uint32_t dB, uint32_t a0, uint64_t bA, uint64_t bB,
+                                             uint64_t inck, uint32_t idA, uint32_t idB, uint32_t acc0, uint32_t two) {
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk)
-        tc_kstep2(d01, d2, a0 + 8u * kk, bdesc + inck * kk, inc2, idesc01, idesc2, kk ? 1u : acc0);
-}
-template <int NK>
-__device__ __forceinline__ void tc_stage_stacked(uint32_t d0, uint32_t a0, uint64_t bdesc, uint64_t inck,
-                                                 uint32_t idesc, uint32_t acc0) {
-#pragma unroll
-    for (int kk = 0; kk < NK; ++kk) {
-        asm volatile(
-            "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;\n"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p; }" ::"r"(d0),
-            "r"(a0 + 8u * kk), "l"(bdesc + inck * kk), "r"(idesc), "r"(kk ? 1u : acc0)
-            : "memory");
-    }
+        tc_kstep_gen(dA, dB, a0 + 8u * kk, bA + inck * kk, bB + inck * kk, idA, idB, kk ? 1u : acc0, two);
 }
 
 // K-major, no swizzle: 8-row x 16-byte core matrices; LBO = stride between the
@@ -417,6 +409,32 @@ struct RoleClock {
     __device__ void store(int) {}
 };
 #endif
+
+// MMAs of one k-step over the layer's live digit planes (pack flag bits 1..3): MMA A covers
+// planes [pA, pA + nA), MMA B (nB = 1) plane pB.  Stacked layouts (3 Nt <= 256) take the live
+// span in one MMA; otherwise (N <= 256 per MMA) planes 0-1 and plane 2 are separate MMAs.
+// Planes outside the MMAs are never written: the epilogue reads them as zero (live_cols).
+__device__ __forceinline__ void plane_plan(const TcArgs& a, uint32_t& pA, uint32_t& nA, uint32_t& pB, uint32_t& nB) {
+    uint32_t pm = a.wflag ? ((uint32_t)__ldcg(a.wflag) >> 1) & 7u : 7u;
+    if (pm == 0) pm = 4u;  // all-zero weights: one plane of zeros
+    const uint32_t lo = __ffs(pm) - 1, hi = 31 - __clz(pm);
+    pB = 0;
+    nB = 0;
+    if (a.stack == 1 || lo >= 1) {
+        pA = lo;
+        nA = hi - lo + 1;
+    } else {  // plane 0 live, 3 Nt > 256: planes 0-1 (N = 2 Nt) [+ plane 2 (N = Nt)]
+        pA = 0;
+        nA = hi >= 1 ? 2 : 1;
+        if (hi == 2) pB = 2, nB = 1;
+    }
+}
+__device__ __forceinline__ uint32_t live_planes(const TcArgs& a) {
+    if (a.stack == 0) return 7u;
+    uint32_t pA, nA, pB, nB;
+    plane_plan(a, pA, nA, pB, nB);
+    return (((1u << nA) - 1u) << pA) | (nB ? 1u << pB : 0u);
+}
 
 // ------------------------------------------------------------------ the kernel
 template <int EPI, bool PSTAR, int TP>
@@ -687,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         // output staging ring: [kNOB tiles][Nt][PPT] lat bytes, then [kNOB][Nt][PPT] P* floats
         uint8_t* ob_lat = smem + a.ob_off;
         float* ob_ps = reinterpret_cast<float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
+        const uint32_t lp = live_planes(a);  // digit planes the MMAs write (others read as 0)
         TileIter ti;
         ti.init(a);
         int buf = 0, ob = 0, ep_it = 0;
@@ -712,9 +731,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) d0[q] = d1[q] = d2[q] = (uint32_t)(n0 + q + lane);
 #else
-                tmem_ld16(tbase + n0, d0);
-                tmem_ld16(tbase + a.Nt + n0, d1);
-                tmem_ld16(tbase + 2 * a.Nt + n0, d2);
+                if (lp & 1u) tmem_ld16(tbase + n0, d0);
+                else for (int q = 0; q < 16; ++q) d0[q] = 0u;
+                if (lp & 2u) tmem_ld16(tbase + a.Nt + n0, d1);
+                else for (int q = 0; q < 16; ++q) d1[q] = 0u;
+                if (lp & 4u) tmem_ld16(tbase + 2 * a.Nt + n0, d2);
+                else for (int q = 0; q < 16; ++q) d2[q] = 0u;
                 tmem_wait_ld();
 #endif
                 const int obase = nt * a.Nt + n0;
@@ -764,9 +786,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #pragma unroll
                     for (int q = 0; q < 24; ++q) r[q] = (uint32_t)(n0 * 7 + q + lane);
 #else
-                    tmem_ld8(tbase + n0, r);
-                    tmem_ld8(tbase + a.Nt + n0, r + 8);
-                    tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
+                    if (lp & 1u) tmem_ld8(tbase + n0, r);
+                    else for (int q = 0; q < 8; ++q) r[q] = 0u;
+                    if (lp & 2u) tmem_ld8(tbase + a.Nt + n0, r + 8);
+                    else for (int q = 0; q < 8; ++q) r[8 + q] = 0u;
+                    if (lp & 4u) tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
+                    else for (int q = 0; q < 8; ++q) r[16 + q] = 0u;
 #endif
                 };
                 uint32_t mine = 0;
@@ -856,8 +881,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             auto mk_idesc = [](int n) {  // s32 D, u8 A/B, K-major, M = 128
                 return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             };
-            const uint32_t idesc = mk_idesc(a.stack == 1 ? 3 * a.Nt : a.Nt);  // N of one MMA
-            const uint32_t idesc01 = mk_idesc(2 * a.Nt);                      // planes 0-1 (stack == 2)
+            const uint32_t idesc = mk_idesc(a.Nt);  // one plane per MMA (stack == 0)
+            // live digit planes (written by the pack kernel earlier on the stream)
+            uint32_t pA, nA, pB, nB;
+            plane_plan(a, pA, nA, pB, nB);
+            const uint32_t idA = mk_idesc((int)nA * a.Nt), idB = mk_idesc(a.Nt);
             const uint32_t b_base = smem_u32(Bs);
             const uint32_t bstage = 3u * a.Nt * KS, bchunk = 3u * a.Nt * 16;  // chunk stride (LBO)
             const uint64_t d0 = smem_desc(b_base, bchunk, 128);                // descriptor template
@@ -918,16 +946,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         }                                                                     \
     }
                     if (SPK_EXP & 32) {
-                    } else if (a.stack == 2) {
-                        const uint32_t e2 = dbase + 2 * a.Nt;
-#define SPK_PAIR(n, kk) \
-    tc_stage_pair<n>(dbase, e2, at + 8u * (kk), dst + inck * (kk), inck, 2 * incd, idesc01, idesc, (kk) ? 1u : acc0)
-                        SPK_NK_DISPATCH(SPK_PAIR)
-#undef SPK_PAIR
-                    } else if (a.stack == 1) {
-#define SPK_STACKED(n, kk) tc_stage_stacked<n>(dbase, at + 8u * (kk), dst + inck * (kk), inck, idesc, (kk) ? 1u : acc0)
-                        SPK_NK_DISPATCH(SPK_STACKED)
-#undef SPK_STACKED
+                    } else if (a.stack != 0) {
+                        const uint32_t eA = dbase + pA * a.Nt, eB = dbase + pB * a.Nt;
+                        const uint64_t xA = dst + incd * pA, xB = dst + incd * pB;
+                        const uint32_t two = nB ? 1u : 0u;
+#define SPK_GEN(n, kk) \
+    tc_stage_gen<n>(eA, eB, at + 8u * (kk), xA + inck * (kk), xB + inck * (kk), inck, idA, idB, (kk) ? 1u : acc0, two)
+                        SPK_NK_DISPATCH(SPK_GEN)
+#undef SPK_GEN
                     } else {
                         const uint32_t e1 = dbase + a.Nt, e2 = dbase + 2 * a.Nt;
 #define SPK_SEP(n, kk) \
@@ -1172,11 +1198,17 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int Co, int K, 
     }
     const uint32_t qv = (uint32_t)__float2int_rn(x);  // 0 .. 2^23
     uint8_t* base = wpk + blk * 3 * per_plane + (size_t)c * 3 * Nt * 16;
+    uint32_t live = 0;  // bit 1 + d: digit d non-zero
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         const int row = d * Nt + n;
-        base[(size_t)(row >> 3) * 128 + (row & 7) * 16 + e] = (uint8_t)((qv >> (8 * d)) & 255u);
+        const uint32_t digit = (qv >> (8 * d)) & 255u;
+        base[(size_t)(row >> 3) * 128 + (row & 7) * 16 + e] = (uint8_t)digit;
+        live |= digit ? 2u << d : 0u;
     }
+    live = __reduce_or_sync(__activemask(), live);
+    // one atomic per warp, and only while it still adds a bit (the flag fills up at once)
+    if ((threadIdx.x & 31) == 0 && (live & ~(uint32_t)__ldcg(flag))) atomicOr(flag, (int)live);
 }
 
 int sm_count() {
@@ -1328,16 +1360,20 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
 
     int* flag = static_cast<int*>(ws);
     uint8_t* wpk = static_cast<uint8_t*>(ws) + 256;
-    if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
-    const size_t nthreads = (size_t)p.n_ntiles * p.nks * p.Nt * KS;
-    pack_weights_kernel<<<spk::ceil_div(nthreads, 256), 256, 0, s>>>(w, g.Co, p.K, p.Nt, p.n_ntiles, p.nks,
-                                                                    inv_scale23, wpk, flag);
-    spk_status st = spk::launched("pack_weights_kernel");
-    if (st != SPK_OK) return st;
+    if (w) {  // w == nullptr: the workspace already holds this layer's packed weights (spk_conv_prepack)
+        if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
+        const size_t nthreads = (size_t)p.n_ntiles * p.nks * p.Nt * KS;
+        pack_weights_kernel<<<spk::ceil_div(nthreads, 256), 256, 0, s>>>(w, g.Co, p.K, p.Nt, p.n_ntiles, p.nks,
+                                                                        inv_scale23, wpk, flag);
+        spk_status st = spk::launched("pack_weights_kernel");
+        if (st != SPK_OK) return st;
+    }
+    if (!lat_in) return SPK_OK;  // pack only (spk_conv_prepack)
 
     TcArgs a{};
     a.lat_in = lat_in;
     a.wpk = wpk;
+    a.wflag = flag;
     a.out0 = out0;
     a.out1 = static_cast<float*>(out1);
     a.g = g;

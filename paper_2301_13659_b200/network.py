@@ -69,6 +69,11 @@ class Network:
                        if li == tl else None),
                 ws=torch.empty(max(1, spk.conv_workspace(geom, lp)), dtype=torch.uint8, device=self.dev),
             )
+            # weight scale: the layer's bound (STDP upper bounds of the trained layer, else the init
+            # clip [0, 1]); set_weights rejects weights outside [0, w_max] (R-NONNEG)
+            rec["w_max"] = max([1.0] + [float(c[3]) for c in cfg.get("stdp") or []]) if li == tl else 1.0
+            # weights of every layer but the trained one are constant within a step: packed once
+            rec["prepacked"] = li != tl and lp in ("exact", "event")
             rec["fused_pool"] = bool(L["pool"]) and li != tl and lp == "event" and spk.conv_fire_pool_supported(
                 geom, lp, L["pool"]["kernel"], L["pool"]["stride"], L["pool"]["pad"])
             if L["pool"]:
@@ -121,8 +126,14 @@ class Network:
 
     # ------------------------------------------------------------ data in
     def set_weights(self, ws):
-        for dst, src in zip(self.weights, ws):
+        for li, (rec, dst, src) in enumerate(zip(self.layers, self.weights, ws)):
             dst.copy_(torch.as_tensor(src))
+            lo, hi = float(dst.min()), float(dst.max())
+            if lo < 0.0 or hi > rec["w_max"]:
+                raise ValueError(f"layer {li}: weights in [{lo}, {hi}] outside [0, w_max={rec['w_max']}] "
+                                 "(the latency-map conv needs non-negative weights, R-NONNEG)")
+            if rec["prepacked"]:
+                spk.conv_prepack(dst, rec["geom"], rec["prec"], rec["w_max"], rec["ws"])
 
     def input_of(self, li: int) -> torch.Tensor:
         if li == 0:
@@ -148,13 +159,13 @@ class Network:
         if rec["fused_pool"] and not pstar:  # layer output only feeds the next layer: conv + pool fused
             p = L["pool"]
             spk.conv_fire_pool(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=rec["prec"],
-                               theta=L["theta"], w_max=1.0, pool_kernel=p["kernel"], pool_stride=p["stride"],
-                               pool_pad=p["pad"], out=rec["pooled"], ws=rec["ws"])
+                               theta=L["theta"], w_max=rec["w_max"], pool_kernel=p["kernel"], pool_stride=p["stride"],
+                               pool_pad=p["pad"], out=rec["pooled"], ws=rec["ws"], prepacked=rec["prepacked"])
             mark(f"conv{li}")
             return
         spk.conv(self.input_of(li), self.weights[li], self.T, L["stride"], L["pad"], prec=rec["prec"], epi="fire",
-                 theta=L["theta"], w_max=1.0, out0=rec["lat"], out1=rec["pstar"] if pstar else None, ws=rec["ws"],
-                 want_pstar=pstar)
+                 theta=L["theta"], w_max=rec["w_max"], out0=rec["lat"], out1=rec["pstar"] if pstar else None,
+                 ws=rec["ws"], want_pstar=pstar, prepacked=rec["prepacked"])
         mark(f"conv{li}")
         if rec["pooled"] is not None and not pstar:
             p = L["pool"]
@@ -242,3 +253,125 @@ class Network:
             self.step()
         else:
             self.graph.replay()
+
+
+class RateNetwork:
+    """Rate-coded inference ("the inference is done with 300 time
+    steps and rate coding"): Listing 1 front end with rate coding instead of rank order, then per
+    layer conv -> fire on every step (Eq. 2 and P:L125 per step, spikes not cumulative) -> pool by
+    firing rates, and the last layer's firing rates as features.
+
+    Trains are step maps u8 [B][T][C][H][W] (0 = spike at that step), i.e. one-step latency maps:
+    the conv runs on B' = B*T images with T' = 1 (include/spk.h NEXT-3).  Weights of layers with a
+    "quantize" entry are quantized on the device at set_weights (Listing 4)."""
+
+    def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "auto", start: int = 0):
+        self.cfg = cfg
+        self.B = batch
+        self.T = T = cfg["T"]
+        self.start = start  # global index of sample 0 (the rate-code stream runs over global indices)
+        self.dev = torch.device(device)
+        im, fr = cfg["image"], cfg["front"]
+        self.img = torch.zeros((batch, im["C"], im["H"], im["W"]), dtype=torch.uint8, device=self.dev)
+        self.pairs = spk.log_pairs(fr["stds"]) if fr["kind"] == "log" else [tuple(p) for p in fr.get("pairs", [])]
+        K = len(self.pairs) if fr["kind"] != "gabor" else len(fr["params"])
+        e = 2 * fr["radius"] + 1
+        H, W = im["H"] + 2 * fr["pad"] - e + 1, im["W"] + 2 * fr["pad"] - e + 1
+        self.y = torch.empty((batch, im["C"] * K, H, W), dtype=torch.float32, device=self.dev)
+        self.step0 = torch.empty((batch, T, im["C"] * K, H, W), dtype=torch.uint8, device=self.dev)
+        self.rc_ws = torch.empty(max(4, 4 * batch), dtype=torch.uint8, device=self.dev)
+        self.layers, self.weights = [], []
+        ci, h, w = im["C"] * K, H, W
+        for li, L in enumerate(cfg["layers"]):
+            Ho = (h + 2 * L["pad"] - L["K"]) // L["stride"] + 1
+            Wo = (w + 2 * L["pad"] - L["K"]) // L["stride"] + 1
+            g = spk.ConvGeom(batch * T, 1, ci, h, w, L["Co"], L["K"], L["K"], L["stride"], L["stride"], L["pad"], L["pad"])
+            lp = prec
+            if prec == "auto":  # the event form where its weight block fits (sparse per-step spikes)
+                lp = "event" if spk.conv_workspace(g, "event") > 0 else "exact"
+            rec = dict(L=L, geom=g, prec=lp, Ho=Ho, Wo=Wo,
+                       step=torch.empty((batch, T, L["Co"], Ho, Wo), dtype=torch.uint8, device=self.dev),
+                       ws=torch.empty(max(1, spk.conv_workspace(g, lp)), dtype=torch.uint8, device=self.dev))
+            p = L["pool"]
+            if p:
+                Hp = (Ho + 2 * p["pad"] - p["kernel"]) // p["stride"] + 1
+                Wp = (Wo + 2 * p["pad"] - p["kernel"]) // p["stride"] + 1
+                rec["rates"] = torch.empty((batch, L["Co"], Ho, Wo), dtype=torch.float32, device=self.dev)
+                rec["pooled"] = torch.empty((batch, T, L["Co"], Hp, Wp), dtype=torch.uint8, device=self.dev)
+                h, w = Hp, Wp
+            else:
+                rec["rates"] = rec["pooled"] = None
+                h, w = Ho, Wo
+            self.layers.append(rec)
+            self.weights.append(torch.zeros((L["Co"], ci, L["K"], L["K"]), dtype=torch.float32, device=self.dev))
+            ci = L["Co"]
+        last = self.layers[-1]
+        src = last["pooled"] if last["pooled"] is not None else last["step"]
+        self.features = torch.empty((batch,) + tuple(src.shape[2:]), dtype=torch.float32, device=self.dev)
+        self.graph = None
+
+    def set_weights(self, ws):
+        for rec, dst, src in zip(self.layers, self.weights, ws):
+            L = rec["L"]
+            dst.copy_(torch.as_tensor(src))
+            if L.get("quantize"):
+                spk.quantize(dst, *L["quantize"])
+            if float(dst.min()) < 0.0 or float(dst.max()) > 1.0:
+                raise ValueError("weights outside [0, 1] (R-NONNEG)")
+            if rec["prec"] in ("exact", "event"):  # forward only: every layer packed once
+                spk.conv_prepack(dst, rec["geom"], rec["prec"], 1.0, rec["ws"])
+
+    def input_of(self, li: int) -> torch.Tensor:
+        if li == 0:
+            return self.step0
+        prev = self.layers[li - 1]
+        return prev["pooled"] if prev["pooled"] is not None else prev["step"]
+
+    def front(self, mark=_nomark):
+        fr = self.cfg["front"]
+        if fr["kind"] == "gabor":
+            spk.gabor(self.img, fr["params"], fr["radius"], fr["pad"], out=self.y)
+        else:
+            spk.dog(self.img, self.pairs, fr["radius"], fr["pad"], out=self.y)
+        mark("filter")
+        spk.rate_code(self.y, self.T, fr["thresh"], self.cfg["rate_seed"], b0=self.start, out=self.step0, ws=self.rc_ws)
+        mark("rate_code")
+
+    def layer(self, li: int, mark=_nomark):
+        rec = self.layers[li]
+        L, B, T = rec["L"], self.B, self.T
+        src = self.input_of(li)
+        x = src.view((B * T,) + tuple(src.shape[2:]))
+        out = rec["step"].view((B * T,) + tuple(rec["step"].shape[2:]))
+        spk.conv(x, self.weights[li], 1, L["stride"], L["pad"], prec=rec["prec"], epi="fire", theta=L["theta"],
+                 w_max=1.0, out0=out, ws=rec["ws"], want_pstar=False, prepacked=rec["prec"] in ("exact", "event"))
+        mark(f"conv{li}")
+        p = L["pool"]
+        if p:
+            spk.rate_gather(rec["step"], out=rec["rates"])
+            mark(f"rates{li}")
+            if L.get("pool_rates"):
+                spk.pool_rates(rec["step"], rec["rates"], p["kernel"], p["stride"], p["pad"], out=rec["pooled"])
+            else:
+                po = rec["pooled"].view((B * T,) + tuple(rec["pooled"].shape[2:]))
+                spk.pool(out, 1, p["kernel"], p["stride"], p["pad"], out=po)
+            mark(f"pool{li}")
+
+    def infer(self, mark=_nomark):
+        mark("start")
+        self.front(mark)
+        for li in range(len(self.layers)):
+            self.layer(li, mark=mark)
+        last = self.layers[-1]
+        src = last["pooled"] if last["pooled"] is not None else last["step"]
+        spk.rate_gather(src, out=self.features)
+        mark("gather")
+
+    def step(self):
+        self.infer()
+
+    def step_marked(self, mark):
+        self.infer(mark)
+
+    capture = Network.capture
+    replay = Network.replay

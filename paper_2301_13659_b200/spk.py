@@ -42,6 +42,8 @@ EXPORTS = [
     "spk_rank_code_workspace", "spk_rank_code", "spk_conv_workspace", "spk_conv", "spk_fire", "spk_pool",
     "spk_inhibit", "spk_wta", "spk_stdp_workspace", "spk_stdp", "spk_rstdp_route", "spk_winners_rebase", "spk_gather",
     "spk_lat_to_dense", "spk_dense_to_lat", "spk_conv_status", "spk_conv_fire_pool_supported", "spk_conv_fire_pool",
+    "spk_rate_code_workspace", "spk_rate_code", "spk_rate_gather", "spk_pool_rates", "spk_quantize", "spk_fc_workspace",
+    "spk_fc", "spk_fcwta", "spk_zca_fit_workspace", "spk_zca_fit", "spk_zca_apply", "spk_conv_prepack",
 ]
 
 
@@ -79,6 +81,18 @@ def lib():
             "spk_conv_status": ([V, ctypes.POINTER(I), V], I),
             "spk_conv_fire_pool_supported": ([ctypes.POINTER(ConvGeom), I, ctypes.POINTER(PoolGeom)], I),
             "spk_conv_fire_pool": ([V, V, ctypes.POINTER(ConvGeom), I, F, F, ctypes.POINTER(PoolGeom), V, V, Z, V], I),
+            "spk_rate_code_workspace": ([I, I, I], Z),
+            "spk_rate_code": ([V, I, I, I, F, U64, U64, V, V, Z, V], I),
+            "spk_rate_gather": ([V, I, I, Z, V, V], I),
+            "spk_pool_rates": ([V, V, I, I, I, I, I, ctypes.POINTER(PoolGeom), V, V], I),
+            "spk_quantize": ([V, Z, F, F, F, V], I),
+            "spk_fc_workspace": ([I, I, I, I, I], Z),
+            "spk_fc": ([V, V, I, I, I, I, I, I, F, F, V, V, V, Z, V], I),
+            "spk_fcwta": ([V, V, I, I, I, I, I, V, V, V], I),
+            "spk_zca_fit_workspace": ([I, I], Z),
+            "spk_zca_fit": ([V, I, I, ctypes.c_double, V, V, V, Z, V], I),
+            "spk_zca_apply": ([V, I, I, V, V, V, V], I),
+            "spk_conv_prepack": ([V, ctypes.POINTER(ConvGeom), I, F, V, Z, V], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -180,9 +194,10 @@ def conv_workspace(g: ConvGeom, prec: str = "exact") -> int:
 
 def conv(lat_in: torch.Tensor, w: torch.Tensor, T: int, stride=1, pad=0, prec: str = "exact",
          epi: str = "fire", theta: float = 0.0, w_max: float = 1.0, out0=None, out1=None, ws=None,
-         want_pstar: bool = True):
+         want_pstar: bool = True, prepacked: bool = False):
     """Eq. 2 potentials (epi='potential' -> f32 [B][T][Co][Ho][Wo]) or IF fire
-    (epi='fire' -> (lat u8 [B][Co][Ho][Wo], P* f32 or None))."""
+    (epi='fire' -> (lat u8 [B][Co][Ho][Wo], P* f32 or None)).  prepacked: ws holds w packed by
+    conv_prepack (w only gives the shape)."""
     g = conv_geom(lat_in, w, T, stride, pad)
     Ho, Wo = conv_out_hw(g)
     dev = lat_in.device
@@ -195,9 +210,17 @@ def conv(lat_in: torch.Tensor, w: torch.Tensor, T: int, stride=1, pad=0, prec: s
     if ws is None and need:
         ws = torch.empty(need, dtype=torch.uint8, device=dev)
     nbytes = ws.numel() if ws is not None else 0
-    _check("spk_conv", lib().spk_conv(_p(lat_in), _p(w), ctypes.byref(g), SPK_PREC[prec], SPK_EPI[epi],
+    _check("spk_conv", lib().spk_conv(_p(lat_in), None if prepacked else _p(w), ctypes.byref(g), SPK_PREC[prec],
+                                      SPK_EPI[epi],
                                       float(theta), float(w_max), _p(out0), _p(out1), _p(ws), nbytes, _s()))
     return out0 if epi == "potential" else (out0, out1)
+
+
+def conv_prepack(w: torch.Tensor, g: ConvGeom, prec: str, w_max: float, ws: torch.Tensor):
+    """Pack a layer's weights into ws once; later conv()/conv_fire_pool() calls pass w=None."""
+    _check("spk_conv_prepack", lib().spk_conv_prepack(_p(w), ctypes.byref(g), SPK_PREC[prec], float(w_max), _p(ws),
+                                                      ws.numel(), _s()))
+    return ws
 
 
 def conv_clamp_flag(ws: torch.Tensor) -> int:
@@ -246,7 +269,7 @@ def conv_fire_pool_supported(g: ConvGeom, prec: str, kernel, stride=None, pad=0)
 
 def conv_fire_pool(lat_in: torch.Tensor, w: torch.Tensor, T: int, stride=1, pad=0, prec: str = "event",
                    theta: float = 0.0, w_max: float = 1.0, pool_kernel=2, pool_stride=None, pool_pad=0,
-                   out=None, ws=None) -> torch.Tensor:
+                   out=None, ws=None, prepacked: bool = False) -> torch.Tensor:
     """spk_conv(FIRE) + spk_pool fused: pooled latencies [B][Co][Hp][Wp]."""
     g = conv_geom(lat_in, w, T, stride, pad)
     Ho, Wo = conv_out_hw(g)
@@ -258,7 +281,8 @@ def conv_fire_pool(lat_in: torch.Tensor, w: torch.Tensor, T: int, stride=1, pad=
     if ws is None and need:
         ws = torch.empty(need, dtype=torch.uint8, device=lat_in.device)
     nbytes = ws.numel() if ws is not None else 0
-    _check("spk_conv_fire_pool", lib().spk_conv_fire_pool(_p(lat_in), _p(w), ctypes.byref(g), SPK_PREC[prec],
+    _check("spk_conv_fire_pool", lib().spk_conv_fire_pool(_p(lat_in), None if prepacked else _p(w), ctypes.byref(g),
+                                                          SPK_PREC[prec],
                                                           float(theta), float(w_max), ctypes.byref(pg), _p(out),
                                                           _p(ws), nbytes, _s()))
     return out
@@ -343,3 +367,108 @@ def dense_to_lat(dense: torch.Tensor):
     bad = torch.empty((1,), dtype=torch.int32, device=dense.device)
     _check("spk_dense_to_lat", lib().spk_dense_to_lat(_p(dense), B, T, N, _p(lat), _p(bad), _s()))
     return lat, bad
+
+
+# ---------------------------------------------------------------- NEXT-3 rate coding
+def rate_code(y: torch.Tensor, T: int, thresh: float, seed: int, b0: int = 0, out=None, ws=None) -> torch.Tensor:
+    """Per-step Bernoulli rate coding -> step map u8 [B][T][...] (0 = spike at that step); b0 = global
+    index of sample 0 (the random stream runs over global sample indices)."""
+    B = y.shape[0]
+    N = y[0].numel()
+    if out is None:
+        out = torch.empty((B, T) + tuple(y.shape[1:]), dtype=torch.uint8, device=y.device)
+    if ws is None:
+        ws = torch.empty(int(lib().spk_rate_code_workspace(B, N, T)), dtype=torch.uint8, device=y.device)
+    _check("spk_rate_code", lib().spk_rate_code(_p(y), B, N, T, float(thresh), int(seed) & (2 ** 64 - 1), int(b0), _p(out),
+                                                _p(ws), ws.numel(), _s()))
+    return out
+
+
+def rate_gather(step: torch.Tensor, out=None) -> torch.Tensor:
+    """Firing rate (spikes / T) of a step map [B][T][...] -> f32 [B][...]."""
+    B, T = step.shape[:2]
+    N = step[0, 0].numel()
+    if out is None:
+        out = torch.empty((B,) + tuple(step.shape[2:]), dtype=torch.float32, device=step.device)
+    _check("spk_rate_gather", lib().spk_rate_gather(_p(step), B, T, N, _p(out), _s()))
+    return out
+
+
+def pool_rates(step: torch.Tensor, rate: torch.Tensor, kernel, stride=None, pad=0, out=None) -> torch.Tensor:
+    """Rate-based max pooling of a step map [B][T][C][H][W] with rates [B][C][H][W]."""
+    B, T, C, H, W = step.shape
+    pg = _pool_geom(kernel, stride, pad)
+    Ho, Wo = (H + 2 * pg.Ph - pg.Lh) // pg.Sh + 1, (W + 2 * pg.Pw - pg.Lw) // pg.Sw + 1
+    if out is None:
+        out = torch.empty((B, T, C, Ho, Wo), dtype=torch.uint8, device=step.device)
+    _check("spk_pool_rates", lib().spk_pool_rates(_p(step), _p(rate), B, T, C, H, W, ctypes.byref(pg), _p(out), _s()))
+    return out
+
+
+# ---------------------------------------------------------------- NEXT-4 quantize, FC, fcwta, ZCA
+def quantize(w: torch.Tensor, lower: float, mid: float, upper: float) -> torch.Tensor:
+    """Listing 4 quantize(kernel, lower, mid, upper), in place."""
+    _check("spk_quantize", lib().spk_quantize(_p(w), w.numel(), float(lower), float(mid), float(upper), _s()))
+    return w
+
+
+def fc_workspace(B: int, T: int, I: int, O: int, prec: str = "exact") -> int:
+    return int(lib().spk_fc_workspace(B, T, I, O, SPK_PREC[prec]))
+
+
+def fc(lat_in: torch.Tensor, w: torch.Tensor, T: int, prec: str = "exact", epi: str = "fire", theta: float = 0.0,
+       w_max: float = 1.0, out0=None, out1=None, ws=None, want_pstar: bool = True):
+    """FC IF layer: lat_in u8 [B][I], w f32 [O][I] (the paper's I x O kernel, output-major)."""
+    B, I = lat_in.shape
+    O, I2 = w.shape
+    if I != I2:
+        raise SpkError(f"FC input size mismatch {I} vs {I2}")
+    dev = lat_in.device
+    if out0 is None:
+        out0 = (torch.empty((B, T, O), dtype=torch.float32, device=dev) if epi == "potential"
+                else torch.empty((B, O), dtype=torch.uint8, device=dev))
+    if epi == "fire" and want_pstar and out1 is None:
+        out1 = torch.empty((B, O), dtype=torch.float32, device=dev)
+    need = fc_workspace(B, T, I, O, prec)
+    if ws is None and need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    nbytes = ws.numel() if ws is not None else 0
+    _check("spk_fc", lib().spk_fc(_p(lat_in), _p(w), B, T, I, O, SPK_PREC[prec], SPK_EPI[epi], float(theta),
+                                  float(w_max), _p(out0), _p(out1), _p(ws), nbytes, _s()))
+    return out0 if epi == "potential" else (out0, out1)
+
+
+def fcwta(lat: torch.Tensor, pstar: torch.Tensor, T: int, k: int, radius: int, win=None, nwin=None):
+    B, O = lat.shape
+    if win is None:
+        win = torch.empty((B, k, 6), dtype=torch.int32, device=lat.device)
+    if nwin is None:
+        nwin = torch.empty((B,), dtype=torch.int32, device=lat.device)
+    _check("spk_fcwta", lib().spk_fcwta(_p(lat), _p(pstar), B, O, T, k, radius, _p(win), _p(nwin), _s()))
+    return win, nwin
+
+
+def fc_stdp(w: torch.Tensor, lat_in: torch.Tensor, win: torch.Tensor, nwin: torch.Tensor, cfgs, T: int, ws=None,
+            cfg_arr=None):
+    """STDP of an FC layer (w [O][I]) = spk_stdp on the 1x1 geometry."""
+    B, I = lat_in.shape
+    return stdp(w.view(w.shape[0], I, 1, 1), lat_in.view(B, I, 1, 1), win, nwin, cfgs, T, 1, 0, ws=ws,
+                cfg_arr=cfg_arr)
+
+
+def zca_fit(x: torch.Tensor, eps: float):
+    """ZCA fit (synchronous): x f32 [B][F] -> (mean [F], Wz [F][F])."""
+    B, F = x.shape
+    mean = torch.empty((F,), dtype=torch.float32, device=x.device)
+    wz = torch.empty((F, F), dtype=torch.float32, device=x.device)
+    ws = torch.empty(int(lib().spk_zca_fit_workspace(B, F)), dtype=torch.uint8, device=x.device)
+    _check("spk_zca_fit", lib().spk_zca_fit(_p(x), B, F, float(eps), _p(mean), _p(wz), _p(ws), ws.numel(), _s()))
+    return mean, wz
+
+
+def zca_apply(x: torch.Tensor, mean: torch.Tensor, wz: torch.Tensor, out=None) -> torch.Tensor:
+    B, F = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    _check("spk_zca_apply", lib().spk_zca_apply(_p(x), B, F, _p(mean), _p(wz), _p(out), _s()))
+    return out

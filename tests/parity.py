@@ -65,8 +65,8 @@ class ParityReport:
     def _e(cls, key):
         return cls.entries.setdefault(key, dict(neurons=0, near_threshold=0, mismatch_in_near_threshold=0,
                                                 mismatch_outside=0, near_ties=0, tie_decisions=0,
-                                                samples_excluded=0, potentials=0, max_rel_err=0.0,
-                                                p9999_rel_err=None))
+                                                samples_excluded=0, potentials=0, max_abs_err=0.0,
+                                                max_rel_err=0.0, p9999_rel_err=None))
 
     @classmethod
     def latency(cls, key, gpu_lat, ref_lat, excluded):
@@ -83,11 +83,18 @@ class ParityReport:
     @classmethod
     def potentials(cls, key, gpu, ref):
         e = cls._e(key)
-        ref = np.asarray(ref, np.float64)
-        rel = (np.abs(np.asarray(gpu, np.float64) - ref) / np.maximum(np.abs(ref), 1e-12)).ravel()
+        ref = np.asarray(ref, np.float64).ravel()
+        err = np.abs(np.asarray(gpu, np.float64).ravel() - ref)
+        if err.size == 0:
+            return
+        e["potentials"] += int(err.size)
+        e["max_abs_err"] = max(e["max_abs_err"], float(err.max()))
+        # relative errors over potentials of at least 1e-3 (a weight sum; smaller ones are
+        # covered by the absolute term ATOL of the protocol)
+        big = np.abs(ref) >= 1e-3
+        rel = err[big] / np.abs(ref[big])
         if rel.size == 0:
             return
-        e["potentials"] += int(rel.size)
         e["max_rel_err"] = max(e["max_rel_err"], float(rel.max()))
         if rel.size > cls.CAP:
             rel = np.random.default_rng(0).choice(rel, cls.CAP, replace=False)

@@ -682,8 +682,20 @@ def test_c5_full_batch_sampled(spk):
 
 
 def test_pipeline_c4_train_t30(spk):
-    """Caltech-shaped C4 (Gabor front end, T = 30 -> 32-row time tiles), layer-2 training step, 1 image."""
-    assert _check_pipeline(synth.load_config("c4"), 1) <= 1
+    """Caltech-shaped C4 (Gabor front end, T = 30 -> 32-row time tiles), layer-2 training step on
+    2 images: end to end, then stage by stage with each layer teacher-forced on the GPU's own
+    input (so a near-threshold flip in conv0 does not hide the trained layer from the check)."""
+    from paper_2301_13659_b200.network import Network
+    cfg = synth.load_config("c4")
+    assert _check_pipeline(cfg, 2) <= 2
+    imgs = synth.images(cfg, 0, 2)
+    Ws = synth.layer_weights(cfg)
+    net = Network(cfg, 2, prec="exact")
+    net.img.copy_(cu(imgs))
+    net.set_weights([cu(w) for w in Ws])
+    net.train_step()
+    torch.cuda.synchronize()
+    assert _check_rows_train(cfg, net, imgs, [0, 1], Ws) <= 1
 
 
 def _check_forward(cfg, n, prec="exact"):

@@ -75,6 +75,8 @@ def test_rate_code_per_sample_and_scale_invariant():
     S2 = oracle.rate_code(y2, 50, seed=3)
     np.testing.assert_array_equal(S2, S)
     assert oracle.rate_code(np.zeros((1, 9), np.float32), 20, 1).sum() == 0
+    # a shard coded with its global base row draws exactly the whole batch's numbers
+    np.testing.assert_array_equal(oracle.rate_code(y[1:], 50, seed=3, b0=1), S[1:])
 
 
 # --------------------------------------------------------------- O16 rate pooling
