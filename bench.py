@@ -6,11 +6,18 @@ One step = one pass of the whole hot path over one batch: for configs[1] (C2,
 the default) the layer-3 training step of the 3-layer STDP SDNN at batch 1024,
 T = 15: DoG/LoG filter -> rank-order code -> conv1+fire -> pool -> conv2+fire ->
 pool -> conv3+fire record -> lateral inhibition -> k-WTA -> STDP (in place).
-Under torchrun every rank trains its own replica on its own images (STDP is
-sample-sequential): weak scaling, no data-path
-collective.  Timing: CUDA events on the launching stream around each replayed
-CUDA graph, L2 flushed (256 MiB write) between timed steps, max over ranks.
-Prints one JSON line on rank 0.
+With --gpus N > 1 (and no torchrun around it) the script relaunches itself under
+torch.distributed.run with N ranks on 127.0.0.1.  Training configs at N > 1 run
+the data-parallel mini-batch STDP of SURVEY NEXT-2 by default (one model, global
+batch N x B, winners + trained-layer inputs all-gathered over NCCL, identical
+update on every rank; --replicas trains N independent replicas instead);
+forward configs (C5, C6) shard the global batch.  Timing: CUDA events on the
+launching stream around each replayed CUDA graph, L2 flushed (256 MiB write)
+between timed steps, max over ranks.  Prints one JSON line on rank 0.
+
+Workloads: --config c2 (default, BASELINE configs[1]), c1, c3, c4, c5 (the other
+BASELINE configs), c2q (Listing 4: layers 1-2 quantized to {0,1}, NEXT-4), c6
+(rate-coded T=300 inference, NEXT-3).
 """
 from __future__ import annotations
 
@@ -42,8 +49,10 @@ def parse():
     ap.add_argument("--prec", default="auto", choices=["auto", "exact", "event", "fp32"],
                     help="conv engine: auto = event form for small-N layers, tcgen05 otherwise (bit-identical)")
     ap.add_argument("--dp", action="store_true",
-                    help="training configs under torchrun: one model, data-parallel mini-batch STDP (SURVEY NEXT-2): "
+                    help="data-parallel mini-batch STDP (SURVEY NEXT-2) also at N = 1 (the default at N > 1): "
                          "per-GPU batch fixed, winners + input maps all-gathered, same update on every rank")
+    ap.add_argument("--replicas", action="store_true",
+                    help="training configs at N > 1: N independent replicas instead of one data-parallel model")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8, help="images in the oracle cpu_baseline sample")
     return ap.parse_args()
@@ -112,35 +121,53 @@ def event_adds(net, li):
 SMEM_WORDS_PER_CLK_SM = 32  # 128 B/clk/SM shared-memory bandwidth / 4-byte weight per add
 
 
+def _oracle_step(cfg, imgs, Ws, lab, start):
+    """One step of the plain oracle on `imgs` (global indices start..)."""
+    from oracle import pipeline as opipe
+
+    if cfg.get("coding") == "rate":
+        return opipe.rate_infer(cfg, imgs, Ws, start)
+    if cfg["timed"] == "train":
+        return opipe.train_step(cfg, imgs, Ws, lab)
+    return opipe.infer(cfg, imgs, Ws)
+
+
 def cpu_baseline(cfg, n_images):
     """The oracle as it stands (oracle/, single thread) on a bounded sample of the same workload."""
     import oracle
     import synth
-    from oracle import pipeline as opipe
 
     imgs = synth.images(cfg, 0, n_images)
     lab = synth.labels(cfg, 0, n_images)
     Ws = synth.layer_weights(cfg)
     oracle.lib()
     t0 = time.perf_counter()
-    if cfg["timed"] == "train":
-        opipe.train_step(cfg, imgs, Ws, lab)
-    else:
-        opipe.infer(cfg, imgs, Ws)
+    _oracle_step(cfg, imgs, Ws, lab, 0)
     dt = time.perf_counter() - t0
-    return {"value": n_images / dt, "unit": "images/s", "cores": 1, "kind": "oracle",
+    return {"value": n_images / dt, "unit": "images/s", "cores": 1, "kind": "oracle", **host_info(),
             "sample": f"{n_images} images of {cfg['name']} (global indices 0..{n_images - 1}), one full "
                       f"{cfg['timed']} step of the plain oracle (direct Eq. 2), 1 host thread, {dt:.1f} s"}
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per_step = max(1, args.cpu_sample // 4)
+    per_step = max(1, args.cpu_sample // (8 if cfg.get("coding") == "rate" else 4))
     import oracle
     import synth
-    from oracle import pipeline as opipe
 
     oracle.lib()
     Ws = synth.layer_weights(cfg)
@@ -149,11 +176,9 @@ def run_reference(args, cfg):
         imgs = synth.images(cfg, s * per_step, per_step)
         lab = synth.labels(cfg, s * per_step, per_step)
         t0 = time.perf_counter()
+        r = _oracle_step(cfg, imgs, Ws, lab, s * per_step)
         if cfg["timed"] == "train":
-            r = opipe.train_step(cfg, imgs, Ws, lab)
             Ws[cfg["train_layer"]] = r["W_new"]
-        else:
-            opipe.infer(cfg, imgs, Ws)
         if s >= args.warmup:
             times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
@@ -165,9 +190,56 @@ def run_reference(args, cfg):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg['name']}: {cfg['about']}", "global_batch": per_step, "T": cfg["T"],
                    "parallelism": "cpu oracle, rank 0 only"},
-        "cpu_baseline": {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         **host_info()},
         "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def relaunch(args):
+    """--gpus N > 1 without a launcher: run this script under torch.distributed.run, N ranks."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def stage_bytes(net, cfg, B):
+    """Algorithmic HBM bytes of each bandwidth stage of one step (natural compact
+    I/O types, no re-reads): the numerators of the per-stage HBM fractions."""
+    T = cfg["T"]
+    out = {}
+    fr = cfg["front"]
+    img = B * cfg["image"]["C"] * cfg["image"]["H"] * cfg["image"]["W"]
+    y = net.y.numel()
+    out["filter"] = img + 4 * y
+    if cfg.get("coding") == "rate":
+        out["rate_code"] = 4 * y + T * y  # f32 response in, one step-map byte per (t, neuron) out
+        for li, rec in enumerate(net.layers):
+            if rec["rates"] is not None:
+                out[f"rates{li}"] = rec["step"].numel() + 4 * rec["rates"].numel()
+                out[f"pool{li}"] = 4 * rec["rates"].numel() + 2 * rec["pooled"].numel()
+        last = net.layers[-1]
+        src = last["pooled"] if last["pooled"] is not None else last["step"]
+        out["gather"] = src.numel() + 4 * net.features.numel()
+        return out
+    out["rank_code"] = 5 * y
+    for li, rec in enumerate(net.layers):
+        if rec.get("pooled") is not None and not rec.get("fused_pool"):
+            out[f"pool{li}"] = rec["lat"].numel() + rec["pooled"].numel()
+    tl = cfg.get("train_layer")
+    if tl is not None and cfg["timed"] == "train":
+        n = net.layers[tl]["lat"].numel()
+        out["inhibit"] = 10 * n
+        out["wta"] = 5 * n + 24 * net.k * B
+    else:
+        out["gather"] = 5 * net.features.numel()
+    return out
 
 
 def main():
@@ -177,43 +249,57 @@ def main():
     cfg = synth.load_config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
 
     import torch
     import torch.distributed as dist
 
     from paper_2301_13659_b200 import spk
-    from paper_2301_13659_b200.network import Network
+    from paper_2301_13659_b200.network import Network, RateNetwork
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)  # communicator up before timing
+        print(f"bench.py rank {rank}/{world}: NCCL communicator initialised on cuda:{local} "
+              f"({torch.cuda.get_device_name(dev)}), all_reduce check {int(t.item())} == {world}",
+              file=sys.stderr, flush=True)
 
     from paper_2301_13659_b200 import parallel
 
     T = cfg["T"]
+    rate = cfg.get("coding") == "rate"
     forward = cfg["timed"] == "forward"
     if forward:
         # sharded batched forward: the global batch is split across ranks (strong scaling)
         start, B = parallel.shard_range(cfg["batch"], world, rank)
     else:
-        # training replicas: every rank trains its own replica on its own batch (weak scaling)
+        # training: per-GPU batch fixed (weak scaling); data-parallel by default at N > 1
         B = cfg["batch"]
         start = rank * B
     imgs = synth.images_parallel(cfg, start, B)
     labels = synth.labels(cfg, start, B)
     Ws = synth.layer_weights(cfg)
-    net = Network(cfg, B, device=dev, prec=args.prec)
-    dp = args.dp and not forward
+    if rate:
+        net = RateNetwork(cfg, B, device=dev, prec=args.prec, start=start)
+    else:
+        net = Network(cfg, B, device=dev, prec=args.prec)
+    dp = (not forward) and (args.dp or (world > 1 and not args.replicas))
     if dp:
         net.enable_dp(start, B * world, parallel.allgather_equal)
     # NCCL collectives stay outside CUDA graphs: a data-parallel step at N > 1 runs eagerly
     use_graph = not (dp and world > 1)
     net.img.copy_(torch.from_numpy(imgs))
-    net.labels.copy_(torch.from_numpy(labels))
+    if hasattr(net, "labels"):
+        net.labels.copy_(torch.from_numpy(labels))
     net.set_weights([torch.from_numpy(w) for w in Ws])
     stream = torch.cuda.current_stream(dev)
     bcast_ms = 0.0
@@ -226,8 +312,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         bcast_ms = e0.elapsed_time(e1)
+        net.set_weights([w.clone() for w in net.weights])  # re-pack the broadcast weights
 
-    # kernels per step (counted at the ABI) and a per-stage profile of one un-graphed step
+    # kernels per step (counted at the ABI)
     n0 = spk.launch_count()
     net.step()
     torch.cuda.synchronize()
@@ -247,7 +334,10 @@ def main():
         net.capture(warmup=1, mark=gmark)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     for _ in range(args.warmup):
-        net.replay()
+        if use_graph:
+            net.replay()
+        else:
+            net.step()
     torch.cuda.synchronize()
 
     clocks = Clocks(local)
@@ -278,12 +368,13 @@ def main():
         dist.barrier()
     ms = float(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
 
-    # end to end through the public API: pinned host images in, winners out, every step
+    # end to end through the public API: pinned host images in, winners (or features) out, every step
     h_img = torch.from_numpy(imgs).pin_memory()
     h_lab = torch.from_numpy(labels).pin_memory()
-    h_win = torch.empty(net.win.shape, dtype=torch.int32).pin_memory() if hasattr(net, "win") else None
-    h_nwin = torch.empty(net.nwin.shape, dtype=torch.int32).pin_memory() if hasattr(net, "nwin") else None
-    h_feat = None if hasattr(net, "win") else torch.empty(net.features.shape, dtype=torch.float32).pin_memory()
+    train = hasattr(net, "win") and not forward
+    h_win = torch.empty(net.win.shape, dtype=torch.int32).pin_memory() if train else None
+    h_nwin = torch.empty(net.nwin.shape, dtype=torch.int32).pin_memory() if train else None
+    h_feat = None if train else torch.empty(net.features.shape, dtype=torch.float32).pin_memory()
     e2e_evs = []
     torch.cuda.synchronize()
     for _ in range(args.steps):
@@ -293,7 +384,10 @@ def main():
         net.img.copy_(h_img, non_blocking=True)
         if cfg["learning"] == "rstdp":
             net.labels.copy_(h_lab, non_blocking=True)
-        net.replay()
+        if use_graph:
+            net.replay()
+        else:
+            net.step()
         if h_win is not None:
             h_win.copy_(net.win, non_blocking=True)
             h_nwin.copy_(net.nwin, non_blocking=True)
@@ -318,7 +412,11 @@ def main():
         convs = {k: v for k, v in live_ms.items() if k.startswith("conv")}
         dom = max(convs, key=convs.get)
         li = int(dom[4:])
-        flops = conv_flops(net.layers[li], B, T)
+        rec = net.layers[li]
+        Bk = B * T if rate else B  # samples of that launch (rate coding: one image per step, T' = 1)
+        Tk = 1 if rate else T
+        flops = 2.0 * Bk * Tk * rec["Ho"] * rec["Wo"] * rec["geom"].Co * (rec["geom"].Ci * rec["geom"].Kh *
+                                                                          rec["geom"].Kw)
         achieved = flops / (convs[dom] * 1e-3) / 1e12
         peak = bf16 * INT8_OVER_BF16
         traffic = None
@@ -326,9 +424,15 @@ def main():
         if tf.exists():
             traffic = json.loads(tf.read_text()).get(f"{cfg['name']}:{dom}")
         total_imgs = cfg["batch"] if forward else world * B
-        if net.layers[li]["prec"] == "event":
+        if rec["prec"] == "event":
             # event form on CUDA cores: one shared-memory weight read + integer add per active synapse
-            adds = event_adds(net, li)
+            g = rec["geom"]
+            x = net.input_of(li)
+            x = x.reshape((g.B, g.Ci, g.Hi, g.Wi))
+            act = (x < g.T).float().sum(dim=1, keepdim=True)
+            ones = torch.ones((1, 1, g.Kh, g.Kw), device=act.device)
+            adds = float(torch.nn.functional.conv2d(act, ones, stride=(g.Sh, g.Sw), padding=(g.Ph, g.Pw))
+                         .sum().item()) * g.Co
             sm_mhz = clk.get("sm_mhz") or 1965.0
             peak_g = 148 * SMEM_WORDS_PER_CLK_SM * sm_mhz * 1e6 / 1e9
             ach_g = adds / (convs[dom] * 1e-3) / 1e9
@@ -338,12 +442,17 @@ def main():
                                  "sampled SM clock; one read + int add per active synapse (DESIGN §5.1b)",
                     "algorithmic_adds_per_launch": adds, "launch_ms": convs[dom]}
         else:
-            roof = {"bound": "tensor", "kernel": f"conv_tc_kernel ({dom}, incl. weight pack)",
+            roof = {"bound": "tensor", "kernel": f"conv_tc_kernel ({dom})",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": traffic,
                     "peak_note": f"int8 dense = {src} bf16 burst {bf16} x {INT8_OVER_BF16} (nominal 4.5/2.25); "
-                                 "the exact path issues 3 int8 MMAs per algorithmic MAC, so its ceiling is 1/3",
+                                 "the exact path issues one int8 MMA per live digit plane per algorithmic MAC "
+                                 "(3 for fp32 weights: ceiling 1/3; 1 for quantized binary weights)",
                     "algorithmic_flops_per_launch": flops, "launch_ms": convs[dom]}
+        sb = stage_bytes(net, cfg, B)
+        hbm_frac = {k: {"bytes": v, "ms": live_ms[k], "GBps": v / (live_ms[k] * 1e-3) / 1e9,
+                        "frac": v / (live_ms[k] * 1e-3) / 1e9 / hbm}
+                    for k, v in sb.items() if k in live_ms and live_ms[k] > 0}
         line = {
             "metric": METRIC,
             "value": total_imgs / (ms * 1e-3),
@@ -356,10 +465,11 @@ def main():
             "scaling": "strong" if forward else "weak",
             "vs_baseline": None,
             "dtype": ("int32/int64 exact: u8 spikes x 23-bit fixed-point weights" if args.prec != "fp32" else "f32"),
-            "data": "synthetic (seeded MNIST-like images, N(0.5, 0.02) initial weights)",
+            "data": "synthetic (seeded images, N(mean, std) initial weights" +
+                    (", quantized to {0,1} (Listing 4)" if any(L.get("quantize") for L in cfg["layers"]) else "") + ")",
             "config": {"workload": f"{cfg['name']}: {cfg['about']}", "global_batch": total_imgs, "per_gpu_batch": B,
                        "T": T, "precision": args.prec,
-                       "conv_engines": {f"conv{i}": rec["prec"] for i, rec in enumerate(net.layers)},
+                       "conv_engines": {f"conv{i}": r["prec"] for i, r in enumerate(net.layers)},
                        "parallelism": (f"dp{world}: image shards, NCCL weight broadcast ({bcast_ms:.3f} ms, untimed)"
                                        if forward else
                                        f"dp{world}: one model, mini-batch STDP over {world * B} images, all-gather of "
@@ -370,16 +480,18 @@ def main():
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches_per_step * args.steps),
             "roofline": roof,
+            "hbm_frac": hbm_frac,
+            "hbm_frac_note": f"algorithmic bytes per stage (SURVEY §8(d)-2) / live stage time, against {hbm} GB/s",
             "stage_ms": live_ms,
             "stage_ms_note": "per-stage device time inside the timed graph replays (external event nodes)",
             "clocks": clk,
         }
         if not args.no_cpu_baseline and world == 1:  # the oracle baseline is an N = 1 figure
-            line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
+            line["cpu_baseline"] = cpu_baseline(cfg, 2 if rate else args.cpu_sample)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

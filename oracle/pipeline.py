@@ -58,6 +58,7 @@ def forward(cfg: dict, imgs: np.ndarray, weights, upto: int | None = None, event
     Returns (y, lat0, inputs) where inputs[l] is the dense BTCHW train fed to layer l;
     if upto is None the list also holds the output train of the last layer (pooled)."""
     T = cfg["T"]
+    weights = quantized_weights(cfg, weights)
     y, lat0 = front_end(cfg, imgs)
     S = lat_to_dense(lat0, T)
     inputs = [S]
@@ -77,6 +78,7 @@ def train_step(cfg: dict, imgs: np.ndarray, weights, labels=None, event: bool = 
     li = cfg["train_layer"]
     L = cfg["layers"][li]
     T = cfg["T"]
+    weights = quantized_weights(cfg, weights)  # Listing 4: layers quantized after their training
     y, lat0, inputs = forward(cfg, imgs, weights, upto=li, event=event)
     S_in = inputs[li]
     P = _conv(S_in, weights[li], L, event, T)

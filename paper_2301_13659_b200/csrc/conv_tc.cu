@@ -705,7 +705,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         // output staging ring: [kNOB tiles][Nt][PPT] lat bytes, then [kNOB][Nt][PPT] P* floats
         uint8_t* ob_lat = smem + a.ob_off;
         float* ob_ps = reinterpret_cast<float*>(smem + a.ob_off + kNOB * a.Nt * PPT);
-        const uint32_t lp = live_planes(a);  // digit planes the MMAs write (others read as 0)
+        {  // digit planes no MMA writes (all-zero digits) hold zeros for the whole kernel: the
+           // epilogue then reads every plane unconditionally
+            const uint32_t lp = live_planes(a);
+            if (lp != 7u) {
+                const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                for (int b = 0; b < a.NB; ++b)
+                    for (int d = 0; d < 3; ++d)
+                        if (!((lp >> d) & 1u))
+                            for (int c = eh * 16; c < a.Nt; c += 32)
+                                tmem_st16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * 3 * a.Nt + d * a.Nt + c), z);
+                tmem_wait_st();
+            }
+        }
         TileIter ti;
         ti.init(a);
         int buf = 0, ob = 0, ep_it = 0;
@@ -731,12 +743,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) d0[q] = d1[q] = d2[q] = (uint32_t)(n0 + q + lane);
 #else
-                if (lp & 1u) tmem_ld16(tbase + n0, d0);
-                else for (int q = 0; q < 16; ++q) d0[q] = 0u;
-                if (lp & 2u) tmem_ld16(tbase + a.Nt + n0, d1);
-                else for (int q = 0; q < 16; ++q) d1[q] = 0u;
-                if (lp & 4u) tmem_ld16(tbase + 2 * a.Nt + n0, d2);
-                else for (int q = 0; q < 16; ++q) d2[q] = 0u;
+                tmem_ld16(tbase + n0, d0);
+                tmem_ld16(tbase + a.Nt + n0, d1);
+                tmem_ld16(tbase + 2 * a.Nt + n0, d2);
                 tmem_wait_ld();
 #endif
                 const int obase = nt * a.Nt + n0;
@@ -786,12 +795,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #pragma unroll
                     for (int q = 0; q < 24; ++q) r[q] = (uint32_t)(n0 * 7 + q + lane);
 #else
-                    if (lp & 1u) tmem_ld8(tbase + n0, r);
-                    else for (int q = 0; q < 8; ++q) r[q] = 0u;
-                    if (lp & 2u) tmem_ld8(tbase + a.Nt + n0, r + 8);
-                    else for (int q = 0; q < 8; ++q) r[8 + q] = 0u;
-                    if (lp & 4u) tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
-                    else for (int q = 0; q < 8; ++q) r[16 + q] = 0u;
+                    tmem_ld8(tbase + n0, r);
+                    tmem_ld8(tbase + a.Nt + n0, r + 8);
+                    tmem_ld8(tbase + 2 * a.Nt + n0, r + 16);
 #endif
                 };
                 uint32_t mine = 0;

@@ -128,6 +128,8 @@ class Network:
     def set_weights(self, ws):
         for li, (rec, dst, src) in enumerate(zip(self.layers, self.weights, ws)):
             dst.copy_(torch.as_tensor(src))
+            if rec["L"].get("quantize"):  # Listing 4: a layer quantized after its training
+                spk.quantize(dst, *rec["L"]["quantize"])
             lo, hi = float(dst.min()), float(dst.max())
             if lo < 0.0 or hi > rec["w_max"]:
                 raise ValueError(f"layer {li}: weights in [{lo}, {hi}] outside [0, w_max={rec['w_max']}] "

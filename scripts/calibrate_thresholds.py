@@ -21,7 +21,7 @@ import synth  # noqa: E402
 
 def calibrate(name: str, n_images: int = 16) -> dict:
     cfg = synth.load_config(name)
-    Ws = synth.layer_weights(cfg)
+    Ws = pipeline.quantized_weights(cfg, synth.layer_weights(cfg))  # Listing 4 layers quantized
     T = cfg["T"]
     nl = len(cfg["layers"])
     for li in range(nl):

@@ -903,3 +903,37 @@ def test_sharded_forward_bitwise_equals_whole_batch(spk, name, batch, shards):
     parts = [run(*parallel.shard_range(batch, shards, g)) for g in range(shards)]
     np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), whole_l)
     np.testing.assert_array_equal(np.concatenate([p[0] for p in parts]), whole_f)
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+@pytest.mark.parametrize("wkind", ["fp16", "binary", "zero", "digit0_only"])
+def test_conv_live_digit_planes(spk, case, wkind):
+    """The tcgen05 conv issues MMAs only for digit planes with a non-zero digit (fp16-representable
+    weights: planes 1-2; binary {0,1}: plane 2; all-zero weights; weights with only the lowest
+    digit): potentials and fire records equal the event form (which has no planes) bit for bit and
+    the oracle within the fp32 protocol; prepacked weights give the same outputs."""
+    B, T, Ci, Hi, Wi, Co, K, s, p = case
+    lat, w = _conv_inputs(B, T, Ci, Hi, Wi, Co, K)
+    if wkind == "fp16":
+        w = w.astype(np.float16).astype(np.float32)
+    elif wkind == "binary":
+        w = oracle.quantize(w, 0, 0.5, 1)
+    elif wkind == "zero":
+        w[:] = 0
+    else:
+        w = (np.floor(w * 255) * 2.0 ** -23).astype(np.float32)  # q = 0..255: only digit 0
+    ref = oracle.conv_event(lat, T, w, (s, s), (p, p))
+    got = host(spk.conv(cu(lat), cu(w), T, s, p, prec="exact", epi="potential"))
+    assert_potentials(got, ref)
+    theta = float(np.percentile(ref[:, -1], 60)) + 1e-7
+    xl, xp = spk.conv(cu(lat), cu(w), T, s, p, prec="exact", epi="fire", theta=theta)
+    g = spk.conv_geom(cu(lat), cu(w), T, s, p)
+    ws = torch.empty(spk.conv_workspace(g, "exact"), dtype=torch.uint8, device="cuda")
+    spk.conv_prepack(cu(w), g, "exact", 1.0, ws)
+    pl, pp = spk.conv(cu(lat), cu(w) * 0 + 7, T, s, p, prec="exact", epi="fire", theta=theta, ws=ws, prepacked=True)
+    np.testing.assert_array_equal(host(pl), host(xl))
+    np.testing.assert_array_equal(host(pp), host(xp))
+    if spk.conv_workspace(g, "event") > 0:
+        el, ep = spk.conv(cu(lat), cu(w), T, s, p, prec="event", epi="fire", theta=theta)
+        np.testing.assert_array_equal(host(el), host(xl))
+        np.testing.assert_array_equal(host(ep), host(xp))
