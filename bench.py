@@ -125,6 +125,18 @@ def _oracle_step(cfg, imgs, Ws, lab, start):
     """One step of the plain oracle on `imgs` (global indices start..)."""
     from oracle import pipeline as opipe
 
+    if cfg.get("kind") == "fc":
+        import oracle
+        import synth
+        S = oracle.lat_to_dense(synth.latencies(cfg, start, len(imgs), cfg["I"], cfg["T"], cfg["p_fire"]), cfg["T"])
+        W = synth.fc_weights(cfg)
+        Q = oracle.threshold(oracle.fc(S, W), cfg["theta"])
+        win, nwin = oracle.fcwta(Q, cfg["wta"]["count"], cfg["wta"]["radius"])
+        return {"W_new": oracle.fc_stdp(W, S, win, nwin, [tuple(c) for c in cfg["stdp"]])}
+    if cfg.get("kind") == "zca":
+        from oracle import zca as ozca
+        X = imgs.reshape(len(imgs), -1).astype(np.float64) / 255.0
+        return ozca.apply(X, *ozca.fit(X, cfg["eps"])) if len(imgs) > 1 else None
     if cfg.get("coding") == "rate":
         return opipe.rate_infer(cfg, imgs, Ws, start)
     if cfg["timed"] == "train":
@@ -170,14 +182,17 @@ def run_reference(args, cfg):
     import synth
 
     oracle.lib()
-    Ws = synth.layer_weights(cfg)
+    Ws = synth.layer_weights(cfg) if "layers" in cfg else None
+    if cfg.get("kind") in ("fc", "zca"):
+        per_step = max(per_step, 64)
     times = []
     for s in range(args.warmup + args.steps):
-        imgs = synth.images(cfg, s * per_step, per_step)
+        imgs = (synth.images(cfg, s * per_step, per_step) if "image" in cfg
+                else np.zeros((per_step, 1), np.uint8))  # FC: the step draws its own input latencies
         lab = synth.labels(cfg, s * per_step, per_step)
         t0 = time.perf_counter()
         r = _oracle_step(cfg, imgs, Ws, lab, s * per_step)
-        if cfg["timed"] == "train":
+        if cfg["timed"] == "train" and "train_layer" in cfg:
             Ws[cfg["train_layer"]] = r["W_new"]
         if s >= args.warmup:
             times.append(time.perf_counter() - t0)
@@ -242,6 +257,221 @@ def stage_bytes(net, cfg, B):
     return out
 
 
+def fc_zca_line(args, cfg, value, ms, e2e_ms, h2d, d2h, launches, roof, live_ms, clk, cpu, extra=None):
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32/int64 exact (FC)" if cfg["kind"] == "fc" else "f32",
+            "data": "synthetic", "config": {"workload": f"{cfg['name']}: {cfg['about']}", "global_batch": cfg["batch"],
+                                            "T": cfg["T"], "l2": "flushed between timed steps (256 MiB write)",
+                                            "cuda_graph": True, **(extra or {})},
+            "e2e": {"value": cfg["batch"] / (e2e_ms * 1e-3), "unit": "images/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches * args.steps), "roofline": roof, "stage_ms": live_ms, "clocks": clk}
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def timed_graph(args, body, dev, stages):
+    """Capture body(mark) in a CUDA graph; time K replays (L2 flushed between) with per-stage events."""
+    import torch
+
+    marks = []
+
+    def mark(name):
+        e = torch.cuda.Event(enable_timing=True, external=True)
+        e.record(torch.cuda.current_stream(dev))
+        marks.append((name, e))
+
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s):
+        body(lambda n: None)
+    torch.cuda.current_stream(dev).wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        mark("start")
+        body(mark)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    clocks = Clocks(dev.index or 0)
+    clocks.start()
+    time.sleep(0.3)
+    evs, live = [], {}
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        evs.append((e0, e1))
+        e1.synchronize()
+        for (n1, m1), (n2, m2) in zip(marks[:-1], marks[1:]):
+            live.setdefault(n2, []).append(m1.elapsed_time(m2))
+    torch.cuda.synchronize()
+    ms = float(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
+    return g, ms, {k: float(np.mean(v)) for k, v in live.items()}, clocks, flush
+
+
+def run_fc(args, cfg):
+    """NEXT-4 FC training step: spk_fc(FIRE) -> spk_fcwta -> FC STDP (spk_stdp, 1x1 geometry)."""
+    import torch
+
+    import synth
+    from paper_2301_13659_b200 import spk
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    B, T, I_, O = cfg["batch"], cfg["T"], cfg["I"], cfg["O"]
+    lat_h = torch.from_numpy(synth.latencies(cfg, 0, B, I_, T, cfg["p_fire"]))
+    W = synth.fc_weights(cfg)
+    w = torch.from_numpy(np.ascontiguousarray(W.T)).to(dev)  # output-major [O][I] (R-FC-LAYOUT)
+    w0 = w.clone()
+    lat = lat_h.to(dev)
+    prec = "event" if spk.fc_workspace(B, T, I_, O, "event") > 0 else "exact"
+    ws = torch.empty(max(1, spk.fc_workspace(B, T, I_, O, prec)), dtype=torch.uint8, device=dev)
+    out_lat = torch.empty((B, O), dtype=torch.uint8, device=dev)
+    out_ps = torch.empty((B, O), dtype=torch.float32, device=dev)
+    k, r = cfg["wta"]["count"], cfg["wta"]["radius"]
+    win = torch.empty((B, k, 6), dtype=torch.int32, device=dev)
+    nwin = torch.empty((B,), dtype=torch.int32, device=dev)
+    g = spk.ConvGeom(B, T, I_, 1, 1, O, 1, 1, 1, 1, 0, 0)
+    sws = torch.empty(spk.stdp_workspace(g, k), dtype=torch.uint8, device=dev)
+    carr = spk.stdp_configs(cfg["stdp"])
+
+    def body(mark):
+        spk.fc(lat, w, T, prec=prec, epi="fire", theta=cfg["theta"], out0=out_lat, out1=out_ps, ws=ws)
+        mark("fc")
+        spk.fcwta(out_lat, out_ps, T, k, r, win=win, nwin=nwin)
+        mark("fcwta")
+        spk.fc_stdp(w, lat, win, nwin, None, T, ws=sws, cfg_arr=carr)
+        mark("stdp")
+
+    n0 = spk.launch_count()
+    body(lambda n: None)
+    torch.cuda.synchronize()
+    launches = spk.launch_count() - n0
+    w.copy_(w0)
+    graph, ms, live, clocks, flush = timed_graph(args, body, dev, 3)
+    stream = torch.cuda.current_stream(dev)
+    h_lat, h_win = lat_h.pin_memory(), torch.empty((B, k, 6), dtype=torch.int32).pin_memory()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lat.copy_(h_lat, non_blocking=True)
+        graph.replay()
+        h_win.copy_(win, non_blocking=True)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    e2e_ms = float(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
+    _, bf16, _, src = peaks()
+    flops = 2.0 * B * T * O * I_
+    if prec == "exact":
+        ach = flops / (live["fc"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "conv_tc_kernel (FC as 1x1 conv)", "achieved": ach,
+                "peak": bf16 * INT8_OVER_BF16, "unit": "TFLOP/s", "frac": ach / (bf16 * INT8_OVER_BF16),
+                "traffic": None, "algorithmic_flops_per_launch": flops, "launch_ms": live["fc"],
+                "peak_note": "int8 dense (measured bf16 x 2); an FC layer is one pixel per sample, so the "
+                             "time-tiled M tile (8 pixels x 16 steps) holds one valid pixel: ceiling 1/8 of 1/3"}
+    else:
+        adds = float((lat < T).sum().item()) * O
+        sm = clk.get("sm_mhz") or 1965.0
+        peak_g = 148 * SMEM_WORDS_PER_CLK_SM * sm * 1e6 / 1e9
+        ach = adds / (live["fc"] * 1e-3) / 1e9
+        roof = {"bound": "alu", "kernel": "conv_event_kernel (FC as 1x1 conv)", "achieved": ach, "peak": peak_g,
+                "unit": "Gadd/s", "frac": ach / peak_g, "traffic": None, "launch_ms": live["fc"]}
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        n = 64
+        t0 = time.perf_counter()
+        S = oracle.lat_to_dense(lat_h[:n].numpy(), T)
+        P = oracle.fc(S, W)
+        Q = oracle.threshold(P, cfg["theta"])
+        wn, nw = oracle.fcwta(Q, k, r)
+        oracle.fc_stdp(W, S, wn, nw, [tuple(c) for c in cfg["stdp"]])
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "images/s", "cores": 1, "kind": "oracle", **host_info(),
+               "sample": f"{n} rows, one FC train step of the plain oracle, 1 host thread, {dt:.2f} s"}
+    fc_zca_line(args, cfg, B / (ms * 1e-3), ms, e2e_ms, h_lat.numel(), h_win.numel() * 4, launches, roof, live, clk,
+                cpu, {"engine": prec, "I": I_, "O": O})
+
+
+def run_zca(args, cfg):
+    """NEXT-4 ZCA: fit once (reported), timed step = apply to the batch."""
+    import torch
+
+    import synth
+    from paper_2301_13659_b200 import spk
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    B = cfg["batch"]
+    x_h = torch.from_numpy((synth.images(cfg, 0, B).reshape(B, -1).astype(np.float32) / np.float32(255)))
+    F = x_h.shape[1]
+    x = x_h.to(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mean, wz = spk.zca_fit(x, cfg["eps"])
+    fit_s = time.perf_counter() - t0
+    y = torch.empty_like(x)
+
+    def body(mark):
+        spk.zca_apply(x, mean, wz, out=y)
+        mark("zca_apply")
+
+    n0 = spk.launch_count()
+    body(lambda n: None)
+    torch.cuda.synchronize()
+    launches = spk.launch_count() - n0
+    graph, ms, live, clocks, flush = timed_graph(args, body, dev, 1)
+    stream = torch.cuda.current_stream(dev)
+    h_x, h_y = x_h.pin_memory(), torch.empty_like(x_h).pin_memory()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x.copy_(h_x, non_blocking=True)
+        graph.replay()
+        h_y.copy_(y, non_blocking=True)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    e2e_ms = float(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
+    sm = clk.get("sm_mhz") or 1965.0
+    peak = 148 * 128 * 2 * sm * 1e6 / 1e12  # FP32 FMA lanes x 2 flop at the sampled clock
+    flops = 2.0 * B * F * F
+    ach = flops / (live["zca_apply"] * 1e-3) / 1e12
+    roof = {"bound": "alu", "kernel": "zca_apply_kernel (fp32 CUDA-core GEMM)", "achieved": ach, "peak": peak,
+            "unit": "TFLOP/s", "frac": ach / peak, "traffic": None, "algorithmic_flops_per_launch": flops,
+            "launch_ms": live["zca_apply"],
+            "peak_note": "148 SMs x 128 fp32 FMA lanes x 2 flop at the sampled SM clock (fp32 so the whitened "
+                         "values keep the oracle's 1e-4 tolerance; tf32 tensor cores would not)"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import zca as ozca
+        with threadpool_limits(1):
+            mu, Wz = ozca.fit(x_h.numpy().astype(np.float64), cfg["eps"])
+            t0 = time.perf_counter()
+            ozca.apply(x_h.numpy(), mu, Wz)
+            dt = time.perf_counter() - t0
+        cpu = {"value": B / dt, "unit": "images/s", "cores": 1, "kind": "oracle", **host_info(),
+               "sample": f"apply to the {B}-image batch, numpy fp64 (1 BLAS thread), {dt:.3f} s"}
+    fc_zca_line(args, cfg, B / (ms * 1e-3), ms, e2e_ms, h_x.numel() * 4, h_y.numel() * 4, launches, roof, live, clk,
+                cpu, {"F": F, "eps": cfg["eps"], "fit_s": fit_s})
+
+
 def main():
     args = parse()
     import synth
@@ -249,6 +479,10 @@ def main():
     cfg = synth.load_config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg.get("kind") == "fc":
+        return run_fc(args, cfg)
+    if cfg.get("kind") == "zca":
+        return run_zca(args, cfg)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(args)
 

@@ -253,6 +253,19 @@ typedef struct {
 SPK_API spk_status spk_wta(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T, int k,
                    int radius, spk_winner* win, int32_t* nwin, spk_stream stream);
 
+/* spk_inhibit_wta — spk_inhibit then spk_wta, fused (the trained layer's
+ * Listing 3 `inhibit(output)` -> `convwta(output, r, k)`): the
+ * winners are exactly spk_wta's on the inhibited records, computed in ONE read
+ * of the (lat, P*) record without writing the inhibited map (nothing downstream
+ * of the WTA reads it: STDP uses the winners and the layer's INPUT).  The
+ * inhibition survivor of a pixel is its least (lat, P* desc, c) key, which is
+ * also its least WTA key, so keeping the per-pixel minimum and running the
+ * greedy rounds on those keys is exact.  Arguments as spk_wta (lat, pstar are
+ * read only).  Errors: as spk_wta; SPK_ERR_UNSUPPORTED when a cluster slice
+ * holds more than 12288 pixels (H*W > 98304): use the unfused pair. */
+SPK_API spk_status spk_inhibit_wta(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T,
+                                   int k, int radius, spk_winner* win, int32_t* nwin, spk_stream stream);
+
 /* ========================================================================
  * a8  STDP / R-STDP (Eq. 4-7)
  * ======================================================================== */
@@ -277,11 +290,18 @@ SPK_API size_t spk_stdp_workspace(const spk_conv_geom* g, int k);
  *   g: geometry of the conv layer whose input is lat_in [dev] u8 [B][Ci][Hi][Wi];
  *   win/nwin [dev] as spk_wta (winner.t = t_i, winner.(y,x) = output position);
  *   cfgs [host] spk_stdp_config [ncfg], 1 <= ncfg <= 8.
- * Winners with cfg outside [0, ncfg) or coordinates outside the output are skipped.
+ * Winners with cfg outside [0, ncfg) or coordinates outside the output (S:L422 errors)
+ * are skipped and COUNTED in the workspace: spk_stdp_status reads the count.
  * Errors: SPK_ERR_ARG (L >= U, ncfg out of range), SPK_ERR_SHAPE, SPK_ERR_WORKSPACE. */
 SPK_API spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* lat_in, const spk_winner* win,
                     const int32_t* nwin, int k, const spk_stdp_config* cfgs, int ncfg, void* ws,
                     size_t ws_bytes, spk_stream stream);
+
+/* spk_stdp_status — number of winners the last spk_stdp on `ws` (same g, k) skipped
+ * because a coordinate or its cfg was out of range (a data-dependent fault, e.g. a
+ * mis-rebased data-parallel winner).  Synchronises `stream`. */
+SPK_API spk_status spk_stdp_status(const void* ws, const spk_conv_geom* g, int k, int32_t* invalid_out,
+                                   spk_stream stream);
 
 /* spk_rstdp_route — R-STDP configuration routing (Eq. 7: "passing
  * two configurations ... and mapping each winner neuron to a configuration

@@ -258,6 +258,7 @@ def stdp(W: np.ndarray, S_in: np.ndarray, win, nwin, cfgs, stride=(1, 1), pad=(0
     Co, Ci, Kh, Kw = W.shape
     B, T, Ci2, Hi, Wi = S_in.shape
     assert Ci2 == Ci
+    assert win.shape[0] == B and nwin.shape[0] == B and win.shape[2] == 6, "winners must cover every sample"
     cfg = _c([[c[0], c[1], c[2], c[3]] for c in cfgs], np.float32)
     stab = _c([int(bool(c[4])) for c in cfgs], np.int32)
     lib().oracle_stdp(_p(W), Co, Ci, Kh, Kw, *stride, *pad, _p(S_in), B, T, Hi, Wi, _p(win),
@@ -344,6 +345,7 @@ def fc_stdp(W: np.ndarray, S_in: np.ndarray, win, nwin, cfgs) -> np.ndarray:
     I_, O = W.shape
     B, T, I2 = S_in.shape
     assert I2 == I_
+    assert win.shape[0] == B and nwin.shape[0] == B and win.shape[2] == 6, "winners must cover every sample"
     cfg = _c([[c[0], c[1], c[2], c[3]] for c in cfgs], np.float32)
     stab = _c([int(bool(c[4])) for c in cfgs], np.int32)
     lib().oracle_fc_stdp(_p(W), I_, O, _p(S_in), B, T, _p(win), _p(nwin), win.shape[1], _p(cfg), _p(stab),

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -21,6 +22,29 @@ spk_status launched(const char* kernel);
 inline cudaStream_t as_cuda(spk_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+// True the first time it is called for the current device with this mask (per-device,
+// thread-safe one-time setup such as cudaFuncSetAttribute opt-ins; devices 0..63).
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    return !(mask.fetch_or(bit) & bit);
+}
+
+// SM count of the current device (cached per device).
+inline int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int n = cache[dev & 63].load();
+    if (n <= 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        cache[dev & 63].store(n);
+    }
+    return n;
+}
 
 }  // namespace spk
 

@@ -1217,23 +1217,11 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, int Co, int K, 
     if ((threadIdx.x & 31) == 0 && (live & ~(uint32_t)__ldcg(flag))) atomicOr(flag, (int)live);
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
-
 template <int EPI, bool PSTAR, int TP>
 void launch(const TcArgs& a, unsigned grid, size_t smem, cudaStream_t s) {
-    static bool done = false;
-    if (!done) {
+    static std::atomic<uint64_t> done{0};
+    if (spk::first_on_device(done)) {
         cudaFuncSetAttribute(conv_tc_kernel<EPI, PSTAR, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        done = true;
     }
     conv_tc_kernel<EPI, PSTAR, TP><<<grid, kThreads, smem, s>>>(a);
 }
@@ -1429,7 +1417,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.kt16 = p.kt16;
     a.ob_off = (a.rg_off + (uint32_t)(p.nrb * p.rb_stride) + 15u) & ~15u;
     a.bar_off = (a.ob_off + (uint32_t)(kNOB * p.Nt * p.PPT * 5) + 15u) & ~15u;
-    const long long grid = p.total_tiles < sm_count() ? p.total_tiles : sm_count();
+    const long long grid = p.total_tiles < spk::sm_count() ? p.total_tiles : spk::sm_count();
     if (p.TP == 16) launch_tp<16>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
     else launch_tp<32>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
     return spk::launched("conv_tc_kernel");

@@ -484,11 +484,10 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
         SPK_CHECK(nblk < (1ll << 31), SPK_ERR_SHAPE, "B*C too large");
         const bool bulk = ((H * W) % 16 == 0) && (plane_out % 16 == 0) &&
                           ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};
+        if (spk::first_on_device(attr)) {
             cudaFuncSetAttribute(pool_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPoolSmem);
             cudaFuncSetAttribute(pool_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPoolSmem);
-            attr = true;
         }
         if (bulk) {
             pool_smem_kernel<true><<<(unsigned)nblk, kT, smem, spk::as_cuda(stream)>>>(lat, BC, ppc, H, W, T, *p, Ho, Wo, out);

@@ -503,11 +503,10 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
     }();
     if (sort && N <= kSortMax && !old_sort) {  // small samples: staged values, 4096-bucket histogram
         using Cfg = HistCfg<19, 256, 1024, true>;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};
+        if (spk::first_on_device(attr)) {
             cudaFuncSetAttribute(rank_code_hist_kernel<19, 256, 1024, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(kSortMax));
-            attr = true;
         }
         rank_code_hist_kernel<19, 256, 1024, true><<<B, 256, Cfg::smem(N), s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel<small>");
@@ -516,11 +515,10 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         int cap = 1;
         while (cap < N) cap <<= 1;
         const size_t smem = sizeof(unsigned long long) * (size_t)cap;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};
+        if (spk::first_on_device(attr)) {
             cudaFuncSetAttribute(rank_code_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned long long) * kSortMax));
-            attr = true;
         }
         rank_code_sort_kernel<<<B, kSortThreads, smem, s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_sort_kernel");
@@ -529,33 +527,30 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         // 16384 buckets (exponent + 6 mantissa bits) and 4096 candidates: 96 KB, two CTAs per
         // SM (C5 samples have 2-3K boundary-bucket values; more falls back to the radix select)
         using Cfg = HistCfg<17, 1024, 4096, false>;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};
+        if (spk::first_on_device(attr)) {
             cudaFuncSetAttribute(rank_code_hist_kernel<17, 1024, 4096, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(0));
-            attr = true;
         }
         rank_code_hist_kernel<17, 1024, 4096, false><<<B, 1024, Cfg::smem(0), s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel");
     }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
         const size_t smem = sizeof(unsigned int) * (size_t)N;
-        static bool attr = false;  // up to 32 KB of staged values next to the static RankSmem
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};  // up to 32 KB of staged values next to the static RankSmem
+        if (spk::first_on_device(attr)) {
             cudaFuncSetAttribute(rank_code_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned int) * 8192));
-            attr = true;
         }
         rank_code_kernel<true, 256><<<B, 256, smem, s>>>(y, N, T, thresh, sort, lat);
         return spk::launched("rank_code_kernel<staged,256>");
     }
     if (N <= kStageMax) {
         const size_t smem = sizeof(unsigned int) * (size_t)N;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<uint64_t> attr{0};
+        if (spk::first_on_device(attr)) {
             cudaFuncSetAttribute(rank_code_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned int) * kStageMax));
-            attr = true;
         }
         rank_code_kernel<true, 1024><<<B, 1024, smem, s>>>(y, N, T, thresh, sort, lat);
         return spk::launched("rank_code_kernel<staged,1024>");

@@ -27,14 +27,16 @@ __device__ __forceinline__ bool winner_valid(const spk_winner& w, int B, int ncf
 }
 
 __global__ void stdp_slotmap_kernel(const spk_winner* __restrict__ win, const int32_t* __restrict__ nwin, int B,
-                                    int k, int ncfg, int Ho, int Wo, int Co, int32_t* __restrict__ slotmap) {
+                                    int k, int ncfg, int Ho, int Wo, int Co, int32_t* __restrict__ slotmap,
+                                    int32_t* __restrict__ invalid) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= B * k) return;
     const int b = s / k, q = s - b * k;
     int m = -1;
-    if (q < nwin[b]) {
+    if (q < min(nwin[b], k)) {
         const spk_winner w = win[s];
         if (winner_valid(w, B, ncfg, Ho, Wo, Co)) m = w.c;
+        else atomicAdd(invalid, 1);  // out-of-range coordinate or config: skipped, counted
     }
     slotmap[s] = m;
 }
@@ -227,8 +229,10 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     int32_t* cnt = start + g->Co;
     int32_t* slotmap = cnt + g->Co;
     cudaStream_t s = spk::as_cuda(stream);
+    int32_t* invalid = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + need - 256);  // spk_stdp_status
+    if (cudaMemsetAsync(invalid, 0, sizeof(int32_t), s) != cudaSuccess) return spk::launched("memset(invalid)");
     stdp_slotmap_kernel<<<spk::ceil_div((size_t)cap, 256), 256, 0, s>>>(win, nwin, g->B, k, ncfg, Ho, Wo, g->Co,
-                                                                      slotmap);
+                                                                      slotmap, invalid);
     spk_status st = spk::launched("stdp_slotmap_kernel");
     if (st != SPK_OK) return st;
     stdp_bucket_kernel<<<g->Co, kBucketThreads, 0, s>>>(slotmap, cap, cap, list, start, cnt);
@@ -239,4 +243,22 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     const dim3 grid(spk::ceil_div(K, kUpdW), (unsigned)g->Co);
     stdp_update_kernel<<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
     return spk::launched("stdp_update_kernel");
+}
+
+extern "C" spk_status spk_stdp_status(const void* ws, const spk_conv_geom* g, int k, int32_t* invalid_out,
+                                      spk_stream stream) {
+    spk::clear_error();
+    SPK_CHECK_PTR(ws);
+    SPK_CHECK_PTR(g);
+    SPK_CHECK_PTR(invalid_out);
+    const size_t need = spk_stdp_workspace(g, k);
+    SPK_CHECK(need > 0, SPK_ERR_ARG, "bad geometry or k");
+    cudaStream_t s = spk::as_cuda(stream);
+    int32_t v = 0;
+    if (cudaMemcpyAsync(&v, static_cast<const char*>(ws) + need - 256, sizeof(int32_t), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return spk::launched("spk_stdp_status");
+    *invalid_out = v;
+    return SPK_OK;
 }

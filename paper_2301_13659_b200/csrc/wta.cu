@@ -240,11 +240,10 @@ template <int KK>
 spk_status launch_wta(const WtaArgs& a, int B, size_t cap, cudaStream_t s) {
     auto kern = wta_cluster_kernel<KK>;
     const size_t smem = cap * 8;  // shared key buffer sized to the slice's candidate bound
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (spk::first_on_device(attr)) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kCapKeys * 8) != cudaSuccess)
             return spk::launched("wta_cluster_kernel(attr)");
-        attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)a.cs, (unsigned)B, 1);
@@ -264,8 +263,26 @@ spk_status launch_wta(const WtaArgs& a, int B, size_t cap, cudaStream_t s) {
 
 }  // namespace
 
+static spk_status wta_impl(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T, int k,
+                           int radius, spk_winner* win, int32_t* nwin, spk_stream stream, bool inhibit);
+
 extern "C" spk_status spk_wta(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T,
                               int k, int radius, spk_winner* win, int32_t* nwin, spk_stream stream) {
+    return wta_impl(lat, pstar, B, C, H, W, T, k, radius, win, nwin, stream, false);
+}
+
+// Lateral inhibition fused into the k-WTA (Listing 3 inhibit -> convwta on the trained layer):
+// the inhibition survivor of a pixel is its least (lat, P*, c) key (R-INHIBIT-TIE), which is
+// also its least WTA key, so keeping exactly the per-pixel minimum in phase 1 and running the
+// rounds on those keys gives the winners of spk_wta(spk_inhibit(records)) — in one read of the
+// records, without writing the inhibited map.
+extern "C" spk_status spk_inhibit_wta(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T,
+                                      int k, int radius, spk_winner* win, int32_t* nwin, spk_stream stream) {
+    return wta_impl(lat, pstar, B, C, H, W, T, k, radius, win, nwin, stream, true);
+}
+
+static spk_status wta_impl(const uint8_t* lat, const float* pstar, int B, int C, int H, int W, int T, int k,
+                           int radius, spk_winner* win, int32_t* nwin, spk_stream stream, bool inhibit) {
     spk::clear_error();
     SPK_CHECK_PTR(lat);
     SPK_CHECK_PTR(pstar);
@@ -292,6 +309,14 @@ extern "C" spk_status spk_wta(const uint8_t* lat, const float* pstar, int B, int
     while (KK < keep) KK <<= 1;
     const long long slice_p = (HW + a.cs - 1) / a.cs;
     long long cap = 1;
+    if (inhibit) {  // per-pixel minimum only (the inhibition survivor)
+        SPK_CHECK(slice_p <= kCapKeys, SPK_ERR_UNSUPPORTED,
+                  "fused inhibit+WTA needs <= %d pixels per CTA slice (H*W=%lld); call spk_inhibit + spk_wta",
+                  kCapKeys, HW);
+        a.mode = 1;
+        a.cap = (unsigned)slice_p;
+        return launch_wta<1>(a, B, (size_t)slice_p, spk::as_cuda(stream));
+    }
     if (slice_n <= kCapKeys) a.mode = 0, cap = slice_n;
     else if (KK <= 16 && slice_p * KK <= kCapKeys) a.mode = 1, cap = slice_p * KK;
     else a.mode = 2;

@@ -21,7 +21,7 @@ def _nomark(name: str) -> None:
 
 
 class Network:
-    def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "exact"):
+    def __init__(self, cfg: dict, batch: int, device="cuda", prec: str = "exact", fuse_inhibit: bool = True):
         """prec: "exact" (tcgen05 EXACT_I8 for every conv), "event" (latency-sorted form
         on CUDA cores where its weight block fits), "auto" (event for the first layer and
         for narrow layers, Co <= 64; tensor cores otherwise) or "fp32".  exact/event/auto
@@ -31,6 +31,9 @@ class Network:
         self.T = cfg["T"]
         self.dev = torch.device(device)
         self.prec = prec
+        # trained layer: inhibition fused into the WTA (spk_inhibit_wta; the inhibited record is
+        # then not materialised) when its maps are small enough, else spk_inhibit + spk_wta
+        self.fuse_inhibit = fuse_inhibit
         im, fr = cfg["image"], cfg["front"]
         self.img = torch.zeros((batch, im["C"], im["H"], im["W"]), dtype=torch.uint8, device=self.dev)
         self.labels = torch.zeros((batch,), dtype=torch.int32, device=self.dev)
@@ -89,9 +92,11 @@ class Network:
             self.layers.append(rec)
             self.weights.append(torch.zeros((L["Co"], geom.Ci, L["K"], L["K"]), dtype=torch.float32,
                                             device=self.dev))
+        self.fused_inhibit = False
         if tl is not None:
             rec = self.layers[tl]
             wk = rec["L"]["wta"]
+            self.fused_inhibit = fuse_inhibit and rec["Ho"] * rec["Wo"] <= 12288  # one cluster slice
             self.k = wk["count"]
             self.win = torch.empty((batch, self.k, 6), dtype=torch.int32, device=self.dev)
             self.nwin = torch.empty((batch,), dtype=torch.int32, device=self.dev)
@@ -189,10 +194,14 @@ class Network:
         self.layer(tl, pstar=True, mark=mark)
         rec = self.layers[tl]
         L = rec["L"]
-        spk.inhibit(rec["lat"], rec["pstar"], self.T)
-        mark("inhibit")
-        spk.wta(rec["lat"], rec["pstar"], self.T, self.k, L["wta"]["radius"], win=self.win, nwin=self.nwin)
-        mark("wta")
+        if self.fused_inhibit:
+            spk.inhibit_wta(rec["lat"], rec["pstar"], self.T, self.k, L["wta"]["radius"], win=self.win, nwin=self.nwin)
+            mark("inhibit_wta")
+        else:
+            spk.inhibit(rec["lat"], rec["pstar"], self.T)
+            mark("inhibit")
+            spk.wta(rec["lat"], rec["pstar"], self.T, self.k, L["wta"]["radius"], win=self.win, nwin=self.nwin)
+            mark("wta")
         if self.cfg["learning"] == "rstdp":
             spk.rstdp_route(self.win, self.nwin, self.labels, self.cfg["maps_per_class"])
             mark("rstdp_route")

@@ -44,6 +44,7 @@ EXPORTS = [
     "spk_lat_to_dense", "spk_dense_to_lat", "spk_conv_status", "spk_conv_fire_pool_supported", "spk_conv_fire_pool",
     "spk_rate_code_workspace", "spk_rate_code", "spk_rate_gather", "spk_pool_rates", "spk_quantize", "spk_fc_workspace",
     "spk_fc", "spk_fcwta", "spk_zca_fit_workspace", "spk_zca_fit", "spk_zca_apply", "spk_conv_prepack",
+    "spk_stdp_status", "spk_inhibit_wta",
 ]
 
 
@@ -93,6 +94,8 @@ def lib():
             "spk_zca_fit": ([V, I, I, ctypes.c_double, V, V, V, Z, V], I),
             "spk_zca_apply": ([V, I, I, V, V, V, V], I),
             "spk_conv_prepack": ([V, ctypes.POINTER(ConvGeom), I, F, V, Z, V], I),
+            "spk_stdp_status": ([V, ctypes.POINTER(ConvGeom), I, ctypes.POINTER(ctypes.c_int32), V], I),
+            "spk_inhibit_wta": ([V, V, I, I, I, I, I, I, I, V, V, V], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -305,6 +308,18 @@ def wta(lat: torch.Tensor, pstar: torch.Tensor, T: int, k: int, radius: int, win
     return win, nwin
 
 
+def inhibit_wta(lat: torch.Tensor, pstar: torch.Tensor, T: int, k: int, radius: int, win=None, nwin=None):
+    """spk_inhibit + spk_wta fused: winners of the inhibited records (records not modified)."""
+    B, C, H, W = lat.shape
+    if win is None:
+        win = torch.empty((B, k, 6), dtype=torch.int32, device=lat.device)
+    if nwin is None:
+        nwin = torch.empty((B,), dtype=torch.int32, device=lat.device)
+    _check("spk_inhibit_wta", lib().spk_inhibit_wta(_p(lat), _p(pstar), B, C, H, W, T, k, radius, _p(win), _p(nwin),
+                                                    _s()))
+    return win, nwin
+
+
 # ---------------------------------------------------------------- a8 stdp
 def stdp_configs(cfgs):
     arr = (StdpConfig * len(cfgs))()
@@ -329,6 +344,14 @@ def stdp(w: torch.Tensor, lat_in: torch.Tensor, win: torch.Tensor, nwin: torch.T
     _check("spk_stdp", lib().spk_stdp(_p(w), ctypes.byref(g), _p(lat_in), _p(win), _p(nwin), k, arr, len(arr),
                                       _p(ws), ws.numel(), _s()))
     return w
+
+
+def stdp_invalid(ws: torch.Tensor, lat_in: torch.Tensor, w: torch.Tensor, T: int, k: int, stride=1, pad=0) -> int:
+    """Winners the last stdp() on ws skipped (out-of-range coordinate or config)."""
+    g = conv_geom(lat_in, w, T, stride, pad)
+    v = ctypes.c_int32(0)
+    _check("spk_stdp_status", lib().spk_stdp_status(_p(ws), ctypes.byref(g), k, ctypes.byref(v), _s()))
+    return v.value
 
 
 def rstdp_route(win: torch.Tensor, nwin: torch.Tensor, labels: torch.Tensor, maps_per_class: int):

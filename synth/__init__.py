@@ -153,3 +153,22 @@ def layer_weights(cfg: dict) -> list[np.ndarray]:
                            init.get("lower", 0.0), init.get("upper", 1.0), init.get("fp16", False)))
         ci = L["Co"]
     return out
+
+
+def latencies(cfg: dict, start: int, count: int, n: int, T: int, p_fire: float) -> np.ndarray:
+    """Synthetic first-spike latency maps u8 [count][n] (an input to the FC workload): each input
+    fires with probability p_fire at a uniform step 0..T-1, else never (T).  One draw per global row."""
+    out = np.empty((count, n), np.uint8)
+    for q in range(count):
+        g = _rng(cfg["seed"], 0x1A7, start + q)
+        lat = g.integers(0, T, n)
+        lat[g.random(n) >= p_fire] = T
+        out[q] = lat.astype(np.uint8)
+    return out
+
+
+def fc_weights(cfg: dict) -> np.ndarray:
+    """FC kernel in the paper's I x O layout, N(mean, std) clipped to [0, 1]."""
+    g = _rng(cfg["seed"], 0xFC, 0)
+    w = np.clip(g.normal(cfg["init"]["mean"], cfg["init"]["std"], (cfg["I"], cfg["O"])), 0.0, 1.0)
+    return np.ascontiguousarray(w.astype(np.float32))

@@ -439,10 +439,10 @@ def test_gather_vectorised(spk, T):
 
 
 # ------------------------------------------------------------------ pipelines end to end
-def _gpu_train(cfg, imgs, Ws, labels=None, prec="exact"):
+def _gpu_train(cfg, imgs, Ws, labels=None, prec="exact", fuse=True):
     from paper_2301_13659_b200.network import Network
 
-    net = Network(cfg, imgs.shape[0], prec=prec)
+    net = Network(cfg, imgs.shape[0], prec=prec, fuse_inhibit=fuse)
     net.img.copy_(cu(imgs))
     if labels is not None:
         net.labels.copy_(cu(labels))
@@ -472,13 +472,13 @@ def _layer_out_diff(rec, L, rlat, excl, excluded, T, key=None):
     return diff.any(axis=(1, 2, 3))
 
 
-def _check_pipeline(cfg, n, labels=False, prec="exact"):
-    name = f"{cfg['name']} train step, batch {n}, prec={prec}"
+def _check_pipeline(cfg, n, labels=False, prec="exact", fuse=True):
+    name = f"{cfg['name']} train step, batch {n}, prec={prec}" + ("" if fuse else ", unfused inhibit")
     imgs = synth.images(cfg, 0, n)
     lab = synth.labels(cfg, 0, n) if labels else None
     Ws = synth.layer_weights(cfg)
     ref = opipe.train_step(cfg, imgs, Ws, lab, event=True)
-    net = _gpu_train(cfg, imgs, Ws, lab, prec)
+    net = _gpu_train(cfg, imgs, Ws, lab, prec, fuse)
     T = cfg["T"]
     np.testing.assert_array_equal(host(net.lat0), ref["lat0"])
     tl = cfg["train_layer"]
@@ -494,10 +494,12 @@ def _check_pipeline(cfg, n, labels=False, prec="exact"):
     # trained layer: (lat, P*) after inhibition, winners, weights
     L = cfg["layers"][tl]
     excl = near_threshold(ref["P"], L["theta"])
-    rlat, rps = lat_and_pstar(ref["Qi"], 0.0)
+    # fused inhibition+WTA leaves the fire record un-inhibited (only the winners carry it)
+    rlat, rps = lat_and_pstar(ref["Q"] if net.fused_inhibit else ref["Qi"], 0.0)
     glat = host(net.layers[tl]["lat"])
     keep = ~excluded_samples
-    ParityReport.latency((name, f"conv{tl} fire + inhibit"), glat[keep], rlat[keep], excl[keep])
+    ParityReport.latency((name, f"conv{tl} fire" + ("" if net.fused_inhibit else " + inhibit")), glat[keep], rlat[keep],
+                         excl[keep])
     ParityReport.ties((name, f"conv{tl} inhibit"), *near_ties_inhibit(ref["Q"]))
     ParityReport.ties((name, f"conv{tl} wta"), *near_ties_wta(ref["Qi"], L["wta"]["count"], L["wta"]["radius"]))
     gps = host(net.layers[tl]["pstar"])
@@ -530,6 +532,13 @@ def test_pipeline_c1(spk):
 @pytest.mark.parametrize("prec", ["exact", "fp32", "auto", "event"])
 def test_pipeline_c2_small_batch(spk, prec):
     assert _check_pipeline(synth.load_config("c2"), 12, prec=prec) <= 1
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_pipeline_unfused_inhibit(spk, name):
+    """The unfused trained-layer path (spk_inhibit writes the inhibited record, then spk_wta)."""
+    cfg = synth.load_config(name)
+    assert _check_pipeline(cfg, 1 if name == "c1" else 12, labels=name == "c3", fuse=False) <= 1
 
 
 def test_pipeline_c3_rstdp(spk):
@@ -596,22 +605,24 @@ def _check_rows_train(cfg, net, imgs, rows, Ws, labels=None):
                             key=(name, f"conv{li} fire"))
         L = cfg["layers"][tl]
         P = oracle.conv_event(host(net.input_of(tl)[b:b + 1]), T, Ws[tl], (L["stride"],) * 2, (L["pad"],) * 2)
-        Qi = oracle.inhibit(oracle.threshold(P, L["theta"]))
+        Q = oracle.threshold(P, L["theta"])
+        Qi = oracle.inhibit(Q)
         win, nwin = oracle.wta(Qi, L["wta"]["count"], L["wta"]["radius"])
         if cfg["learning"] == "rstdp":
             win = oracle.rstdp_route(win, nwin, labels[b:b + 1], cfg["maps_per_class"])
-        rlat, rps = lat_and_pstar(Qi, 0.0)
+        rlat, rps = lat_and_pstar(Q if net.fused_inhibit else Qi, 0.0)
         glat_b = host(net.layers[tl]["lat"][b:b + 1])
         diff = glat_b != rlat
         excl_b = near_threshold(P, L["theta"])
-        ParityReport.latency((name, f"conv{tl} fire + inhibit"), glat_b, rlat, excl_b)
-        ParityReport.ties((name, f"conv{tl} inhibit"), *near_ties_inhibit(oracle.threshold(P, L["theta"])))
+        ParityReport.latency((name, f"conv{tl} fire" + ("" if net.fused_inhibit else " + inhibit")), glat_b, rlat,
+                             excl_b)
+        ParityReport.ties((name, f"conv{tl} inhibit"), *near_ties_inhibit(Q))
         ParityReport.ties((name, f"conv{tl} wta"), *near_ties_wta(Qi, L["wta"]["count"], L["wta"]["radius"]))
         gps_b = host(net.layers[tl]["pstar"][b:b + 1])
         okp = (glat_b == rlat) & (rlat < T)
         ParityReport.potentials((name, f"conv{tl} P*"), gps_b[okp], rps[okp])
         assert not (diff & ~excl_b).any(), "trained layer: unexplained mismatches"
-        del P, Qi
+        del P, Q, Qi
         if diff.any():
             excluded += 1
             ParityReport.excluded_samples((name, "samples"), 1)
@@ -937,3 +948,44 @@ def test_conv_live_digit_planes(spk, case, wkind):
         el, ep = spk.conv(cu(lat), cu(w), T, s, p, prec="event", epi="fire", theta=theta)
         np.testing.assert_array_equal(host(el), host(xl))
         np.testing.assert_array_equal(host(ep), host(xp))
+
+
+@pytest.mark.parametrize("shape,k,r", [((4, 200, 4, 4), 8, 1), ((2, 30, 28, 28), 5, 3), ((1, 32, 28, 28), 5, 3),
+                                       ((2, 128, 80, 125), 8, 1), ((3, 7, 1, 1), 3, 0), ((2, 64, 30, 40), 20, 2)])
+@pytest.mark.parametrize("ties", [False, True])
+def test_inhibit_wta_fused_exact(spk, shape, k, r, ties):
+    """spk_inhibit_wta == oracle inhibit -> wta (winners bit-exact), records left untouched."""
+    B, C, H, W = shape
+    T = 15
+    Q, lat, ps = _records(B, T, C, H, W, 0.4, ties)
+    win, nwin = oracle.wta(oracle.inhibit(Q), k, r)
+    glat, gps = cu(lat), cu(ps.astype(np.float32))
+    gw, gn = spk.inhibit_wta(glat, gps, T, k, r)
+    gw, gn = host(gw), host(gn)
+    np.testing.assert_array_equal(gn, nwin)
+    for b in range(B):
+        np.testing.assert_array_equal(gw[b, :nwin[b]], win[b, :nwin[b]])
+        assert (gw[b, nwin[b]:] == -1).all()
+    np.testing.assert_array_equal(host(glat), lat)
+
+
+def test_stdp_invalid_winners_counted(spk):
+    """Out-of-range winners (coordinate or cfg) are skipped and counted (spk_stdp_status)."""
+    T, B, k = 15, 2, 3
+    lat_in = RNG.integers(0, T + 1, (B, 2, 6, 6)).astype(np.uint8)
+    W0 = RNG.uniform(0.1, 0.9, (4, 2, 3, 3)).astype(np.float32)
+    win = np.full((B, k, 6), -1, np.int32)
+    win[0, 0] = [0, 3, 1, 2, 2, 0]     # valid
+    win[0, 1] = [0, 3, 9, 2, 2, 0]     # map out of range
+    win[1, 0] = [1, 3, 1, 2, 2, 5]     # cfg out of range
+    win[1, 1] = [1, 3, 1, 2, 7, 0]     # x out of range
+    nwin = np.array([2, 2], np.int32)
+    cfgs = [(0.004, -0.003, 0.0, 1.0, 1)]
+    # the only valid winner is (sample 0, pick 0): the oracle applies just that one
+    ref = oracle.stdp(W0, oracle.lat_to_dense(lat_in[:1], T), win[:1, :1], np.ones(1, np.int32), cfgs, (1, 1), (1, 1))
+    w = cu(W0)
+    g = spk.conv_geom(cu(lat_in), w, T, 1, 1)
+    ws = torch.empty(spk.stdp_workspace(g, k), dtype=torch.uint8, device="cuda")
+    spk.stdp(w, cu(lat_in), cu(win), cu(nwin), cfgs, T, 1, 1, ws=ws)
+    assert spk.stdp_invalid(ws, cu(lat_in), w, T, k, 1, 1) == 3
+    np.testing.assert_array_equal(host(w), ref)
