@@ -257,6 +257,11 @@ def stage_bytes(net, cfg, B):
     return out
 
 
+def _trace(msg):
+    if os.environ.get("SPK_BENCH_TRACE"):
+        print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+
 def fc_zca_line(args, cfg, value, ms, e2e_ms, h2d, d2h, launches, roof, live_ms, clk, cpu, extra=None):
     line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -285,18 +290,23 @@ def timed_graph(args, body, dev, stages):
 
     s = torch.cuda.Stream(device=dev)
     s.wait_stream(torch.cuda.current_stream(dev))
+    _trace("warm-up body on a side stream")
     with torch.cuda.stream(s):
         body(lambda n: None)
     torch.cuda.current_stream(dev).wait_stream(s)
+    torch.cuda.synchronize()
+    _trace("capture")
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         mark("start")
         body(mark)
+    _trace("captured")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         g.replay()
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
+    _trace("replays")
     clocks = Clocks(dev.index or 0)
     clocks.start()
     time.sleep(0.3)
@@ -313,6 +323,7 @@ def timed_graph(args, body, dev, stages):
             live.setdefault(n2, []).append(m1.elapsed_time(m2))
     torch.cuda.synchronize()
     ms = float(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
+    g.spk_marks = marks  # the graph's event-record nodes point at these events: keep them alive
     return g, ms, {k: float(np.mean(v)) for k, v in live.items()}, clocks, flush
 
 
@@ -350,10 +361,12 @@ def run_fc(args, cfg):
         spk.fc_stdp(w, lat, win, nwin, None, T, ws=sws, cfg_arr=carr)
         mark("stdp")
 
+    _trace(f"fc eager step (engine {prec})")
     n0 = spk.launch_count()
     body(lambda n: None)
     torch.cuda.synchronize()
     launches = spk.launch_count() - n0
+    _trace("fc eager step done")
     w.copy_(w0)
     graph, ms, live, clocks, flush = timed_graph(args, body, dev, 3)
     stream = torch.cuda.current_stream(dev)
@@ -418,8 +431,10 @@ def run_zca(args, cfg):
     F = x_h.shape[1]
     x = x_h.to(dev)
     torch.cuda.synchronize()
+    _trace("zca fit")
     t0 = time.perf_counter()
     mean, wz = spk.zca_fit(x, cfg["eps"])
+    _trace("zca fit done")
     fit_s = time.perf_counter() - t0
     y = torch.empty_like(x)
 
@@ -474,6 +489,9 @@ def run_zca(args, cfg):
 
 def main():
     args = parse()
+    if os.environ.get("SPK_BENCH_WATCHDOG"):  # debugging aid: dump every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["SPK_BENCH_WATCHDOG"]), exit=True)
     import synth
 
     cfg = synth.load_config(args.config)

@@ -440,8 +440,8 @@ __device__ __forceinline__ uint32_t live_planes(const TcArgs& a) {
 template <int EPI, bool PSTAR, int TP>
 // 20 warps: 5 per scheduler, whose 16K-register file then allows 96 registers per thread
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
-    constexpr int LOGTP = TP == 16 ? 4 : 5;
-    constexpr int PPT = 128 / TP;
+    constexpr int LOGTP = TP == 1 ? 0 : TP == 16 ? 4 : 5;
+    constexpr int PPT = 128 / TP;  // pixels per M tile (TP = 1: one time step, rows = 128 pixels)
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* Bs = smem + a.b_off;
     uint8_t* LC = smem + a.lc_off;  // per-producer-warp latcol: [8 warps][2 bufs][2 pixels][KS/2]
@@ -526,7 +526,95 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 #endif
 
     if (warp < kProdWarps && (SPK_EXP & 32768)) {  // timing experiment: no producers (MMA skips A waits)
-    } else if (warp < kProdWarps) {
+    } else if (TP == 1 && warp < kProdWarps) {
+        // ======================= producers, one time step (TP = 1) =======================
+        // T = 1 (e.g. rate-coded trains as one-step latency maps, B' = B T): row r of an M tile is
+        // pixel j*128 + r, A[r][k] = 0x80 [in(r, k) == 0]; each lane gathers its own pixel's
+        // receptive field (64 synapses of its K half per stage) — the synapse-table entries are
+        // the same for every lane (broadcast reads), the staged-band bytes are neighbouring pixels'.
+        RoleClock rc(a.prof != 0);
+        const int quad = warp & 3, half = warp >> 2;
+        constexpr int HK = KS / 2;
+        const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(a.aCol0 + half * (HK / 4));
+        TileIter ti;
+        ti.init(a);
+        int rb = 0, rbn = 0, sA = 0;
+        uint32_t phA = 0, rgph = 0;
+        bool need_region = true;
+        for (; ti.valid(); ti.next(a)) {
+            if (a.retain && ti.nt != 0) continue;
+            if (need_region) {
+                rb = rbn;
+                rc.template group_wait<kBarProd, kProdWarps * 32>(rgf0 + 8 * rb, rgph, threadIdx.x == 0);
+                if (++rbn == a.nrb) rbn = 0, rgph ^= 1u;
+            }
+            const bool last_use = a.retain ? ti.template region_ends_m<PPT>(a) : ti.template region_ends<PPT>(a);
+            need_region = last_use;
+            const uint8_t* region = RG + rb * a.rb_stride;
+            const int p = ti.j * PPT + quad * 32 + lane;
+            const bool pvalid = p < a.HWo;
+            int pixbase = 0;
+            if (pvalid) {
+                const int yo = p / a.Wo, xo = p - yo * a.Wo;
+                pixbase = (yo * g.Sh - ti.r0<PPT>(a)) * a.WiP + xo * g.Sw;
+            }
+            for (int ks = 0; ks < a.nks; ++ks) {
+                const int kin = a.G == 1 ? 0 : (ks & 1);
+                const bool gfirst = kin == 0, glast = kin == a.G - 1 || ks + 1 == a.nks;
+                const int s = sA * a.G + kin;
+                const uint32_t ph = phA;
+                const uint32_t gbar = 8u * (uint32_t)sA;
+                if (glast && ++sA == a.NA / a.G) sA = 0, phA ^= 1u;
+                uint32_t r[16];
+                const int kb = ks * KS + half * HK;
+                // the stage's 64 table entries first (broadcast reads, all in flight), then the
+                // band bytes: one dependent load deep instead of one per 8 synapses
+                uint32_t tw[32];  // kt16: 2 entries per word; else 1 entry per word (first 32 synapses)
+                if (a.kt16) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(ktab) + kb + 8 * q);
+                        tw[4 * q] = v.x, tw[4 * q + 1] = v.y, tw[4 * q + 2] = v.z, tw[4 * q + 3] = v.w;
+                    }
+                }
+#pragma unroll
+                for (int q8 = 0; q8 < HK / 8; ++q8) {  // 8 synapses per step
+                    uint32_t te[8];
+                    if (a.kt16) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) te[2 * e] = tw[4 * q8 + e] & 0xFFFFu, te[2 * e + 1] = tw[4 * q8 + e] >> 16;
+                    } else {
+                        const uint4 v0 = *reinterpret_cast<const uint4*>(ktab + kb + 8 * q8);
+                        const uint4 v1 = *reinterpret_cast<const uint4*>(ktab + kb + 8 * q8 + 4);
+                        te[0] = v0.x, te[1] = v0.y, te[2] = v0.z, te[3] = v0.w;
+                        te[4] = v1.x, te[5] = v1.y, te[6] = v1.z, te[7] = v1.w;
+                    }
+                    uint32_t w0 = 0x7F7F7F7Fu, w1 = 0x7F7F7F7Fu;  // never (invalid pixel)
+                    if (pvalid) {
+                        uint32_t bt[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) bt[e] = region[pixbase + (int)te[e]];
+                        w0 = __byte_perm(__byte_perm(bt[0], bt[1], 0x0040), __byte_perm(bt[2], bt[3], 0x0040), 0x5410);
+                        w1 = __byte_perm(__byte_perm(bt[4], bt[5], 0x0040), __byte_perm(bt[6], bt[7], 0x0040), 0x5410);
+                    }
+                    r[2 * q8] = le_bytes80(w0, 0x80808080u);  // 0x80 where the input spikes at the step
+                    r[2 * q8 + 1] = le_bytes80(w1, 0x80808080u);
+                }
+                if (ks + 1 == a.nks && last_use) {  // staged band no longer read by this warp
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(rge0 + 8 * rb);
+                }
+                if (gfirst) rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + gbar, ph ^ 1u, threadIdx.x == 0);
+                tc_fence_after();
+                tmem_st16(trow + (uint32_t)(s * kACols), r);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0 && glast) mbar_arrive(full0 + gbar);
+            }
+        }
+        if (threadIdx.x == 0) rc.store(0);
+    } else if (TP != 1 && warp < kProdWarps) {
         // ======================= producers =======================
         RoleClock rc(a.prof != 0);
         const int quad = warp & 3, half = warp >> 2;
@@ -785,7 +873,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 }
             }
             bool released = false;
-            if (EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 128)) {
+            if (TP == 1 && EPI != SPK_EPI_POTENTIAL) {
+                // one time step: row = pixel, fire iff X > theta (lat 0, else T = 1); P* = potential
+                for (int n0 = eh * 16; n0 < a.Nt; n0 += 32) {
+#pragma unroll
+                    for (int h8 = 0; h8 < 16; h8 += 8) {
+                        uint32_t r[24];
+                        tmem_ld8(tbase + n0 + h8, r);
+                        tmem_ld8(tbase + a.Nt + n0 + h8, r + 8);
+                        tmem_ld8(tbase + 2 * a.Nt + n0 + h8, r + 16);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const long long X = (long long)((unsigned long long)r[16 + j] * 65536ull +
+                                                            ((unsigned long long)r[8 + j] * 256ull + r[j]));
+                            const bool fire = X > thq;
+                            const int ol = ob * a.Nt * PPT + (n0 + h8 + j) * PPT + pix;
+                            ob_lat[ol] = fire ? (uint8_t)0 : (uint8_t)g.T;
+                            if (PSTAR) ob_ps[ol] = fire ? __fmul_rn(__ll2float_rn(X), a.out_scale) : 0.0f;
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acce0 + 8 * buf);
+                released = true;
+            } else if (EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 128)) {
                 // 16-column chunks n0 = eh*16 + 32 i, each read as two 8-column halves; the
                 // TMEM loads of the next half overlap the threshold work on the current one,
                 // and the accumulator is released as soon as its last load has landed
@@ -1061,42 +1174,35 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const int total = g.Ci * a.band;
             if (SPK_EXP & 2048) {  // timing experiment: no input staging (stale region)
             } else if (a.NR == a.HiP) {
-                // whole padded sample: the halo was filled once at kernel start; copy the
-                // interior, one contiguous block of Ci*Hi*Wi bytes, 4 bytes per load when aligned
-                const int n = g.Ci * (int)plane;
-                const float inv_plane = 1.0f / (float)plane, inv_w = 1.0f / (float)g.Wi;
-                auto put = [&](int q, uint32_t v) {  // byte v of interior index q
-                    int c = (int)((float)q * inv_plane);
-                    c -= (c * (int)plane > q);
-                    c += ((c + 1) * (int)plane <= q);
-                    const int rem = q - c * (int)plane;
-                    int iy = (int)((float)rem * inv_w);
-                    iy -= (iy * g.Wi > rem);
-                    iy += ((iy + 1) * g.Wi <= rem);
-                    const int ix = rem - iy * g.Wi;
-                    dst[c * a.band + (iy + g.Ph) * a.WiP + ix + g.Pw] = (uint8_t)min(v, 0x7Fu);
-                };
-                if ((reinterpret_cast<uintptr_t>(src) & 3) == 0) {
-                    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
-                    const int n4 = n >> 2;
-                    for (int q0 = 0; q0 < n4; q0 += kLoaders * kLoadBatch) {
-                        uint32_t v[kLoadBatch];
+                // whole padded sample: the halo was filled once at kernel start; copy the interior
+                // rows, one input row (c, iy) per lane per pass — four rows' loads in flight, 4-byte
+                // loads when the sample is 4-byte aligned (Wi % 4 == 0 keeps every row aligned)
+                const int nrows = g.Ci * g.Hi;
+                const bool al4 = (g.Wi & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 3) == 0;
+                for (int r0 = lt; r0 < nrows; r0 += kLoaders) {
+                    const int c = r0 / g.Hi, iy = r0 - c * g.Hi;
+                    const uint8_t* sr = src + (size_t)r0 * g.Wi;
+                    uint8_t* d = dst + c * a.band + (iy + g.Ph) * a.WiP + g.Pw;
+                    if (al4) {
+                        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(sr);
+                        int x4 = 0;
+                        for (; x4 + 4 <= (g.Wi >> 2); x4 += 4) {
+                            uint32_t v[4];
 #pragma unroll
-                        for (int u = 0; u < kLoadBatch; ++u) {
-                            const int q = q0 + u * kLoaders + lt;
-                            v[u] = q < n4 ? __ldg(s4 + q) : 0u;
+                            for (int u = 0; u < 4; ++u) v[u] = __ldg(s4 + x4 + u);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) d[4 * (x4 + u) + e] = (uint8_t)min((v[u] >> (8 * e)) & 0xFFu, 0x7Fu);
                         }
+                        for (; x4 < (g.Wi >> 2); ++x4) {
+                            const uint32_t v = __ldg(s4 + x4);
 #pragma unroll
-                        for (int u = 0; u < kLoadBatch; ++u) {
-                            const int q = q0 + u * kLoaders + lt;
-                            if (q < n4)
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) put(4 * q + e, (v[u] >> (8 * e)) & 0xFFu);
+                            for (int e = 0; e < 4; ++e) d[4 * x4 + e] = (uint8_t)min((v >> (8 * e)) & 0xFFu, 0x7Fu);
                         }
+                    } else {
+                        for (int x = 0; x < g.Wi; ++x) d[x] = min(__ldg(sr + x), (uint8_t)0x7F);
                     }
-                    for (int q = (n4 << 2) + lt; q < n; q += kLoaders) put(q, __ldg(src + q));
-                } else {
-                    for (int q = lt; q < n; q += kLoaders) put(q, __ldg(src + q));
                 }
             } else {
                 // band of NR padded rows: one padded row (c, r) per thread per pass
@@ -1148,6 +1254,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const uint8_t* sl = ob_lat + ob * a.Nt * PPT;
             const float* sp = ob_ps + ob * a.Nt * PPT;
             const int npix = min(PPT, a.HWo - p0);
+            if (TP == 1) {
+                const int nmap = min(a.Nt, g.Co - nt * a.Nt);
+                for (int ol = 0; ol < nmap; ++ol) {
+                    const size_t oi = ((size_t)b * g.Co + nt * a.Nt + ol) * a.HWo + p0;
+                    uint8_t* dl = static_cast<uint8_t*>(a.out0) + oi;
+                    if (npix == PPT && (reinterpret_cast<uintptr_t>(dl) & 3) == 0) {
+                        reinterpret_cast<uint32_t*>(dl)[lane] = reinterpret_cast<const uint32_t*>(sl + ol * PPT)[lane];
+                    } else {
+                        for (int q = lane; q < npix; q += 32) dl[q] = sl[ol * PPT + q];
+                    }
+                    if (PSTAR)
+                        for (int q = lane; q < npix; q += 32) a.out1[oi + q] = sp[ol * PPT + q];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(fls0 + 8 * ob);
+                ++fl_it;
+                if (++ob == kNOB) ob = 0, ph ^= 1u;
+                continue;
+            }
             for (int ol = lane; ol < a.Nt; ol += 32) {
                 const int o = nt * a.Nt + ol;
                 if (o >= g.Co || (SPK_EXP & 8)) continue;
@@ -1240,12 +1365,13 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     p.Wo = (g.Wi + 2 * g.Pw - g.Kw) / g.Sw + 1;
     p.K = g.Ci * g.Kh * g.Kw;
     if (g.T > 32 || p.K > kTcMaxK || g.Kh > 16 || g.Kw > 16) return false;
-    if ((long long)g.B * ((p.Ho * p.Wo + 128 / (g.T <= 16 ? 16 : 32) - 1) / (128 / (g.T <= 16 ? 16 : 32))) * 4 >= (1ll << 31))
+    // rows of an M tile: (pixel, t) with t padded to 16 or 32; one time step (T = 1): pixels only
+    p.TP = g.T == 1 ? 1 : g.T <= 16 ? 16 : 32;
+    p.PPT = 128 / p.TP;
+    if ((long long)g.B * ((p.Ho * p.Wo + p.PPT - 1) / p.PPT) * 4 >= (1ll << 31))
         return false;  // tile indices are 32-bit
     p.KS = KS;
     p.nks = (p.K + KS - 1) / KS;
-    p.TP = g.T <= 16 ? 16 : 32;
-    p.PPT = 128 / p.TP;
     // N tiling: accumulators (3 digit planes) + the TMEM A ring share 512 columns; at least
     // 4 A slots, at most 2 accumulator buffers, every remaining column to the A ring
     const int acc_cols = 512 - 4 * kACols;  // 384
@@ -1262,6 +1388,9 @@ bool tc_plan(const spk_conv_geom& g, TcPlan& p) {
     }();
     if (nt_force >= 16 && nt_force % 16 == 0 && nt_force <= 128) {
         p.Nt = nt_force;
+    } else if (p.TP == 1) {
+        p.Nt = std::min(32, ((g.Co + 15) / 16) * 16);  // output staging of 128-pixel rows: 32 maps per tile
+        p.retain = p.retain && g.Co > 32;
     } else if (p.retain) {
         p.Nt = 64;
     } else if (g.Co <= 64) {
@@ -1418,7 +1547,8 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     a.ob_off = (a.rg_off + (uint32_t)(p.nrb * p.rb_stride) + 15u) & ~15u;
     a.bar_off = (a.ob_off + (uint32_t)(kNOB * p.Nt * p.PPT * 5) + 15u) & ~15u;
     const long long grid = p.total_tiles < spk::sm_count() ? p.total_tiles : spk::sm_count();
-    if (p.TP == 16) launch_tp<16>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
+    if (p.TP == 1) launch_tp<1>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
+    else if (p.TP == 16) launch_tp<16>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
     else launch_tp<32>(a, epi, out1 != nullptr, (unsigned)grid, p.smem_bytes, s);
     return spk::launched("conv_tc_kernel");
 }

@@ -107,6 +107,23 @@ __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) 
             }
             emit(key, key != ~0ull);
         }
+    } else if (a.mode == 3) {
+        // fused inhibition on a small slice (C2 layer 3: 16 pixels x 200 maps): the per-pixel
+        // minimum key (the inhibition survivor) with channel groups in parallel — thread q takes
+        // pixel q % np and channels q / np, q / np + ng, ... — combined by a shared 64-bit atomicMin
+        for (int q = threadIdx.x; q < np_slice; q += kThreads) keys[q] = ~0ull;
+        __syncthreads();
+        const int ng = kThreads / np_slice;
+        const int pp = threadIdx.x % np_slice, gq = threadIdx.x / np_slice;
+        if (gq < ng) {
+            unsigned long long m = ~0ull;
+            for (int c = gq; c < a.C; c += ng) m = umin64(m, wta_key(L, P, c * HW + p_lo + pp, T));
+            if (m != ~0ull) atomicMin(&keys[pp], m);
+        }
+        __syncthreads();
+        const unsigned long long key = threadIdx.x < np_slice ? keys[threadIdx.x] : ~0ull;
+        __syncthreads();
+        emit(key, key != ~0ull);  // np_slice <= kThreads / 2: one pass compacts every survivor
     } else if (a.mode == 1) {
         for (int q0 = 0; q0 < np_slice; q0 += kThreads) {
             const int p = p_lo + q0 + threadIdx.x;
@@ -313,7 +330,7 @@ static spk_status wta_impl(const uint8_t* lat, const float* pstar, int B, int C,
         SPK_CHECK(slice_p <= kCapKeys, SPK_ERR_UNSUPPORTED,
                   "fused inhibit+WTA needs <= %d pixels per CTA slice (H*W=%lld); call spk_inhibit + spk_wta",
                   kCapKeys, HW);
-        a.mode = 1;
+        a.mode = slice_p * 2 <= kThreads ? 3 : 1;  // small slices: channel groups in parallel
         a.cap = (unsigned)slice_p;
         return launch_wta<1>(a, B, (size_t)slice_p, spk::as_cuda(stream));
     }

@@ -298,8 +298,8 @@ class RateNetwork:
             Wo = (w + 2 * L["pad"] - L["K"]) // L["stride"] + 1
             g = spk.ConvGeom(batch * T, 1, ci, h, w, L["Co"], L["K"], L["K"], L["stride"], L["stride"], L["pad"], L["pad"])
             lp = prec
-            if prec == "auto":  # the event form where its weight block fits (sparse per-step spikes)
-                lp = "event" if spk.conv_workspace(g, "event") > 0 else "exact"
+            if prec == "auto":  # one time step per row on the tensor cores (TP = 1), else the event form
+                lp = "exact" if spk.conv_workspace(g, "exact") > 0 else "event"
             rec = dict(L=L, geom=g, prec=lp, Ho=Ho, Wo=Wo,
                        step=torch.empty((batch, T, L["Co"], Ho, Wo), dtype=torch.uint8, device=self.dev),
                        ws=torch.empty(max(1, spk.conv_workspace(g, lp)), dtype=torch.uint8, device=self.dev))

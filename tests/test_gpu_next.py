@@ -53,19 +53,24 @@ def test_rate_gather_and_pool_rates_exact(spk):
 
 
 @pytest.mark.parametrize("prec", ["event", "exact"])
-def test_rate_coded_conv_fire_per_step(spk, prec):
+@pytest.mark.parametrize("shape", [(2, 20, 6, 12, 13, 25, 5), (3, 9, 25, 14, 14, 50, 3), (1, 40, 6, 28, 28, 25, 5),
+                                   (2, 5, 30, 9, 11, 70, 3)])
+def test_rate_coded_conv_fire_per_step(spk, prec, shape):
     """Eq. 2 per step on non-cumulative trains: spk_conv on the step map with B' = B*T, T' = 1
-    equals the oracle's direct BTCHW conv (potentials) and its per-step fire (spikes)."""
-    B, T, Ci, H, W, Co, K = 2, 20, 6, 12, 13, 25, 5
+    (tensor path: one time step per row, 128 pixels per M tile) equals the oracle's direct BTCHW
+    conv (potentials) and its per-step fire (spikes), P* included."""
+    B, T, Ci, H, W, Co, K = shape
     S = (RNG.random((B, T, Ci, H, W)) < 0.25).astype(np.uint8)
     w = oracle.quantize(RNG.uniform(0, 1, (Co, Ci, K, K)).astype(np.float32), 0, 0.5, 1)
-    P = oracle.conv(S, w, (1, 1), (2, 2))
+    P = oracle.conv(S, w, (1, 1), ((K - 1) // 2,) * 2)
     x = cu((1 - S).reshape(B * T, Ci, H, W))
-    got = host(spk.conv(x, cu(w), 1, 1, 2, prec=prec, epi="potential")).reshape(P.shape)
+    got = host(spk.conv(x, cu(w), 1, 1, (K - 1) // 2, prec=prec, epi="potential")).reshape(P.shape)
     np.testing.assert_array_equal(got, P)  # binary weights: exact integers on every engine
-    theta = 13.0
-    lat, _ = spk.conv(x, cu(w), 1, 1, 2, prec=prec, epi="fire", theta=theta)
-    np.testing.assert_array_equal(host(lat).reshape(B, T, Co, H, W), 1 - oracle.fire(P, theta))
+    theta = float(np.percentile(P, 80)) + 0.5
+    lat, ps = spk.conv(x, cu(w), 1, 1, (K - 1) // 2, prec=prec, epi="fire", theta=theta)
+    S = oracle.fire(P, theta)
+    np.testing.assert_array_equal(host(lat).reshape(B, T, Co, H, W), 1 - S)
+    np.testing.assert_array_equal(host(ps).reshape(B, T, Co, H, W), np.where(S == 1, P, 0).astype(np.float32))
 
 
 def test_rate_pipeline_c6(spk):
