@@ -155,14 +155,91 @@ static spk_conv_geom fc_geom(int B, int T, int I, int O) {
     return g;
 }
 
+// EXACT_I8 with T > 1: the samples become the pixels of ONE image (Bp = B rounded up to 8 pixels,
+// laid out as Bp/8 rows of 8), so an M tile holds 8 samples x 16 steps instead of one sample's
+// single pixel: the input is transposed to channel-major [I][Bp] ("never" in the padding), the
+// 1x1 conv writes [O][Bp], and the records are transposed back to [B][O].
+static bool fc_batched(int B, int T, spk_precision prec) { return prec == SPK_PREC_EXACT_I8 && T > 1 && B >= 8; }
+
+static spk_conv_geom fc_geom_batched(int B, int T, int I, int O) {
+    spk_conv_geom g = fc_geom(1, T, I, O);
+    const int Bp = (B + 7) / 8 * 8;
+    g.Hi = Bp / 8;
+    g.Wi = 8;
+    return g;
+}
+
+static size_t fc_conv_ws(const spk_conv_geom& g) { return (spk_conv_workspace(&g, SPK_PREC_EXACT_I8) + 255) / 256 * 256; }
+
 extern "C" size_t spk_fc_workspace(int B, int T, int I, int O, spk_precision prec) {
+    if (B < 1 || T < 1 || I < 1 || O < 1) return 0;
+    if (fc_batched(B, T, prec)) {
+        const spk_conv_geom g = fc_geom_batched(B, T, I, O);
+        const size_t cw = fc_conv_ws(g);
+        if (cw == 0) return 0;
+        const size_t Bp = (size_t)(B + 7) / 8 * 8;
+        return cw + (size_t)I * Bp + (size_t)O * Bp * 5 + 256;
+    }
     const spk_conv_geom g = fc_geom(B, T, I, O);
     return spk_conv_workspace(&g, prec);
 }
 
+namespace {
+// out[c * ldo + r] = in[r * ldi + c] for r < R, c < C, `pad` elsewhere; c < Cout, r < Rout
+// (32 x 32 tiles through shared memory)
+template <typename E>
+__global__ void transpose_kernel(const E* __restrict__ in, int R, int C, int ldi, int Cout, int Rout, E pad,
+                                 E* __restrict__ out, int ldo) {
+    __shared__ E tile[32][33];
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < R && c < C) ? in[(size_t)r * ldi + c] : pad;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (c < Cout && r < Rout) out[(size_t)c * ldo + r] = tile[threadIdx.x][i];
+    }
+}
+
+template <typename E>
+spk_status transpose(const E* in, int R, int C, int ldi, int Cout, int Rout, E pad, E* out, int ldo, cudaStream_t s) {
+    const dim3 grid(spk::ceil_div(Cout, 32), spk::ceil_div(Rout, 32)), block(32, 8);
+    transpose_kernel<E><<<grid, block, 0, s>>>(in, R, C, ldi, Cout, Rout, pad, out, ldo);
+    return spk::launched("transpose_kernel");
+}
+}  // namespace
+
 extern "C" spk_status spk_fc(const uint8_t* lat_in, const float* w, int B, int T, int I, int O, spk_precision prec,
                              spk_epilogue epi, float theta, float w_max, void* out0, void* out1, void* ws,
                              size_t ws_bytes, spk_stream stream) {
-    const spk_conv_geom g = fc_geom(B, T, I, O);
-    return spk_conv(lat_in, w, &g, prec, epi, theta, w_max, out0, out1, ws, ws_bytes, stream);
+    if (!fc_batched(B, T, prec) || epi != SPK_EPI_FIRE) {
+        const spk_conv_geom g = fc_geom(B, T, I, O);
+        return spk_conv(lat_in, w, &g, prec, epi, theta, w_max, out0, out1, ws, ws_bytes, stream);
+    }
+    spk::clear_error();
+    SPK_CHECK_PTR(lat_in);
+    SPK_CHECK_PTR(out0);
+    SPK_CHECK(T <= 254, SPK_ERR_UNSUPPORTED, "T=%d > 254 (u8 latency)", T);
+    const spk_conv_geom g = fc_geom_batched(B, T, I, O);
+    const size_t cw = fc_conv_ws(g);
+    const size_t need = spk_fc_workspace(B, T, I, O, prec);
+    SPK_CHECK(cw > 0 && need > 0, SPK_ERR_UNSUPPORTED, "EXACT_I8 FC geometry not supported (I=%d)", I);
+    SPK_CHECK(ws != nullptr && ws_bytes >= need, SPK_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+    const int Bp = (B + 7) / 8 * 8;
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    uint8_t* lat_t = base + cw;                          // [I][Bp]
+    uint8_t* lo_t = lat_t + (size_t)I * Bp;              // [O][Bp]
+    float* ps_t = reinterpret_cast<float*>(lo_t + (size_t)O * Bp);  // [O][Bp]
+    cudaStream_t s = spk::as_cuda(stream);
+    // [B][I] -> [I][Bp]; the padding samples never fire
+    spk_status st = transpose<uint8_t>(lat_in, B, I, I, I, Bp, (uint8_t)T, lat_t, Bp, s);
+    if (st != SPK_OK) return st;
+    st = spk_conv(lat_t, w, &g, SPK_PREC_EXACT_I8, SPK_EPI_FIRE, theta, w_max, lo_t, out1 ? ps_t : nullptr, base, cw,
+                  stream);
+    if (st != SPK_OK) return st;
+    st = transpose<uint8_t>(lo_t, O, Bp, Bp, B, O, 0, static_cast<uint8_t*>(out0), O, s);  // [O][Bp] -> [B][O]
+    if (st != SPK_OK || !out1) return st;
+    return transpose<float>(ps_t, O, Bp, Bp, B, O, 0.0f, static_cast<float*>(out1), O, s);
 }

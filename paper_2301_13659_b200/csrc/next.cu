@@ -17,16 +17,6 @@ namespace {
 
 constexpr int kT = 256;
 
-// ------------------------------------------------------------ counter-based stream
-// value `c` of stream `seed`: splitmix64 output for the state seed + (c + 1) * golden
-// (DESIGN R-RATE-RNG; the oracle implements the same definition independently)
-__device__ __forceinline__ uint64_t mix64(uint64_t seed, uint64_t c) {
-    uint64_t z = seed + (c + 1ull) * 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
 // ------------------------------------------------------------ rate coding
 // pass 1: per-sample maximum of the thresholded values (positive floats order like their
 // bits, so an integer atomicMax on the bit pattern is exact and order-independent)
@@ -51,37 +41,55 @@ __global__ void __launch_bounds__(kT) rate_max_kernel(const float* __restrict__ 
 }
 
 // pass 2: step map out[b][t][i] = 0 if u24(b, t, i) * 2^-24 < p_i else 1, p_i = min(1, v_i / vmax)
-// (fp32 IEEE division, as the oracle).  4 neurons per thread, grid (i-chunks, t, b).
+// (fp32 IEEE division, as the oracle).  A thread owns 4 consecutive neurons of one sample and walks
+// the T steps: p is divided once per neuron, and the generator state of step t+1 is that of step t
+// plus N golden increments (the counter advances by N per step), so a draw costs the two
+// multiply-xorshift rounds of the mix only.  One 4-byte coalesced store per step.
+__device__ __forceinline__ uint64_t mix_state(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 __global__ void __launch_bounds__(kT) rate_emit_kernel(const float* __restrict__ y, int N, int T, float thresh,
                                                        uint64_t seed, uint64_t b0, const unsigned* __restrict__ vmax_bits,
                                                        uint8_t* __restrict__ out) {
-    const int b = blockIdx.z, t = blockIdx.y;
+    const int b = blockIdx.y;
     const int i0 = (blockIdx.x * kT + threadIdx.x) * 4;
     if (i0 >= N) return;
     const float vmax = __uint_as_float(vmax_bits[b]);
     const float* v = y + (size_t)b * N;
-    const uint64_t row = (uint64_t)b * (uint64_t)T + (uint64_t)t;
-    const uint64_t c0 = ((b0 + (uint64_t)b) * (uint64_t)T + (uint64_t)t) * (uint64_t)N;  // global sample
-    uint8_t* o = out + row * (uint64_t)N;
-    uint32_t word = 0;
     const int n = min(4, N - i0);
+    float p[4];
+    uint64_t z[4];  // splitmix64 state of step 0: seed + (counter + 1) * golden
+    const uint64_t c0 = (b0 + (uint64_t)b) * (uint64_t)T * (uint64_t)N;  // counter of (global sample, t = 0, i = 0)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        uint32_t bit = 1u;  // 1 = no spike
+        p[e] = 0.0f;
         if (e < n) {
             const float x = __ldg(v + i0 + e);
-            float p = 0.0f;
-            if (vmax > 0.0f && x > thresh) p = fminf(__fdiv_rn(x, vmax), 1.0f);
-            const uint32_t u24 = (uint32_t)(mix64(seed, c0 + (uint64_t)(i0 + e)) >> 40);
-            const float u = __fmul_rn((float)u24, 5.9604644775390625e-8f);  // exact: 24-bit integer * 2^-24
-            bit = (u < p) ? 0u : 1u;
+            if (vmax > 0.0f && x > thresh) p[e] = fminf(__fdiv_rn(x, vmax), 1.0f);
         }
-        word |= bit << (8 * e);
+        z[e] = seed + (c0 + (uint64_t)(i0 + e) + 1ull) * 0x9E3779B97F4A7C15ull;
     }
-    if (n == 4 && ((reinterpret_cast<uintptr_t>(o + i0) & 3) == 0)) {
-        *reinterpret_cast<uint32_t*>(o + i0) = word;
-    } else {
-        for (int e = 0; e < n; ++e) o[i0 + e] = (uint8_t)((word >> (8 * e)) & 0xFFu);
+    const uint64_t step = (uint64_t)N * 0x9E3779B97F4A7C15ull;
+    uint8_t* o = out + (size_t)b * T * N + i0;
+    const bool vec = n == 4 && ((reinterpret_cast<uintptr_t>(o) & 3) == 0) && (N & 3) == 0;
+    for (int t = 0; t < T; ++t) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t u24 = (uint32_t)(mix_state(z[e]) >> 40);
+            const float u = __fmul_rn((float)u24, 5.9604644775390625e-8f);  // exact: 24-bit integer * 2^-24
+            word |= ((u < p[e]) ? 0u : 1u) << (8 * e);
+            z[e] += step;
+        }
+        uint8_t* ot = o + (size_t)t * N;
+        if (vec) {
+            *reinterpret_cast<uint32_t*>(ot) = word;
+        } else {
+            for (int e = 0; e < n; ++e) ot[e] = (uint8_t)((word >> (8 * e)) & 0xFFu);
+        }
     }
 }
 
@@ -248,7 +256,7 @@ extern "C" spk_status spk_rate_code(const float* y, int B, int N, int T, float t
     spk_status st = spk::launched("rate_max_kernel");
     if (st != SPK_OK) return st;
     const unsigned gx = spk::ceil_div((size_t)(N + 3) / 4, kT);
-    rate_emit_kernel<<<dim3(gx, T, B), kT, 0, s>>>(y, N, T, thresh, seed, b0, vmax, step);
+    rate_emit_kernel<<<dim3(gx, B), kT, 0, s>>>(y, N, T, thresh, seed, b0, vmax, step);
     return spk::launched("rate_emit_kernel");
 }
 

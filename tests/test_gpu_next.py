@@ -134,7 +134,8 @@ def test_quantize_exact(spk):
 
 
 @pytest.mark.parametrize("prec", ["exact", "event", "fp32"])
-@pytest.mark.parametrize("B,T,I,O", [(5, 15, 300, 40), (3, 30, 1000, 10), (2, 1, 17, 3)])
+@pytest.mark.parametrize("B,T,I,O", [(5, 15, 300, 40), (3, 30, 1000, 10), (2, 1, 17, 3), (37, 15, 3200, 200),
+                                     (64, 30, 1000, 10), (8, 2, 17, 3)])
 def test_fc_potentials_and_fire(spk, prec, B, T, I, O):
     lat = RNG.integers(0, T + 1, (B, I)).astype(np.uint8)
     W = RNG.uniform(0, 1, (I, O)).astype(np.float32)  # the paper's I x O kernel
@@ -175,8 +176,9 @@ def test_fcwta_exact(spk, O, k, r):
 
 def test_fc_train_step_fire_fcwta_stdp(spk):
     """An FC layer's training step (Listing 3 with fc + fcwta): fire -> fcwta -> STDP on the
-    1x1 geometry == oracle fc -> threshold -> fcwta -> fc_stdp (I x O weights), bit for bit."""
-    B, T, I, O = 6, 15, 800, 50
+    1x1 geometry == oracle fc -> threshold -> fcwta -> fc_stdp (I x O weights), bit for bit
+    (B = 21: the batched tensor path, samples as the pixels of one image)."""
+    B, T, I, O = 21, 15, 800, 50
     lat = RNG.integers(0, T + 1, (B, I)).astype(np.uint8)
     W = np.clip(RNG.normal(0.5, 0.05, (I, O)), 0, 1).astype(np.float32)
     S = oracle.lat_to_dense(lat, T)
@@ -184,9 +186,9 @@ def test_fc_train_step_fire_fcwta_stdp(spk):
     # a threshold in the middle of a gap of the potentials around their 70th percentile, so no
     # potential lies within the near-threshold band (the comparison below is then all exact)
     v = np.unique(P.ravel())
-    i0 = np.searchsorted(v, np.percentile(P[:, -1], 70))
-    gaps = [(v[i + 1] - v[i], i) for i in range(max(0, i0 - 200), min(len(v) - 1, i0 + 200))]
-    _, i = max(gaps)
+    target = np.percentile(P[:, -1], 70)
+    ok = [i for i in range(len(v) - 1) if v[i + 1] - v[i] > 3e-4 * (v[i] + v[i + 1]) / 2 and v[i] > 0]
+    i = min(ok, key=lambda q: abs(v[q] - target))  # the clear gap nearest the 70th percentile
     theta = float((v[i] + v[i + 1]) / 2)
     Q = oracle.threshold(P, theta)
     win, nwin = oracle.fcwta(Q, 3, 2)

@@ -228,6 +228,22 @@ def test_fire_exact(spk):
     np.testing.assert_array_equal(host(ps), rp.astype(np.float32))
 
 
+@pytest.mark.parametrize("T", [1, 7, 15, 30])
+@pytest.mark.parametrize("monotone", [True, False])
+def test_fire_vectorised_exact(spk, T, monotone):
+    """The 4-neurons-per-thread kernel (N % 4 == 0): first strict crossing and P*, including
+    non-monotone potentials (the first crossing, not the last) and never-firing neurons."""
+    P = RNG.uniform(0, 2, (3, T, 8, 9, 12))
+    if monotone:
+        P = np.cumsum(P, axis=1)
+    P = P.astype(np.float32)
+    theta = float(np.percentile(P, 60))
+    lat, ps = spk.fire(cu(P), theta)
+    rl, rp = lat_and_pstar(P.astype(np.float64), theta)
+    np.testing.assert_array_equal(host(lat), rl)
+    np.testing.assert_array_equal(host(ps), rp.astype(np.float32))
+
+
 # ------------------------------------------------------------------------- a5 pool
 @pytest.mark.parametrize("L,s,p", [(2, 2, 0), (3, 3, 0), (3, 2, 1), (2, 1, 1), (4, 4, 2)])
 def test_pool_exact(spk, L, s, p):
