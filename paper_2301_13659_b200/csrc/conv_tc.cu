@@ -46,6 +46,9 @@
 
 #include "conv.cuh"
 
+#ifndef SPK_MMA_FAST
+#define SPK_MMA_FAST 1  // retained-A N tiles after the first issue all K stages after one wait (C2 conv1 1.08 -> 1.01 ms)
+#endif
 #ifndef SPK_EXP
 #define SPK_EXP 0  // timing experiments only: 1 no wait::st, 2 no gather, 4 no tcgen05.st, 8 no epilogue stores,
                    // 16 no epilogue tcgen05.ld, 32 no MMA, 512 no fire-epilogue TMEM loads,
@@ -1028,6 +1031,42 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 int s = as_cur;  // slot group (G slots per hand-off)
                 uint32_t aph = aph_cur;
                 const int ngrp = a.NA / a.G;
+#if SPK_MMA_FAST
+                // retained A already in TMEM and this tile's weights in one hand-off: every K stage
+                // of the tile is issued back to back after one wait (no per-stage fence or probes)
+                if (a.retain && !newA && (a.bres || a.GB == a.nks) && !(SPK_EXP & 32)) {
+                    rc.wait3(bfull0 + 8 * bs, b_ph, !a.bres && !(SPK_EXP & 4096), acce0 + 8 * buf, acc_ph ^ 1u, wacc);
+                    tc_fence_after();
+                    const uint64_t dst0 = d0 + (((a.bres ? 0u : (uint32_t)(bs * a.GB)) * bstage) >> 4);
+                    const uint32_t eA = dbase + pA * a.Nt, eB = dbase + pB * a.Nt;
+                    const uint32_t two = nB ? 1u : 0u;
+                    for (int ks = 0; ks < a.nks; ks += a.G) {
+                        if (ks) {
+                            if (++s == ngrp) s = 0, aph ^= 1u;
+                        }
+                        const uint64_t dst = dst0 + (((uint32_t)ks * bstage) >> 4);
+                        const uint32_t at = tmem + (uint32_t)(a.aCol0 + s * a.G * kACols);
+                        const int nk = min(a.G * (KS / 32), (a.K - ks * KS + 31) / 32);
+                        const uint32_t acc0 = ks ? 1u : 0u;
+                        const uint64_t xA = dst + incd * pA, xB = dst + incd * pB;
+                        if (nk == 4) {
+                            tc_stage_gen<4>(eA, eB, at, xA, xB, inck, idA, idB, acc0, two);
+                        } else if (nk == 8) {
+                            tc_stage_gen<8>(eA, eB, at, xA, xB, inck, idA, idB, acc0, two);
+                        } else {
+#pragma unroll 1
+                            for (int kk = 0; kk < nk; ++kk)
+                                tc_stage_gen<1>(eA, eB, at + 8u * kk, xA + inck * kk, xB + inck * kk, inck, idA, idB,
+                                                kk ? 1u : acc0, two);
+                        }
+                        if (lastA && !(SPK_EXP & 16384)) tc_commit_elect(empty0 + 8 * s);
+                    }
+                    if (!a.bres && !(SPK_EXP & 4096)) {
+                        tc_commit_elect(bempty0 + 8 * bs);
+                        if (++bs == a.NS) bs = 0, b_ph ^= 1u;
+                    }
+                } else
+#endif
                 for (int ks = 0; ks < a.nks; ks += a.G) {
                     if (ks) {
                         if (++s == ngrp) s = 0, aph ^= 1u;
