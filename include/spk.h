@@ -83,6 +83,14 @@ SPK_API uint64_t spk_launch_count(void);
 SPK_API spk_status spk_dog(const uint8_t* img, int B, int C, int H, int W, const double* sigmas, int K,
                    int radius, int pad, float* y, spk_stream stream);
 
+/* spk_log — Laplacian-of-Gaussian bank `spyker.LoG(size, stds, pad)`: each
+ * std sigma contributes the pair DoG(sigma*sqrt2, sigma/sqrt2), DoG(sigma/sqrt2, sigma*sqrt2),
+ * in std-list order (R-CHORDER), so K = 2n output channels per input channel.
+ *   stds [host] double [n], each > 0, 1 <= n <= 1024.  Other arguments, layout and
+ * errors as spk_dog. */
+SPK_API spk_status spk_log(const uint8_t* img, int B, int C, int H, int W, const double* stds, int n,
+                           int radius, int pad, float* y, spk_stream stream);
+
 /* spk_gabor — Gabor filter bank: params [host] double [K][5] =
  * (sigma, theta, gamma, lambda, psi); g = exp(-(x'^2 + gamma^2 y'^2)/(2 sigma^2))
  * * cos(2 pi x'/lambda + psi), x' = x cos theta + y sin theta,

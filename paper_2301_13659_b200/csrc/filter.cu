@@ -280,6 +280,26 @@ extern "C" spk_status spk_dog(const uint8_t* img, int B, int C, int H, int W, co
     return run_filter(img, B, C, H, W, coef, K, radius, pad, y, stream);
 }
 
+// LoG(sigma) ~ {DoG(sigma*sqrt2, sigma/sqrt2), DoG(sigma/sqrt2, sigma*sqrt2)}: the
+// pair expansion of `spyker.LoG(size, stds, pad)` is part of the definition, so it lives here,
+// behind the ABI, in the std-list order of R-CHORDER.
+extern "C" spk_status spk_log(const uint8_t* img, int B, int C, int H, int W, const double* stds, int n,
+                              int radius, int pad, float* y, spk_stream stream) {
+    spk::clear_error();
+    SPK_CHECK_PTR(stds);
+    SPK_CHECK(n >= 1 && n <= 1024, SPK_ERR_ARG, "need 1..1024 LoG standard deviations");
+    std::vector<double> pairs((size_t)4 * n);
+    const double r2 = std::sqrt(2.0);
+    for (int q = 0; q < n; ++q) {
+        SPK_CHECK(stds[q] > 0 && std::isfinite(stds[q]), SPK_ERR_ARG, "LoG std %d must be positive", q);
+        pairs[4 * q + 0] = stds[q] * r2;
+        pairs[4 * q + 1] = stds[q] / r2;
+        pairs[4 * q + 2] = stds[q] / r2;
+        pairs[4 * q + 3] = stds[q] * r2;
+    }
+    return spk_dog(img, B, C, H, W, pairs.data(), 2 * n, radius, pad, y, stream);
+}
+
 extern "C" spk_status spk_gabor(const uint8_t* img, int B, int C, int H, int W, const double* params,
                                 int K, int radius, int pad, float* y, spk_stream stream) {
     spk::clear_error();

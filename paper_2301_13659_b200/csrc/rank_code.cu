@@ -17,6 +17,9 @@
 
 namespace {
 
+#ifndef SPK_RANK_RUNS
+#define SPK_RANK_RUNS 0  // 1: pass-1 histogram atomics aggregated over runs of equal buckets
+#endif
 constexpr int kGroup = 16;                    // boundary targets resolved per sweep
 constexpr int kStageMax = 40 * 1024;          // values staged in smem up to this many
 
@@ -324,10 +327,32 @@ __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __rest
                 const unsigned int u0 = thr_bits(v[u].x, thresh), u1 = thr_bits(v[u].y, thresh),
                                    u2 = thr_bits(v[u].z, thresh), u3 = thr_bits(v[u].w, thresh);
                 if (STAGE) reinterpret_cast<uint4*>(vals)[q0 + u * kHT] = make_uint4(u0, u1, u2, u3);
+#if SPK_RANK_RUNS
+                // neighbouring values usually share a bucket: one atomic per run of equal buckets
+                {
+                    const unsigned int b0 = u0 ? (u0 >> SHIFT) : 0xFFFFFFFFu, b1 = u1 ? (u1 >> SHIFT) : 0xFFFFFFFFu,
+                                       b2 = u2 ? (u2 >> SHIFT) : 0xFFFFFFFFu, b3 = u3 ? (u3 >> SHIFT) : 0xFFFFFFFFu;
+                    unsigned int cur = b0, n = u0 ? 1u : 0u;
+                    auto push = [&](unsigned int b, bool live) {
+                        if (b == cur) {
+                            n += live;
+                        } else {
+                            if (n) atomicAdd(&tab[cur], n);
+                            cur = b;
+                            n = live;
+                        }
+                    };
+                    push(b1, u1 != 0);
+                    push(b2, u2 != 0);
+                    push(b3, u3 != 0);
+                    if (n) atomicAdd(&tab[cur], n);
+                }
+#else
                 if (u0) atomicAdd(&tab[u0 >> SHIFT], 1u);
                 if (u1) atomicAdd(&tab[u1 >> SHIFT], 1u);
                 if (u2) atomicAdd(&tab[u2 >> SHIFT], 1u);
                 if (u3) atomicAdd(&tab[u3 >> SHIFT], 1u);
+#endif
             }
         }
     } else {

@@ -76,7 +76,11 @@ __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) 
     const int lane = threadIdx.x & 31;
     const uint8_t* L = a.lat + (size_t)b * N;
     const float* P = a.pstar + (size_t)b * N;
-    const int p_lo = (int)((long long)HW * rank / a.cs), p_hi = (int)((long long)HW * (rank + 1) / a.cs);
+    int p_lo = (int)((long long)HW * rank / a.cs), p_hi = (int)((long long)HW * (rank + 1) / a.cs);
+    if (a.mode == 4) {  // 4-pixel aligned slices (HW % 4 == 0)
+        p_lo = (int)((long long)(HW >> 2) * rank / a.cs) * 4;
+        p_hi = (int)((long long)(HW >> 2) * (rank + 1) / a.cs) * 4;
+    }
     const int np_slice = p_hi - p_lo;
     if (threadIdx.x == 0) {
         nkeys = 0;
@@ -106,6 +110,50 @@ __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) 
                 key = wta_key(L, P, c * HW + p, T);
             }
             emit(key, key != ~0ull);
+        }
+    } else if (a.mode == 4) {
+        // fused inhibition on a large slice, 4 pixels per thread: the latencies of 4 neighbouring
+        // pixels of a channel are one 4-byte load (8 channels in flight), P* is read as one float4
+        // only when one of them fired; the per-pixel minimum key is the inhibition survivor
+        const int q_lo = p_lo >> 2, q_hi = p_hi >> 2;  // slices are 4-pixel aligned in this mode
+        constexpr int kC4 = 8;
+        const int iters = (q_hi - q_lo + kThreads - 1) / kThreads;  // the same count in every thread (emit)
+        for (int it = 0; it < iters; ++it) {
+            const int q = q_lo + it * kThreads + (int)threadIdx.x;
+            unsigned long long best[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+            const bool qv = q < q_hi;
+            if (qv) {
+                int c = 0;
+                for (; c < a.C; c += kC4) {
+                    uint32_t w[kC4];
+#pragma unroll
+                    for (int u = 0; u < kC4; ++u)
+                        w[u] = (c + u < a.C) ? __ldg(reinterpret_cast<const uint32_t*>(L + (size_t)(c + u) * HW) + q)
+                                             : 0xFFFFFFFFu;
+#pragma unroll
+                    for (int u = 0; u < kC4; ++u) {
+                        const uint32_t lw = w[u];
+                        const bool any = ((lw & 0xFFu) < (uint32_t)T) || (((lw >> 8) & 0xFFu) < (uint32_t)T) ||
+                                         (((lw >> 16) & 0xFFu) < (uint32_t)T) || ((lw >> 24) < (uint32_t)T);
+                        if (!any) continue;
+                        const int i0 = (c + u) * HW + 4 * q;
+                        const float4 pv = __ldg(reinterpret_cast<const float4*>(P + i0));
+                        const float pe[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint32_t l = (lw >> (8 * e)) & 0xFFu;
+                            if (l < (uint32_t)T) {
+                                const unsigned long long key = ((unsigned long long)l << 56) |
+                                                               ((unsigned long long)(~spk_float_order_u32(pe[e])) << 24) |
+                                                               (unsigned long long)(i0 + e);
+                                best[e] = umin64(best[e], key);
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) emit(best[e], best[e] != ~0ull);
         }
     } else if (a.mode == 3) {
         // fused inhibition on a small slice (C2 layer 3: 16 pixels x 200 maps): the per-pixel
@@ -330,7 +378,15 @@ static spk_status wta_impl(const uint8_t* lat, const float* pstar, int B, int C,
         SPK_CHECK(slice_p <= kCapKeys, SPK_ERR_UNSUPPORTED,
                   "fused inhibit+WTA needs <= %d pixels per CTA slice (H*W=%lld); call spk_inhibit + spk_wta",
                   kCapKeys, HW);
-        a.mode = slice_p * 2 <= kThreads ? 3 : 1;  // small slices: channel groups in parallel
+        const bool vec4 = (HW & 3) == 0 && (reinterpret_cast<uintptr_t>(lat) & 3) == 0 &&
+                          (reinterpret_cast<uintptr_t>(pstar) & 15) == 0;
+        // small slices: channel groups in parallel; large ones: 4 pixels per thread when aligned
+        const long long q_slice = ((HW >> 2) + a.cs - 1) / a.cs;
+        a.mode = slice_p * 2 <= kThreads ? 3 : (vec4 && q_slice * 4 <= kCapKeys) ? 4 : 1;
+        if (a.mode == 4) {
+            a.cap = (unsigned)(q_slice * 4);
+            return launch_wta<1>(a, B, (size_t)(q_slice * 4), spk::as_cuda(stream));
+        }
         a.cap = (unsigned)slice_p;
         return launch_wta<1>(a, B, (size_t)slice_p, spk::as_cuda(stream));
     }

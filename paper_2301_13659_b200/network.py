@@ -40,10 +40,10 @@ class Network:
         if fr["kind"] == "dog":
             self.filters = ("dog", [tuple(p) for p in fr["pairs"]])
         elif fr["kind"] == "log":
-            self.filters = ("dog", spk.log_pairs(fr["stds"]))
+            self.filters = ("log", [float(v) for v in fr["stds"]])
         else:
             self.filters = ("gabor", [tuple(p) for p in fr["params"]])
-        K = len(self.filters[1])
+        K = len(self.filters[1]) * (2 if self.filters[0] == "log" else 1)
         e = 2 * fr["radius"] + 1
         H, W = im["H"] + 2 * fr["pad"] - e + 1, im["W"] + 2 * fr["pad"] - e + 1
         self.y = torch.empty((batch, im["C"] * K, H, W), dtype=torch.float32, device=self.dev)
@@ -154,6 +154,8 @@ class Network:
         kind, filt = self.filters
         if kind == "dog":
             spk.dog(self.img, filt, fr["radius"], fr["pad"], out=self.y)
+        elif kind == "log":
+            spk.log(self.img, filt, fr["radius"], fr["pad"], out=self.y)
         else:
             spk.gabor(self.img, filt, fr["radius"], fr["pad"], out=self.y)
         mark("filter")
@@ -284,8 +286,8 @@ class RateNetwork:
         self.dev = torch.device(device)
         im, fr = cfg["image"], cfg["front"]
         self.img = torch.zeros((batch, im["C"], im["H"], im["W"]), dtype=torch.uint8, device=self.dev)
-        self.pairs = spk.log_pairs(fr["stds"]) if fr["kind"] == "log" else [tuple(p) for p in fr.get("pairs", [])]
-        K = len(self.pairs) if fr["kind"] != "gabor" else len(fr["params"])
+        K = {"log": 2 * len(fr.get("stds", [])), "dog": len(fr.get("pairs", [])),
+             "gabor": len(fr.get("params", []))}[fr["kind"]]
         e = 2 * fr["radius"] + 1
         H, W = im["H"] + 2 * fr["pad"] - e + 1, im["W"] + 2 * fr["pad"] - e + 1
         self.y = torch.empty((batch, im["C"] * K, H, W), dtype=torch.float32, device=self.dev)
@@ -342,8 +344,10 @@ class RateNetwork:
         fr = self.cfg["front"]
         if fr["kind"] == "gabor":
             spk.gabor(self.img, fr["params"], fr["radius"], fr["pad"], out=self.y)
+        elif fr["kind"] == "log":
+            spk.log(self.img, fr["stds"], fr["radius"], fr["pad"], out=self.y)
         else:
-            spk.dog(self.img, self.pairs, fr["radius"], fr["pad"], out=self.y)
+            spk.dog(self.img, [tuple(p) for p in fr["pairs"]], fr["radius"], fr["pad"], out=self.y)
         mark("filter")
         spk.rate_code(self.y, self.T, fr["thresh"], self.cfg["rate_seed"], b0=self.start, out=self.step0, ws=self.rc_ws)
         mark("rate_code")

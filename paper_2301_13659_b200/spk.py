@@ -44,7 +44,7 @@ EXPORTS = [
     "spk_lat_to_dense", "spk_dense_to_lat", "spk_conv_status", "spk_conv_fire_pool_supported", "spk_conv_fire_pool",
     "spk_rate_code_workspace", "spk_rate_code", "spk_rate_gather", "spk_pool_rates", "spk_quantize", "spk_fc_workspace",
     "spk_fc", "spk_fcwta", "spk_zca_fit_workspace", "spk_zca_fit", "spk_zca_apply", "spk_conv_prepack",
-    "spk_stdp_status", "spk_inhibit_wta",
+    "spk_stdp_status", "spk_inhibit_wta", "spk_log",
 ]
 
 
@@ -96,6 +96,7 @@ def lib():
             "spk_conv_prepack": ([V, ctypes.POINTER(ConvGeom), I, F, V, Z, V], I),
             "spk_stdp_status": ([V, ctypes.POINTER(ConvGeom), I, ctypes.POINTER(ctypes.c_int32), V], I),
             "spk_inhibit_wta": ([V, V, I, I, I, I, I, I, I, V, V, V], I),
+            "spk_log": ([V, I, I, I, I, V, I, I, I, V, V], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -144,8 +145,20 @@ def dog(img: torch.Tensor, sigmas, radius: int, pad: int, out: torch.Tensor | No
     return out
 
 
+def log(img: torch.Tensor, stds, radius: int, pad: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """LoG bank: 2 channels (a DoG pair) per std, expanded behind the ABI (spk_log)."""
+    B, C, H, W = img.shape
+    st = (ctypes.c_double * len(stds))(*[float(v) for v in stds])
+    e = 2 * radius + 1
+    if out is None:
+        out = torch.empty((B, C * 2 * len(stds), H + 2 * pad - e + 1, W + 2 * pad - e + 1), dtype=torch.float32,
+                          device=img.device)
+    _check("spk_log", lib().spk_log(_p(img), B, C, H, W, st, len(stds), radius, pad, _p(out), _s()))
+    return out
+
+
 def log_pairs(stds):
-    """LoG(s) ~ DoG(s*sqrt2, s/sqrt2), DoG(s/sqrt2, s*sqrt2): the sigma pairs spk_dog takes."""
+    """The DoG sigma pairs spk_log expands a LoG bank into (for inspection; spk_log does it)."""
     r2 = 2.0 ** 0.5
     out = []
     for s in stds:

@@ -98,7 +98,7 @@ del L, F
 # rate coding, C6 (256 x 6 x 28 x 28, T = 300): 4 B in + T B out per value
 cfg6 = synth.load_config("c6")
 img = torch.from_numpy(synth.images(cfg6, 0, 256)).to(dev)
-y = spk.dog(img, spk.log_pairs(cfg6["front"]["stds"]), 3, 3)
+y = spk.log(img, cfg6["front"]["stds"], 3, 3)
 st = torch.empty((256, 300) + tuple(y.shape[1:]), dtype=torch.uint8, device=dev)
 ms = timeit(lambda: spk.rate_code(y, 300, 0.01, 60606, out=st))
 report("rate_code (C6, T=300)", [256, y[0].numel(), 300], 4 * y.numel() + st.numel(), ms,

@@ -36,7 +36,7 @@ def test_filter_bit_identical(spk, name):
     if fr["kind"] == "dog":
         got = spk.dog(cu(imgs), fr["pairs"], fr["radius"], fr["pad"])
     elif fr["kind"] == "log":
-        got = spk.dog(cu(imgs), spk.log_pairs(fr["stds"]), fr["radius"], fr["pad"])
+        got = spk.log(cu(imgs), fr["stds"], fr["radius"], fr["pad"])  # pairs expanded behind the ABI
     else:
         got = spk.gabor(cu(imgs), fr["params"], fr["radius"], fr["pad"])
     # bit for bit, including the sign of zeros (on/off pairs are computed as 0 - acc)
@@ -967,7 +967,8 @@ def test_conv_live_digit_planes(spk, case, wkind):
 
 
 @pytest.mark.parametrize("shape,k,r", [((4, 200, 4, 4), 8, 1), ((2, 30, 28, 28), 5, 3), ((1, 32, 28, 28), 5, 3),
-                                       ((2, 128, 80, 125), 8, 1), ((3, 7, 1, 1), 3, 0), ((2, 64, 30, 40), 20, 2)])
+                                       ((2, 128, 80, 125), 8, 1), ((3, 7, 1, 1), 3, 0), ((2, 64, 30, 40), 20, 2),
+                                       ((2, 20, 33, 35), 6, 2)])
 @pytest.mark.parametrize("ties", [False, True])
 def test_inhibit_wta_fused_exact(spk, shape, k, r, ties):
     """spk_inhibit_wta == oracle inhibit -> wta (winners bit-exact), records left untouched."""
