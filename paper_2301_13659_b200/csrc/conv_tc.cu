@@ -1317,16 +1317,35 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 if (o >= g.Co || (SPK_EXP & 8)) continue;
                 const size_t oi = ((size_t)b * g.Co + o) * a.HWo + p0;
                 uint8_t* dl = static_cast<uint8_t*>(a.out0) + oi;
-                if (npix == PPT && PPT == 8 && (reinterpret_cast<uintptr_t>(dl) & 7) == 0) {
+                // widest aligned stores (a map's run starts at (b Co + o) HWo + p0: with HWo = 196,
+                // half the runs are only 4-byte aligned)
+                const uintptr_t al = reinterpret_cast<uintptr_t>(dl);
+                if (npix == PPT && PPT == 8 && (al & 7) == 0) {
                     *reinterpret_cast<uint2*>(dl) = *reinterpret_cast<const uint2*>(sl + ol * PPT);
-                } else if (npix == PPT && PPT == 4 && (reinterpret_cast<uintptr_t>(dl) & 3) == 0) {
-                    *reinterpret_cast<uint32_t*>(dl) = *reinterpret_cast<const uint32_t*>(sl + ol * PPT);
+                } else if (npix == PPT && (PPT == 4 || PPT == 8) && (al & 3) == 0) {
+                    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(sl + ol * PPT);
+                    reinterpret_cast<uint32_t*>(dl)[0] = s4[0];
+                    if (PPT == 8) reinterpret_cast<uint32_t*>(dl)[1] = s4[1];
+                } else if (npix == PPT && (PPT == 4 || PPT == 8) && (al & 1) == 0) {
+                    const uint16_t* s2 = reinterpret_cast<const uint16_t*>(sl + ol * PPT);
+#pragma unroll
+                    for (int q = 0; q < PPT / 2; ++q) reinterpret_cast<uint16_t*>(dl)[q] = s2[q];
                 } else {
                     for (int q = 0; q < npix; ++q) dl[q] = sl[ol * PPT + q];
                 }
                 if (PSTAR) {
                     float* dp = a.out1 + oi;
-                    for (int q = 0; q < npix; ++q) dp[q] = sp[ol * PPT + q];
+                    if (npix == PPT && (PPT == 4 || PPT == 8) && (oi & 3) == 0) {
+#pragma unroll
+                        for (int q = 0; q < PPT; q += 4)
+                            *reinterpret_cast<float4*>(dp + q) = *reinterpret_cast<const float4*>(sp + ol * PPT + q);
+                    } else if (npix == PPT && (PPT == 4 || PPT == 8) && (oi & 1) == 0) {
+#pragma unroll
+                        for (int q = 0; q < PPT; q += 2)
+                            *reinterpret_cast<float2*>(dp + q) = *reinterpret_cast<const float2*>(sp + ol * PPT + q);
+                    } else {
+                        for (int q = 0; q < npix; ++q) dp[q] = sp[ol * PPT + q];
+                    }
                 }
             }
             __syncwarp();
