@@ -142,8 +142,30 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
                      : "memory");
     return ok != 0;
 }
+#ifndef SPK_WAIT_HINT
+#define SPK_WAIT_HINT 20000  // > 0: blocking waits suspend in try_wait for up to this many ns per probe
+#endif
+#ifndef SPK_WAIT_HINT_ALL
+#define SPK_WAIT_HINT_ALL 1  // 1: also the MMA issuer's and the slack roles' waits
+#endif
+// try_wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase
+// completes (or the hint elapses) instead of re-issuing probes
+__device__ __forceinline__ bool mbar_try_hint(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "n"(SPK_WAIT_HINT > 0 ? SPK_WAIT_HINT : 1)
+        : "memory");
+    return ok != 0;
+}
 // critical-path waits (producers, MMA issuer) poll
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    if (SPK_WAIT_HINT > 0) {
+        while (!mbar_try_hint(a, parity)) {
+        }
+        return;
+    }
     while (!mbar_try(a, parity)) {
     }
 }
@@ -157,6 +179,12 @@ __device__ __forceinline__ void mbar_wait3(uint32_t a0, uint32_t p0, bool w0, ui
     bool d0 = !w0 || mbar_try(a0, p0);
     bool d1 = !w1 || mbar_try(a1, p1);
     bool d2 = !w2 || mbar_try(a2, p2);
+    if (SPK_WAIT_HINT_ALL && SPK_WAIT_HINT > 0) {
+        while (!d0) d0 = mbar_try_hint(a0, p0);
+        while (!d1) d1 = mbar_try_hint(a1, p1);
+        while (!d2) d2 = mbar_try_hint(a2, p2);
+        return;
+    }
     while (!d0) d0 = mbar_try(a0, p0);
     while (!d1) d1 = mbar_try(a1, p1);
     while (!d2) d2 = mbar_try(a2, p2);
@@ -173,6 +201,11 @@ constexpr int kBarProd = 1, kBarEpi = 2, kBarBand = 3;
 // waits of roles with slack (epilogue, loaders, flusher) back off between polls so that
 // their spinning does not take issue slots from the producers on the same scheduler
 __device__ __forceinline__ void mbar_wait_idle(uint32_t a, uint32_t parity) {
+    if (SPK_WAIT_HINT_ALL && SPK_WAIT_HINT > 0) {
+        while (!mbar_try_hint(a, parity)) {
+        }
+        return;
+    }
     while (!mbar_try(a, parity)) {
         if (SPK_IDLE_NS > 0) __nanosleep(SPK_IDLE_NS);
     }

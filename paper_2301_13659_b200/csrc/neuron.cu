@@ -409,20 +409,69 @@ __global__ void gather_kernel(const uint8_t* __restrict__ lat, size_t n, int T, 
     f[q] = __fdiv_rn((float)(T - l), (float)T);
 }
 
-// 16 latencies per thread (one 16-byte load, four 16-byte stores); the T+1 possible
-// features come from a shared table of the same IEEE divisions (R-GATHER)
-__global__ void __launch_bounds__(kT) gather16_kernel(const uint4* __restrict__ lat, size_t n16, int T,
-                                                      float4* __restrict__ f) {
+// Word per lane: a warp reads 4 x 128 contiguous latency bytes and writes 4 x 512 contiguous
+// feature bytes (every store instruction one contiguous run; a 16-latencies-per-thread form
+// scattered each store over 2 KB and reached 0.64 of HBM against 0.86 for this one at C5); the
+// T+1 possible features come from a shared table of the same IEEE divisions (R-GATHER)
+__global__ void __launch_bounds__(kT) gather4_kernel(const uint32_t* __restrict__ lat, size_t n4, int T,
+                                                     float4* __restrict__ f) {
     __shared__ float tab[256];
     tab[threadIdx.x] = __fdiv_rn((float)(T - min((int)threadIdx.x, T)), (float)T);
     __syncthreads();
-    for (size_t q = (size_t)blockIdx.x * kT + threadIdx.x; q < n16; q += (size_t)gridDim.x * kT) {
-        const uint4 v = __ldg(lat + q);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const int lane = threadIdx.x & 31;
+    const size_t wid = ((size_t)blockIdx.x * kT + threadIdx.x) >> 5, nw = ((size_t)gridDim.x * kT) >> 5;
+    constexpr int U = 4;
+    for (size_t w0 = wid * (32 * U); w0 < n4; w0 += nw * (32 * U)) {
+        uint32_t v[U];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            f[4 * q + j] = make_float4(tab[w[j] & 0xffu], tab[(w[j] >> 8) & 0xffu], tab[(w[j] >> 16) & 0xffu],
-                                       tab[w[j] >> 24]);
+        for (int u = 0; u < U; ++u) {
+            const size_t q = w0 + u * 32 + lane;
+            v[u] = q < n4 ? __ldcs(lat + q) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const size_t q = w0 + u * 32 + lane;
+            if (q < n4)
+                __stcs(f + q, make_float4(tab[v[u] & 0xffu], tab[(v[u] >> 8) & 0xffu], tab[(v[u] >> 16) & 0xffu],
+                                          tab[v[u] >> 24]));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- pool, 2x2 stride 2 streaming form
+// Unpadded 2x2/2 windows on planes whose width is a multiple of 16 (C4, C5 conv layers):
+// a thread reads 16 bytes of each of the window's two input rows and writes the 8 pooled
+// bytes; two items per trip keep four 16-byte loads in flight.  No shared-memory staging:
+// every input byte is read once and the loads stream straight from HBM.
+__global__ void __launch_bounds__(kT) pool2_vec_kernel(const uint4* __restrict__ lat, long long n_items, int cw,
+                                                       int W16, int T, uint2* __restrict__ out) {
+    // item i: chunk c = i % cw of output row r = i / cw (rows of all planes concatenated:
+    // output row r reads input rows 2r, 2r + 1 because H is even)
+    const uint32_t tt = 0x01010101u * (uint32_t)T;
+    auto pool8 = [&](uint4 a, uint4 b) {
+        const uint32_t m[4] = {__vminu4(a.x, b.x), __vminu4(a.y, b.y), __vminu4(a.z, b.z), __vminu4(a.w, b.w)};
+        uint32_t h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k] = __vminu4(m[k] & 0x00ff00ffu, (m[k] >> 8) & 0x00ff00ffu);  // bytes 0, 2
+        const uint32_t lo = (h[0] & 0xffu) | ((h[0] >> 8) & 0xff00u) | ((h[1] & 0xffu) << 16) | ((h[1] << 8) & 0xff000000u);
+        const uint32_t hi = (h[2] & 0xffu) | ((h[2] >> 8) & 0xff00u) | ((h[3] & 0xffu) << 16) | ((h[3] << 8) & 0xff000000u);
+        return make_uint2(__vminu4(lo, tt), __vminu4(hi, tt));
+    };
+    const long long stride = (long long)gridDim.x * kT;
+    long long i = (long long)blockIdx.x * kT + threadIdx.x;
+    for (; i + stride < n_items; i += 2 * stride) {
+        const long long j = i + stride;
+        const long long r0 = i / cw, r1 = j / cw;
+        const long long a0 = 2 * r0 * W16 + (i - r0 * cw), a1 = 2 * r1 * W16 + (j - r1 * cw);
+        const uint4 x0 = __ldcs(lat + a0), y0 = __ldcs(lat + a0 + W16);
+        const uint4 x1 = __ldcs(lat + a1), y1 = __ldcs(lat + a1 + W16);
+        __stcs(out + i, pool8(x0, y0));
+        __stcs(out + j, pool8(x1, y1));
+    }
+    if (i < n_items) {
+        const long long r0 = i / cw;
+        const long long a0 = 2 * r0 * W16 + (i - r0 * cw);
+        __stcs(out + i, pool8(__ldcs(lat + a0), __ldcs(lat + a0 + W16)));
     }
 }
 
@@ -520,6 +569,17 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
         const char* e = std::getenv("SPK_POOL_SMEM_MIN");
         return e ? std::atoll(e) : 2048ll;
     }();
+    // 2x2/2 on even-height planes 16 bytes wide (C5): streaming kernel, no staging
+    if (p->Lh == 2 && p->Lw == 2 && p->Sh == 2 && p->Sw == 2 && p->Ph == 0 && p->Pw == 0 && H % 2 == 0 &&
+        W % 16 == 0 && (long long)H * W >= smem_min &&
+        ((reinterpret_cast<uintptr_t>(lat) & 15) | (reinterpret_cast<uintptr_t>(out) & 7)) == 0) {
+        const int cw = W / 16;
+        const long long n_items = BC * Ho * cw;
+        const unsigned blocks = (unsigned)std::min<long long>((n_items + 2 * kT - 1) / (2 * kT), (long long)spk::sm_count() * 8);
+        pool2_vec_kernel<<<blocks, kT, 0, spk::as_cuda(stream)>>>(reinterpret_cast<const uint4*>(lat), n_items, cw,
+                                                                  cw, T, reinterpret_cast<uint2*>(out));
+        return spk::launched("pool2_vec_kernel");
+    }
     if ((long long)H * W >= smem_min && per_plane + 256 <= (size_t)kPoolSmem) {
         const int ppc = (int)std::min<long long>(BC, std::max<long long>(1, (24 * 1024) / (long long)per_plane));  // ~24 KB per CTA
         const size_t smem = (((size_t)ppc * H * W + 127) & ~(size_t)127) + (size_t)ppc * plane_out;
@@ -596,12 +656,12 @@ extern "C" spk_status spk_gather(const uint8_t* lat, size_t n, int T, float* fea
     SPK_CHECK_PTR(feat);
     SPK_CHECK(T >= 1 && T <= 254, SPK_ERR_UNSUPPORTED, "T=%d outside 1..254", T);
     if (n == 0) return SPK_OK;
-    if (n % 16 == 0 && ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(feat)) & 15) == 0) {
-        const size_t n16 = n / 16;
-        const unsigned blocks = (unsigned)std::min<size_t>(spk::ceil_div(n16, kT), 148 * 16);
-        gather16_kernel<<<blocks, kT, 0, spk::as_cuda(stream)>>>(reinterpret_cast<const uint4*>(lat), n16, T,
-                                                                 reinterpret_cast<float4*>(feat));
-        return spk::launched("gather16_kernel");
+    if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && (reinterpret_cast<uintptr_t>(feat) & 15) == 0) {
+        const size_t n4 = n / 4;
+        const unsigned blocks = (unsigned)std::min<size_t>(spk::ceil_div(n4, (size_t)kT * 4), (size_t)spk::sm_count() * 8);
+        gather4_kernel<<<blocks, kT, 0, spk::as_cuda(stream)>>>(reinterpret_cast<const uint32_t*>(lat), n4, T,
+                                                                reinterpret_cast<float4*>(feat));
+        return spk::launched("gather4_kernel");
     }
     gather_kernel<<<spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream)>>>(lat, n, T, feat);
     return spk::launched("gather_kernel");

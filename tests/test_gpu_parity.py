@@ -253,10 +253,12 @@ def test_pool_exact(spk, L, s, p):
     np.testing.assert_array_equal(host(spk.pool(cu(lat), T, L, s, p)), ref)
 
 
-# plane shapes of the large configs: C5 conv1 (16-byte rows), C4 conv1 (2-byte rows),
+# plane shapes of the large configs: C5 conv1 (16-byte rows: streaming 2x2 kernel; an odd item
+# count), C4 conv1 (2-byte rows),
 # many small planes per CTA, a plane too large for shared memory (global path), and
 # narrow output rows (Wo < 16: one output per thread from shared memory)
-@pytest.mark.parametrize("shape,L,s,p", [((2, 3, 224, 224), 2, 2, 0), ((1, 5, 160, 250), 2, 2, 0),
+@pytest.mark.parametrize("shape,L,s,p", [((2, 3, 224, 224), 2, 2, 0), ((3, 7, 64, 48), 2, 2, 0),
+                                          ((1, 5, 160, 250), 2, 2, 0),
                                           ((3, 250, 14, 14), 3, 3, 0), ((1, 1, 300, 330), 2, 2, 1),
                                           ((2, 4, 50, 45), 3, 2, 1), ((2, 3, 64, 64), 8, 8, 0),
                                           ((2, 3, 61, 47), 5, 4, 2)])
