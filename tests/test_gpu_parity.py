@@ -96,7 +96,21 @@ def test_rank_code_large_sample_histogram_path(spk, T):
     y[4] = -1.0
     y[4, 12345] = 3.0                                          # a single positive
     y[5, 1::3] = np.float32(2.0) ** RNG.integers(-6, 6, y[5, 1::3].shape)  # bucket edges
+    y = np.concatenate([y, np.full((1, y.shape[1]), -1.0, np.float32)])  # nothing fires
     np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, True)), oracle.rank_code(y, T, 0.01, True))
+
+
+@pytest.mark.parametrize("N", [65_536, 301_056, 400_004])
+def test_rank_code_c5_sized_samples(spk, N):
+    """Large samples, sort on (C5: 301,056 values per sample): ties across buckets, N/2 exact
+    ties in the middle of the sample (radix-select fallback), an empty sample, every value twice."""
+    y = RNG.normal(0, 1, (5, N)).astype(np.float32)
+    y[1] = np.round(y[1], 2)                      # ties across buckets and across the CTA parts
+    y[2, N // 4: 3 * N // 4] = 0.75               # N/2 exact ties straddling the parts -> fallback
+    y[3] = -1.0                                   # nothing fires
+    y[4, : N // 2] = y[4, N // 2:]                # every value twice, once in each half
+    for T in (1, 15, 30):
+        np.testing.assert_array_equal(host(spk.rank_code(cu(y), T, 0.01, True)), oracle.rank_code(y, T, 0.01, True))
 
 
 @pytest.mark.parametrize("N", [1, 3, 4705, 8192, 8193, 50_001])
