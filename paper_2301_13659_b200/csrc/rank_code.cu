@@ -17,6 +17,12 @@
 
 namespace {
 
+#ifndef SPK_RANK_SMALL_SHIFT
+#define SPK_RANK_SMALL_SHIFT 19  // small samples: buckets = top (32 - SHIFT) bits of the float
+#endif
+#ifndef SPK_RANK_SMALL_THREADS
+#define SPK_RANK_SMALL_THREADS 256
+#endif
 #ifndef SPK_RANK_RUNS
 #define SPK_RANK_RUNS 0  // 1: pass-1 histogram atomics aggregated over runs of equal buckets
 #endif
@@ -527,13 +533,14 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         return e ? std::atoi(e) : 0;
     }();
     if (sort && N <= kSortMax && !old_sort) {  // small samples: staged values, 4096-bucket histogram
-        using Cfg = HistCfg<19, 256, 1024, true>;
+        constexpr int SH = SPK_RANK_SMALL_SHIFT, TH = SPK_RANK_SMALL_THREADS;
+        using Cfg = HistCfg<SH, TH, 1024, true>;
         static std::atomic<uint64_t> attr{0};
         if (spk::first_on_device(attr)) {
-            cudaFuncSetAttribute(rank_code_hist_kernel<19, 256, 1024, true>,
+            cudaFuncSetAttribute(rank_code_hist_kernel<SH, TH, 1024, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(kSortMax));
         }
-        rank_code_hist_kernel<19, 256, 1024, true><<<B, 256, Cfg::smem(N), s>>>(y, N, T, thresh, lat);
+        rank_code_hist_kernel<SH, TH, 1024, true><<<B, TH, Cfg::smem(N), s>>>(y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel<small>");
     }
     if (sort && N <= kSortMax) {
