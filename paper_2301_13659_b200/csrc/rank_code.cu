@@ -18,10 +18,10 @@
 namespace {
 
 #ifndef SPK_RANK_SMALL_SHIFT
-#define SPK_RANK_SMALL_SHIFT 19  // small samples: buckets = top (32 - SHIFT) bits of the float
+#define SPK_RANK_SMALL_SHIFT 20  // small samples: 2048 buckets (exponent + 3 mantissa bits)
 #endif
 #ifndef SPK_RANK_SMALL_THREADS
-#define SPK_RANK_SMALL_THREADS 256
+#define SPK_RANK_SMALL_THREADS 512  // C2 front end: 49 -> 31 us against 4096 buckets x 256 threads (profiles/r02_ab_rank_small.txt)
 #endif
 #ifndef SPK_RANK_RUNS
 #define SPK_RANK_RUNS 0  // 1: pass-1 histogram atomics aggregated over runs of equal buckets
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const floa
 constexpr int kMaxBnd = 256, kUnroll = 4;
 // Two instantiations: C4/C5 samples (32768 buckets = exponent + 7 mantissa bits, 1024
 // threads, values read twice from global memory) and C1-C3 samples (<= 8192 values:
-// 4096 buckets = exponent + 4 mantissa bits, 256 threads, values staged in smem).
+// 2048 buckets = exponent + 3 mantissa bits, 512 threads, values staged in smem).
 template <int SHIFT, int kHT, int kCand, bool STAGE>
 struct HistCfg {
     static constexpr int kBkt = 1 << (31 - SHIFT);
@@ -532,7 +532,7 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
         const char* e = std::getenv("SPK_RANK_SORT");  // A/B knob: 1 = bitonic sort kernel for small samples
         return e ? std::atoi(e) : 0;
     }();
-    if (sort && N <= kSortMax && !old_sort) {  // small samples: staged values, 4096-bucket histogram
+    if (sort && N <= kSortMax && !old_sort) {  // small samples: staged values, 2048-bucket histogram
         constexpr int SH = SPK_RANK_SMALL_SHIFT, TH = SPK_RANK_SMALL_THREADS;
         using Cfg = HistCfg<SH, TH, 1024, true>;
         static std::atomic<uint64_t> attr{0};
