@@ -137,6 +137,11 @@ CONV_CASES = [
     (1, 16, 5, 6, 5, 17, 4, 3, 1),        # T = TP, odd Co
     (2, 1, 2, 5, 7, 8, 2, 1, 0),          # T = 1
     (160, 15, 2, 12, 12, 8, 5, 1, 2),     # grid >= 148 CTAs: whole sample per event CTA
+    # T = 1 (one time step per row; kernel rows of 3..7 synapses padded to 8 in K, read as words)
+    (3, 1, 6, 13, 17, 20, 5, 1, 2),       # C6 conv0 shape class, ragged 128-pixel tiles
+    (2, 1, 25, 14, 14, 50, 3, 1, 1),      # C6 conv1 shape class, 2 N tiles
+    (2, 1, 3, 11, 9, 12, 7, 2, 3),        # 7-wide rows, stride 2, pad 3 (rows end in the sentinel)
+    (1, 1, 40, 9, 10, 33, 5, 1, 0),       # K' = 1600 over many stages, Co = 33
 ]
 
 
