@@ -61,7 +61,11 @@ constexpr int KS = kTcKS;          // synapses per stage (4 MMAs of K=32)
 static_assert(KS == 128, "an A slot holds 4 k-steps of 32 synapses");
 constexpr int S = kTcStages;       // pipeline depth
 constexpr int kProdWarps = 8;      // warps 0-7: producers
-constexpr int kEpiWarps = 8;       // warps 8-15: epilogue (two per TMEM lane quadrant)
+#ifndef SPK_EPI_WARPS
+#define SPK_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = SPK_EPI_WARPS;  // warps 8..: epilogue (kEpiWarps / 4 per TMEM lane quadrant)
+constexpr int kEpiStride = 16 * (kEpiWarps / 4);  // column stride of one epilogue warp's 16-column chunks
 constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 16: MMA issuer; 17: B loader; 18: band loader
 constexpr int kLoaders = 32;  // one band-loader warp: 20 warps keep 96 registers per thread
 constexpr int kFlushWarp = kMmaWarp + 3;           // warp 19: writes staged output tiles to HBM
@@ -837,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 for (int b = 0; b < a.NB; ++b)
                     for (int d = 0; d < 3; ++d)
                         if (!((lp >> d) & 1u))
-                            for (int c = eh * 16; c < a.Nt; c += 32)
+                            for (int c = eh * 16; c < a.Nt; c += kEpiStride)
                                 tmem_st16(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * 3 * a.Nt + d * a.Nt + c), z);
                 tmem_wait_st();
             }
@@ -861,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             if (threadIdx.x == kProdWarps * 32) TRACE(1, ep_it);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
-            for (int n0 = eh * 16; n0 < ((SPK_EXP & 128) || EPI != SPK_EPI_POTENTIAL ? 0 : a.Nt); n0 += 32) {
+            for (int n0 = eh * 16; n0 < ((SPK_EXP & 128) || EPI != SPK_EPI_POTENTIAL ? 0 : a.Nt); n0 += kEpiStride) {
                 uint32_t d0[16], d1[16], d2[16];
 #if (SPK_EXP & 16)
 #pragma unroll
@@ -911,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             bool released = false;
             if (TP == 1 && EPI != SPK_EPI_POTENTIAL) {
                 // one time step: row = pixel, fire iff X > theta (lat 0, else T = 1); P* = potential
-                for (int n0 = eh * 16; n0 < a.Nt; n0 += 32) {
+                for (int n0 = eh * 16; n0 < a.Nt; n0 += kEpiStride) {
 #pragma unroll
                     for (int h8 = 0; h8 < 16; h8 += 8) {
                         uint32_t r[24];
@@ -991,13 +995,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     ld8(n0, ra);
                     tmem_wait_ld();
                 }
-                for (; n0 < a.Nt; n0 += 32) {
+                for (; n0 < a.Nt; n0 += kEpiStride) {
                     ld8(n0 + 8, rb);
                     half(ra, 0, n0);
                     tmem_wait_ld();
-                    const bool more = n0 + 32 < a.Nt;
+                    const bool more = n0 + kEpiStride < a.Nt;
                     if (more) {
-                        ld8(n0 + 32, ra);
+                        ld8(n0 + kEpiStride, ra);
                     } else if (!(SPK_EXP & 8192)) {  // every TMEM read of this buffer has landed
                         tc_fence_before();
                         __syncwarp();
