@@ -76,7 +76,7 @@ constexpr int kACols = KS / 4;     // TMEM columns of one A stage (4 u8 per 32-b
 constexpr int kMaxA = 8;           // TMEM A ring slots (<= 8; the rest of the 512 columns hold accumulators)
 
 // Optional per-role cycle accounting (SPK_CONV_PROF=1): [block][role][total, wait]
-constexpr int kProfRoles = 17;  // producer, epilogue, mma, b-loader, band-loader, mma:fence/issue/commit, producer sections x6
+constexpr int kProfRoles = 25;  // producer, epilogue, mma, b-loader, band-loader, mma:fence/issue/commit, producer sections x9, epilogue sections x6
 __device__ unsigned long long g_conv_prof[1024][kProfRoles][2];
 #ifdef SPK_CONV_TRACE
 // event timestamps of CTA 0's first kTrace tiles (debug aid)
@@ -819,6 +819,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         // ======================= epilogue =======================
         // two warps per TMEM lane quadrant; warp `eh` of a quadrant takes every other 16-column chunk
         RoleClock rc(a.prof != 0);
+        long long ep_t[6] = {0, 0, 0, 0, 0, 0};  // SPK_CONV_PROF_BUILD: wait, bar.sync, work, tail (leader); sync, work (warp 5)
+        long long ep_w = 0;                      // SPK_CONV_PROF_BUILD: cycles in tcgen05.wait::ld of the fire path
         const int qd = warp & 3;                  // TMEM lane quadrant
         const int eh = (warp - kProdWarps) >> 2;  // 0 or 1
         const int row = qd * 32 + lane;           // accumulator row = (pixel, t)
@@ -858,10 +860,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             const long long thq = rvalid ? a.theta_q : 0x7fffffffffffffffll;
             const int thh = rvalid ? a.thH : 0x7fffffff;
             // the leader probes the staging slot and the accumulator together, the group sleeps
+            const long long ec0 = rc.on ? clock64() : 0;
             if (threadIdx.x == kProdWarps * 32)
                 rc.wait3(fls0 + 8 * ob, ob_ph ^ 1u, EPI != SPK_EPI_POTENTIAL && !(SPK_EXP & 65536), accf0 + 8 * buf, acc_ph,
                          !(SPK_EXP & 8704));
+            const long long ec1 = rc.on ? clock64() : 0;
             asm volatile("bar.sync %0, %1;" ::"n"(kBarEpi), "n"(kEpiWarps * 32) : "memory");
+            const long long ec2 = rc.on ? clock64() : 0;
             if (threadIdx.x == kProdWarps * 32) TRACE(1, ep_it);
             tc_fence_after();
             const uint32_t tbase = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * 3 * a.Nt);
@@ -993,12 +998,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 int n0 = eh * 16;
                 if (n0 < a.Nt) {
                     ld8(n0, ra);
-                    tmem_wait_ld();
+                    { const long long w0_ = rc.on ? clock64() : 0; tmem_wait_ld(); if (rc.on) ep_w += clock64() - w0_; }
                 }
                 for (; n0 < a.Nt; n0 += kEpiStride) {
                     ld8(n0 + 8, rb);
                     half(ra, 0, n0);
-                    tmem_wait_ld();
+                    { const long long w0_ = rc.on ? clock64() : 0; tmem_wait_ld(); if (rc.on) ep_w += clock64() - w0_; }
                     const bool more = n0 + kEpiStride < a.Nt;
                     if (more) {
                         ld8(n0 + kEpiStride, ra);
@@ -1009,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                         released = true;
                     }
                     half(rb, 8, n0 + 8);
-                    if (more) tmem_wait_ld();
+                    if (more) { const long long w0_ = rc.on ? clock64() : 0; tmem_wait_ld(); if (rc.on) ep_w += clock64() - w0_; }
                     if (own_lane) {  // stage (map, pixel) -> smem
                         const unsigned bits = (mine >> (own_seg * TP)) & segmask;
                         const int ol = (n0 + own_col) * PPT + own_pix;
@@ -1023,6 +1028,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 __syncwarp();
                 if (lane == 0 && !(SPK_EXP & 8192)) mbar_arrive(acce0 + 8 * buf);
             }
+            const long long ec3 = rc.on ? clock64() : 0;
             if (threadIdx.x == kProdWarps * 32) TRACE(2, ep_it);
             ++ep_it;
             if (EPI != SPK_EPI_POTENTIAL) {  // hand the staged tile to the flusher warp
@@ -1031,6 +1037,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
             }
             if (++buf == a.NB) buf = 0, acc_ph ^= 1u;
             if (++ob == kNOB) ob = 0, ob_ph ^= 1u;
+            if (rc.on) {
+                const long long ec4 = clock64();
+                if (threadIdx.x == kProdWarps * 32) {
+                    ep_t[0] += ec1 - ec0, ep_t[1] += ec2 - ec1, ep_t[2] += ec3 - ec2, ep_t[3] += ec4 - ec3;
+                } else if (threadIdx.x == (kProdWarps + 5) * 32) {
+                    ep_t[4] += ec2 - ec0, ep_t[5] += ec3 - ec2;
+                }
+            }
+        }
+        if (rc.on && blockIdx.x < 1024) {
+            if (threadIdx.x == kProdWarps * 32)
+                for (int q = 0; q < 4; ++q) g_conv_prof[blockIdx.x][17 + q][0] = ep_t[q];
+            if (threadIdx.x == (kProdWarps + 5) * 32)
+                for (int q = 4; q < 6; ++q) g_conv_prof[blockIdx.x][17 + q][0] = ep_t[q];
+            if (threadIdx.x == kProdWarps * 32) g_conv_prof[blockIdx.x][23][0] = ep_w;
+            if (threadIdx.x == (kProdWarps + 5) * 32) g_conv_prof[blockIdx.x][24][0] = ep_w;
         }
         if (threadIdx.x == kProdWarps * 32) rc.store(1);
     } else if (warp == kMmaWarp) {
