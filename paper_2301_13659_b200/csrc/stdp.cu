@@ -97,8 +97,12 @@ __global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const int32
 // byte; phase 2 — one thread per weight — runs the sequential fp32 chain of
 // Eq. 4-6 from shared memory only.  The gathers are thus fully parallel and the
 // order-dependent part is a few dependent flops per winner.
-constexpr int kUpdW = 32, kUpdThreads = 256, kWinChunk = 256;  // tuned on C2 layer 3 (scripts/ab_stdp.sh)
+// kUpdW weights per CTA: 32 when maps collect many winners (C2 layer 3: ~41 per map, the ordered
+// chain dominates), 128 when they collect few (C3 decision layer: the gathers dominate) —
+// profiles/r02_ab_stdp_width.txt
+constexpr int kUpdThreads = 256, kWinChunk = 256;
 
+template <int kUpdW>
 __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restrict__ w, spk_conv_geom g,
                                                                   const uint8_t* __restrict__ lat_in,
                                                                   const spk_winner* __restrict__ win,
@@ -240,8 +244,14 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     if (st != SPK_OK) return st;
     const size_t K = (size_t)g->Ci * g->Kh * g->Kw;
     SPK_CHECK(g->Co <= 65535, SPK_ERR_SHAPE, "Co=%d > 65535", g->Co);
-    const dim3 grid(spk::ceil_div(K, kUpdW), (unsigned)g->Co);
-    stdp_update_kernel<<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+    // average winners per map (upper bound: every slot a winner) picks the tile width
+    if ((long long)g->B * k >= 16ll * g->Co) {
+        const dim3 grid(spk::ceil_div(K, 32), (unsigned)g->Co);
+        stdp_update_kernel<32><<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+    } else {
+        const dim3 grid(spk::ceil_div(K, 128), (unsigned)g->Co);
+        stdp_update_kernel<128><<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+    }
     return spk::launched("stdp_update_kernel");
 }
 
