@@ -100,9 +100,12 @@ __global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const int32
 // kUpdW weights per CTA: 32 when maps collect many winners (C2 layer 3: ~41 per map, the ordered
 // chain dominates), 128 when they collect few (C3 decision layer: the gathers dominate) —
 // profiles/r02_ab_stdp_width.txt
-constexpr int kUpdThreads = 256, kWinChunk = 256;
+constexpr int kWinChunk = 256;
+#ifndef SPK_STDP_T32
+#define SPK_STDP_T32 256  // threads per CTA of the 32-weight tile
+#endif
 
-template <int kUpdW>
+template <int kUpdW, int kUpdThreads>
 __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restrict__ w, spk_conv_geom g,
                                                                   const uint8_t* __restrict__ lat_in,
                                                                   const spk_winner* __restrict__ win,
@@ -247,10 +250,10 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     // average winners per map (upper bound: every slot a winner) picks the tile width
     if ((long long)g->B * k >= 16ll * g->Co) {
         const dim3 grid(spk::ceil_div(K, 32), (unsigned)g->Co);
-        stdp_update_kernel<32><<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+        stdp_update_kernel<32, SPK_STDP_T32><<<grid, SPK_STDP_T32, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
     } else {
         const dim3 grid(spk::ceil_div(K, 128), (unsigned)g->Co);
-        stdp_update_kernel<128><<<grid, kUpdThreads, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+        stdp_update_kernel<128, 256><<<grid, 256, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
     }
     return spk::launched("stdp_update_kernel");
 }
