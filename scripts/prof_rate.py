@@ -14,7 +14,7 @@ net.img.copy_(torch.from_numpy(synth.images(cfg, 0, B)))
 net.set_weights([torch.from_numpy(w) for w in synth.layer_weights(cfg)])
 net.front()
 L = spk.lib()
-buf = np.zeros((1024, 17, 2), np.uint64)
+buf = np.zeros((1024, 25, 2), np.uint64)
 names = ["producer", "epilogue", "mma", "bload", "band"]
 for li in range(len(net.layers)):
     for rep in range(2):
@@ -24,4 +24,6 @@ for li in range(len(net.layers)):
     ms = e0.elapsed_time(e1)
     tot = buf[:148, :, 0].astype(float); wt = buf[:148, :, 1].astype(float)
     print(f"layer {li}: {ms:.3f} ms (incl. rates/pool) " + "  ".join(f"{n}: busy {np.mean(tot[:, i]-wt[:, i])/1e3:.0f}k wait {np.mean(wt[:, i])/1e3:.0f}k" for i, n in enumerate(names))
-          + f"  | mma fence {np.mean(tot[:, 5])/1e3:.0f}k issue {np.mean(tot[:, 6])/1e3:.0f}k commit {np.mean(tot[:, 7])/1e3:.0f}k")
+          + f"  | mma fence {np.mean(tot[:, 5])/1e3:.0f}k issue {np.mean(tot[:, 6])/1e3:.0f}k commit {np.mean(tot[:, 7])/1e3:.0f}k"
+          + "  | epi lead wait/barsync/work/tail " + " ".join(f"{np.mean(tot[:, 17 + q])/1e3:.0f}k" for q in range(4))
+          + "  warp5 sync+wait/work " + " ".join(f"{np.mean(tot[:, 21 + q])/1e3:.0f}k" for q in range(2)))
