@@ -581,13 +581,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
         int rb = 0, rbn = 0, sA = 0;
         uint32_t phA = 0, rgph = 0;
         bool need_region = true;
+        long long pq[4] = {0, 0, 0, 0};  // SPK_CONV_PROF_BUILD: region wait, gather, slot wait, store+hand-off
         for (; ti.valid(); ti.next(a)) {
             if (a.retain && ti.nt != 0) continue;
+            const long long q0 = rc.on ? clock64() : 0;
             if (need_region) {
                 rb = rbn;
                 rc.template group_wait<kBarProd, kProdWarps * 32>(rgf0 + 8 * rb, rgph, threadIdx.x == 0);
                 if (++rbn == a.nrb) rbn = 0, rgph ^= 1u;
             }
+            if (rc.on) pq[0] += clock64() - q0;
             const bool last_use = a.retain ? ti.template region_ends_m<PPT>(a) : ti.template region_ends<PPT>(a);
             need_region = last_use;
             const uint8_t* region = RG + rb * a.rb_stride;
@@ -606,6 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                 const uint32_t gbar = 8u * (uint32_t)sA;
                 if (glast && ++sA == a.NA / a.G) sA = 0, phA ^= 1u;
                 uint32_t r[16];
+                const long long q1 = rc.on ? clock64() : 0;
                 const int kb = ks * KS + half * HK;
                 // the stage's 64 table entries first (broadcast reads, all in flight), then the
                 // band bytes: one dependent load deep instead of one per 8 synapses
@@ -644,16 +648,26 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(rge0 + 8 * rb);
                 }
+                const long long q2 = rc.on ? clock64() : 0;
                 if (gfirst) rc.template group_wait<kBarProd, kProdWarps * 32>(empty0 + gbar, ph ^ 1u, threadIdx.x == 0);
+                const long long q3 = rc.on ? clock64() : 0;
                 tc_fence_after();
                 tmem_st16(trow + (uint32_t)(s * kACols), r);
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0 && glast) mbar_arrive(full0 + gbar);
+                if (rc.on) {
+                    const long long q4 = clock64();
+                    pq[1] += q2 - q1, pq[2] += q3 - q2, pq[3] += q4 - q3;
+                }
             }
         }
-        if (threadIdx.x == 0) rc.store(0);
+        if (threadIdx.x == 0) {
+            rc.store(0);
+            if (rc.on && blockIdx.x < 1024)
+                for (int q = 0; q < 4; ++q) g_conv_prof[blockIdx.x][8 + q][0] = pq[q];
+        }
     } else if (TP != 1 && warp < kProdWarps) {
         // ======================= producers =======================
         RoleClock rc(a.prof != 0);

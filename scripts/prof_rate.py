@@ -25,5 +25,6 @@ for li in range(len(net.layers)):
     tot = buf[:148, :, 0].astype(float); wt = buf[:148, :, 1].astype(float)
     print(f"layer {li}: {ms:.3f} ms (incl. rates/pool) " + "  ".join(f"{n}: busy {np.mean(tot[:, i]-wt[:, i])/1e3:.0f}k wait {np.mean(wt[:, i])/1e3:.0f}k" for i, n in enumerate(names))
           + f"  | mma fence {np.mean(tot[:, 5])/1e3:.0f}k issue {np.mean(tot[:, 6])/1e3:.0f}k commit {np.mean(tot[:, 7])/1e3:.0f}k"
+          + "  | T=1 prod region/gather/slot-wait/store " + " ".join(f"{np.mean(tot[:, 8 + q])/1e3:.0f}k" for q in range(4))
           + "  | epi lead wait/barsync/work/tail " + " ".join(f"{np.mean(tot[:, 17 + q])/1e3:.0f}k" for q in range(4))
           + "  warp5 sync+wait/work " + " ".join(f"{np.mean(tot[:, 21 + q])/1e3:.0f}k" for q in range(2)))
