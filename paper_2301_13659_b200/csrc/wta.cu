@@ -164,8 +164,28 @@ __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) 
         const int ng = kThreads / np_slice;
         const int pp = threadIdx.x % np_slice, gq = threadIdx.x / np_slice;
         if (gq < ng) {
+            // four channels per trip: their latency loads, then the P* loads of those that fired,
+            // are in flight together instead of two dependent loads per channel
             unsigned long long m = ~0ull;
-            for (int c = gq; c < a.C; c += ng) m = umin64(m, wta_key(L, P, c * HW + p_lo + pp, T));
+            const int i0 = p_lo + pp;
+            for (int c0 = gq; c0 < a.C; c0 += 4 * ng) {
+                int l[4];
+                float pv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = c0 + u * ng;
+                    l[u] = c < a.C ? (int)__ldg(L + c * HW + i0) : T;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) pv[u] = l[u] < T ? __ldg(P + (c0 + u * ng) * HW + i0) : 0.0f;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (l[u] >= T) continue;
+                    const unsigned int po = ~spk_float_order_u32(pv[u]);  // higher potential first
+                    m = umin64(m, ((unsigned long long)l[u] << 56) | ((unsigned long long)po << 24) |
+                                      (unsigned long long)((c0 + u * ng) * HW + i0));
+                }
+            }
             if (m != ~0ull) atomicMin(&keys[pp], m);
         }
         __syncthreads();
