@@ -636,23 +636,24 @@ def main():
     h_nwin = torch.empty(net.nwin.shape, dtype=torch.int32).pin_memory() if train else None
     h_feat = None if train else torch.empty(net.features.shape, dtype=torch.float32).pin_memory()
     e2e_evs = []
+    io_in = [(net.img, h_img)] + ([(net.labels, h_lab)] if cfg["learning"] == "rstdp" else [])
+    io_out = [(h_win, net.win), (h_nwin, net.nwin)] if h_win is not None else [(h_feat, net.features)]
+    if use_graph:  # the public API's host-to-host step: copies in, the step, copies out, one graph
+        net.capture_io(io_in, io_out)
+        net.replay_io()  # warm-up replay (one more STDP update; the timed steps below measure the same work)
     torch.cuda.synchronize()
     for _ in range(args.steps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        net.img.copy_(h_img, non_blocking=True)
-        if cfg["learning"] == "rstdp":
-            net.labels.copy_(h_lab, non_blocking=True)
         if use_graph:
-            net.replay()
+            net.replay_io()
         else:
+            for dst, src in io_in:
+                dst.copy_(src, non_blocking=True)
             net.step()
-        if h_win is not None:
-            h_win.copy_(net.win, non_blocking=True)
-            h_nwin.copy_(net.nwin, non_blocking=True)
-        else:
-            h_feat.copy_(net.features, non_blocking=True)
+            for dst, src in io_out:
+                dst.copy_(src, non_blocking=True)
         e1.record(stream)
         e2e_evs.append((e0, e1))
     torch.cuda.synchronize()

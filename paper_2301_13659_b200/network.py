@@ -267,6 +267,24 @@ class Network:
         else:
             self.graph.replay()
 
+    def capture_io(self, inputs, outputs):
+        """Capture one step TOGETHER with its host I/O in one CUDA graph: `inputs` = [(device
+        tensor, pinned host tensor)] copied in first, `outputs` = [(pinned host tensor, device
+        tensor)] copied out last — a user's whole step from host buffers to host buffers is then
+        one graph launch (`replay_io`) instead of separate copy calls around the step."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for dst, src in inputs:
+                dst.copy_(src, non_blocking=True)
+            self.step()
+            for dst, src in outputs:
+                dst.copy_(src, non_blocking=True)
+        self.io_graph = g
+        return g
+
+    def replay_io(self):
+        self.io_graph.replay()
+
 
 class RateNetwork:
     """Rate-coded inference ("the inference is done with 300 time
@@ -390,3 +408,5 @@ class RateNetwork:
 
     capture = Network.capture
     replay = Network.replay
+    capture_io = Network.capture_io
+    replay_io = Network.replay_io

@@ -929,6 +929,40 @@ def test_run_twice_bitwise_deterministic(spk, name, batch):
         np.testing.assert_array_equal(a, b)
 
 
+@pytest.mark.parametrize("name,batch", [("c2", 32), ("c3", 16), ("c1", 1)])
+def test_host_io_graph_equals_copies_around_step(spk, name, batch):
+    """Network.capture_io (the host-to-host step bench.py's e2e times: copies in, the step, copies
+    out as one CUDA graph) gives the same winners and weights as explicit copies around step()."""
+    import torch
+    from paper_2301_13659_b200.network import Network
+    cfg = synth.load_config(name)
+    h_img = torch.from_numpy(synth.images_parallel(cfg, 0, batch)).pin_memory()
+    h_lab = torch.from_numpy(synth.labels(cfg, 0, batch)).pin_memory()
+    Ws = [cu(w) for w in synth.layer_weights(cfg)]
+    outs = []
+    for use_io in (False, True):
+        net = Network(cfg, batch, prec="auto")
+        net.set_weights(Ws)
+        h_win = torch.empty(net.win.shape, dtype=torch.int32).pin_memory()
+        h_nwin = torch.empty(net.nwin.shape, dtype=torch.int32).pin_memory()
+        io_in, io_out = [(net.img, h_img), (net.labels, h_lab)], [(h_win, net.win), (h_nwin, net.nwin)]
+        if use_io:
+            net.capture_io(io_in, io_out)
+            net.set_weights(Ws)  # the capture ran no step: weights are still the initial ones
+            net.replay_io()
+        else:
+            for dst, src in io_in:
+                dst.copy_(src, non_blocking=True)
+            net.step()
+            for dst, src in io_out:
+                dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        tl = cfg["train_layer"]
+        outs.append((h_win.numpy().copy(), h_nwin.numpy().copy(), host(net.weights[tl])))
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+
+
 @pytest.mark.parametrize("name,batch,shards", [("c5", 8, 2), ("c5", 12, 4), ("c2", 64, 2), ("c4", 6, 3)])
 def test_sharded_forward_bitwise_equals_whole_batch(spk, name, batch, shards):
     """SURVEY §8(e) test: the batched forward split into contiguous image shards (rank g gets
