@@ -3,6 +3,7 @@
 // the filter descriptions (tiny, per call) and passed by value; the filtering
 // runs on the GPU.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -201,7 +202,10 @@ spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std:
                 break;
             }
     if (radius == 3 && pairs && (K == 2 || K == 4 || K == 6)) {  // every DoG / LoG front end
-        const bool small = Ho * Wo < 64 * 64;
+        // small maps of few planes (C1: one image) keep one output row per thread, which spreads them
+        // over more CTAs; with many planes (C2: 1024 images) the 4-row kernel is faster
+        // (21.8 -> 19.8 us, profiles/r02_ab_filter_small.txt)
+        const bool small = Ho * Wo < 64 * 64 && (long long)B * C < 2 * 148;
         const dim3 g4(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY * RY), (unsigned)(B * C));
         switch (K / 2 + (small ? 0 : 8)) {
             case 1: filter_kernel<3, 1, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
