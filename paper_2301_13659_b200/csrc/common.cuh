@@ -7,6 +7,8 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 
 #include "spk.h"
 
@@ -46,7 +48,37 @@ inline int sm_count() {
     return n;
 }
 
+// Programmatic dependent launch (PDL): every libspk kernel starts with spk_pdl_wait()
+// (griddepcontrol.wait: a no-op without a programmatic dependency), so a launch may be marked
+// programmatic-serialization-allowed — the next kernel of a stream (or of a captured graph) is
+// then scheduled while the previous one drains and starts its work the moment it completes.
+// SPK_PDL=0 switches the attribute off (A/B).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPK_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 }  // namespace spk
+
+__device__ __forceinline__ void spk_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 #define SPK_CHECK(cond, status, ...)                          \
     do {                                                      \

@@ -190,6 +190,7 @@ namespace {
 template <typename E>
 __global__ void transpose_kernel(const E* __restrict__ in, int R, int C, int ldi, int Cout, int Rout, E pad,
                                  E* __restrict__ out, int ldo) {
+    spk_pdl_wait();
     __shared__ E tile[32][33];
     const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
     for (int i = threadIdx.y; i < 32; i += 8) {
@@ -206,7 +207,7 @@ __global__ void transpose_kernel(const E* __restrict__ in, int R, int C, int ldi
 template <typename E>
 spk_status transpose(const E* in, int R, int C, int ldi, int Cout, int Rout, E pad, E* out, int ldo, cudaStream_t s) {
     const dim3 grid(spk::ceil_div(Cout, 32), spk::ceil_div(Rout, 32)), block(32, 8);
-    transpose_kernel<E><<<grid, block, 0, s>>>(in, R, C, ldi, Cout, Rout, pad, out, ldo);
+    spk::launch(transpose_kernel<E>, grid, block, 0, s, in, R, C, ldi, Cout, Rout, pad, out, ldo);
     return spk::launched("transpose_kernel");
 }
 }  // namespace

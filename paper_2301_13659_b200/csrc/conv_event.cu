@@ -48,6 +48,7 @@ struct EvArgs {
 
 __global__ void ev_pack_kernel(const float* __restrict__ w, int Co, int K, int Co_pad, float inv_scale23,
                                uint32_t* __restrict__ qT, int* __restrict__ flag) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (size_t)K * Co_pad) return;
     const int k = (int)(q / Co_pad), o = (int)(q % Co_pad);
@@ -101,6 +102,7 @@ __device__ __forceinline__ int lds_u8(uint32_t addr) {
 // NCH = ceil(K / 32) synapse chunks held in registers (1..8), or 0 for large receptive fields
 template <typename ACC, int EPI, bool PSTAR, int NCH, int NW, int MPL>
 __global__ void __launch_bounds__(NW * 32) conv_event_kernel(const EvArgs a) {
+    spk_pdl_wait();
     constexpr bool SMALLK = NCH > 0;
     constexpr int MB = 32 * MPL, LOGM = MPL == 4 ? 2 : MPL == 2 ? 1 : 0;  // maps per CTA; entry = k << (15 + LOGM) | lat
     constexpr int kEvThreads = NW * 32, kEvWarps = NW;
@@ -389,7 +391,7 @@ spk_status launch_ev1(const EvArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
     auto k = conv_event_kernel<ACC, EPI, PSTAR, NCH, NW, MPL>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return spk::launched("conv_event_kernel(attr)");
-    k<<<grid, NW * 32, smem, s>>>(a);
+    spk::launch(k, grid, NW * 32, smem, s, a);
     return spk::launched("conv_event_kernel");
 }
 
@@ -484,7 +486,7 @@ spk_status spk_conv_event(const uint8_t* lat_in, const float* w, const spk_conv_
     if (w) {  // w == nullptr: the workspace already holds this layer's packed weights (spk_conv_prepack)
         if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
         const size_t n = (size_t)p.K * p.Co_pad;
-        ev_pack_kernel<<<spk::ceil_div(n, 256), 256, 0, s>>>(w, g.Co, p.K, p.Co_pad, inv_scale23, qT, flag);
+        spk::launch(ev_pack_kernel, spk::ceil_div(n, 256), 256, 0, s, w, g.Co, p.K, p.Co_pad, inv_scale23, qT, flag);
         spk_status st = spk::launched("ev_pack_kernel");
         if (st != SPK_OK) return st;
     }

@@ -9,6 +9,7 @@ namespace {
 __global__ void conv_fp32_kernel(const uint8_t* __restrict__ lat_in, const float* __restrict__ w,
                                  spk_conv_geom g, int Ho, int Wo, int epi, float theta,
                                  void* __restrict__ out0, float* __restrict__ out1) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t HWo = (size_t)Ho * Wo;
     if (q >= (size_t)g.B * g.Co * HWo) return;
@@ -58,7 +59,7 @@ __global__ void conv_fp32_kernel(const uint8_t* __restrict__ lat_in, const float
 spk_status spk_conv_fp32(const uint8_t* lat_in, const float* w, const spk_conv_geom* g, int Ho, int Wo,
                          spk_epilogue epi, float theta, void* out0, void* out1, cudaStream_t s) {
     const size_t n = (size_t)g->B * g->Co * Ho * Wo;
-    conv_fp32_kernel<<<spk::ceil_div(n, 128), 128, 0, s>>>(lat_in, w, *g, Ho, Wo, (int)epi, theta, out0,
+    spk::launch(conv_fp32_kernel, spk::ceil_div(n, 128), 128, 0, s, lat_in, w, *g, Ho, Wo, (int)epi, theta, out0,
                                                           static_cast<float*>(out1));
     return spk::launched("conv_fp32_kernel");
 }

@@ -480,6 +480,7 @@ __device__ __forceinline__ uint32_t live_planes(const TcArgs& a) {
 template <int EPI, bool PSTAR, int TP>
 // 20 warps: 5 per scheduler, whose 16K-register file then allows 96 registers per thread
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
+    spk_pdl_wait();
     constexpr int LOGTP = TP == 1 ? 0 : TP == 16 ? 4 : 5;
     constexpr int PPT = 128 / TP;  // pixels per M tile (TP = 1: one time step, rows = 128 pixels)
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1443,6 +1444,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 // row d*Nt + n holding digit d of output map nt*Nt + n.
 __global__ void pack_weights_kernel(const float* __restrict__ w, int Co, int K, int Nt, int n_ntiles, int nks,
                                     float inv_scale23, uint8_t* __restrict__ wpk, int* __restrict__ flag) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // over (nt, ks, c, n, e)
     const size_t per_plane = (size_t)Nt * KS;
     if (q >= (size_t)n_ntiles * nks * per_plane) return;
@@ -1479,7 +1481,7 @@ void launch(const TcArgs& a, unsigned grid, size_t smem, cudaStream_t s) {
     if (spk::first_on_device(done)) {
         cudaFuncSetAttribute(conv_tc_kernel<EPI, PSTAR, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     }
-    conv_tc_kernel<EPI, PSTAR, TP><<<grid, kThreads, smem, s>>>(a);
+    spk::launch(conv_tc_kernel<EPI, PSTAR, TP>, grid, kThreads, smem, s, a);
 }
 
 template <int TP>
@@ -1617,7 +1619,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     if (w) {  // w == nullptr: the workspace already holds this layer's packed weights (spk_conv_prepack)
         if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
         const size_t nthreads = (size_t)p.n_ntiles * p.nks * p.Nt * KS;
-        pack_weights_kernel<<<spk::ceil_div(nthreads, 256), 256, 0, s>>>(w, g.Co, p.K, p.Nt, p.n_ntiles, p.nks,
+        spk::launch(pack_weights_kernel, spk::ceil_div(nthreads, 256), 256, 0, s, w, g.Co, p.K, p.Nt, p.n_ntiles, p.nks,
                                                                         inv_scale23, wpk, flag);
         spk_status st = spk::launched("pack_weights_kernel");
         if (st != SPK_OK) return st;

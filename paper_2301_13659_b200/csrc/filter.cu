@@ -49,6 +49,7 @@ template <int R, int KC, bool PAIR = false>
 __global__ void __launch_bounds__(TX* TY) filter_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
                                                        int Kr, int pad, int Ho, int Wo, float* __restrict__ out,
                                                        const FilterCoef coef) {
+    spk_pdl_wait();
     constexpr int E = 2 * R + 1, TW = TX + 2 * R, TH = TY + 2 * R;
     __shared__ float tile[TH][TW];
     __shared__ float lut[256];  // u8 / 255 in fp32 (R-SCALE), one IEEE division per value
@@ -126,6 +127,7 @@ template <int R, int KC, bool PAIR = false>
 __global__ void __launch_bounds__(TX* TY) filter_rb_kernel(const uint8_t* __restrict__ img, int C, int H, int W,
                                                           int pad, int Ho, int Wo, float* __restrict__ out,
                                                           const FilterCoef coef) {
+    spk_pdl_wait();
     constexpr int E = 2 * R + 1, OY = TY * RY, TW = TX + 2 * R, TH = OY + 2 * R;
     __shared__ float tile[TH][TW];
     __shared__ float lut[256];  // u8 / 255 in fp32 (R-SCALE)
@@ -208,43 +210,43 @@ spk_status run_filter(const uint8_t* img, int B, int C, int H, int W, const std:
         const bool small = Ho * Wo < 64 * 64 && (long long)B * C < 2 * 148;
         const dim3 g4(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY * RY), (unsigned)(B * C));
         switch (K / 2 + (small ? 0 : 8)) {
-            case 1: filter_kernel<3, 1, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-            case 2: filter_kernel<3, 2, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-            case 3: filter_kernel<3, 3, true><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-            case 9: filter_rb_kernel<3, 1, true><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
-            case 10: filter_rb_kernel<3, 2, true><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
-            default: filter_rb_kernel<3, 3, true><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 1: spk::launch(filter_kernel<3, 1, true>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 2: spk::launch(filter_kernel<3, 2, true>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 3: spk::launch(filter_kernel<3, 3, true>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 9: spk::launch(filter_rb_kernel<3, 1, true>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 10: spk::launch(filter_rb_kernel<3, 2, true>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
+            default: spk::launch(filter_rb_kernel<3, 3, true>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
         }
         return spk::launched("filter_kernel<pairs>");
     }
     if (radius == 3 && (K == 1 || K == 2 || K == 4 || K == 6) && Ho * Wo < 64 * 64) {  // small maps (C1-C3)
         switch (K) {
-            case 1: filter_kernel<3, 1><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-            case 2: filter_kernel<3, 2><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-            case 4: filter_kernel<3, 4><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-            default: filter_kernel<3, 6><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 1: spk::launch(filter_kernel<3, 1>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 2: spk::launch(filter_kernel<3, 2>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            case 4: spk::launch(filter_kernel<3, 4>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+            default: spk::launch(filter_kernel<3, 6>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
         }
         return spk::launched("filter_kernel");
     }
     if (radius == 3 && (K == 1 || K == 2 || K == 4 || K == 6)) {  // large maps (C4, C5)
         const dim3 g4(spk::ceil_div(Wo, TX), spk::ceil_div(Ho, TY * RY), (unsigned)(B * C));
         switch (K) {
-            case 1: filter_rb_kernel<3, 1><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
-            case 2: filter_rb_kernel<3, 2><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
-            case 4: filter_rb_kernel<3, 4><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
-            default: filter_rb_kernel<3, 6><<<g4, blk, 0, s>>>(img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 1: spk::launch(filter_rb_kernel<3, 1>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 2: spk::launch(filter_rb_kernel<3, 2>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
+            case 4: spk::launch(filter_rb_kernel<3, 4>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
+            default: spk::launch(filter_rb_kernel<3, 6>, g4, blk, 0, s, img, C, H, W, pad, Ho, Wo, y, fc); break;
         }
         return spk::launched("filter_rb_kernel");
     }
     switch (radius) {
-        case 0: filter_kernel<0, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 1: filter_kernel<1, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 2: filter_kernel<2, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 3: filter_kernel<3, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 4: filter_kernel<4, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 5: filter_kernel<5, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        case 6: filter_kernel<6, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
-        default: filter_kernel<7, 0><<<grid, blk, 0, s>>>(img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 0: spk::launch(filter_kernel<0, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 1: spk::launch(filter_kernel<1, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 2: spk::launch(filter_kernel<2, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 3: spk::launch(filter_kernel<3, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 4: spk::launch(filter_kernel<4, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 5: spk::launch(filter_kernel<5, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        case 6: spk::launch(filter_kernel<6, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
+        default: spk::launch(filter_kernel<7, 0>, grid, blk, 0, s, img, C, H, W, K, pad, Ho, Wo, y, fc); break;
     }
     return spk::launched("filter_kernel");
 }

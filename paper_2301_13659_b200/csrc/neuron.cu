@@ -16,6 +16,7 @@ constexpr int kT = 256;
 // BTCHW, so a warp reads 32 consecutive floats per step (coalesced).
 __global__ void fire_kernel(const float* __restrict__ pot, int B, int T, size_t N, float theta,
                             uint8_t* __restrict__ lat, float* __restrict__ pstar) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (size_t)B * N) return;
     const size_t b = q / N, i = q % N;
@@ -41,6 +42,7 @@ __global__ void fire_kernel(const float* __restrict__ pot, int B, int T, size_t 
 constexpr int kFireChunk = 8;
 __global__ void __launch_bounds__(kT) fire4_kernel(const float4* __restrict__ pot, int B, int T, size_t N4, float theta,
                                                    uchar4* __restrict__ lat, float4* __restrict__ pstar) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (size_t)B * N4) return;
     const size_t b = q / N4, i = q % N4;
@@ -75,6 +77,7 @@ __global__ void __launch_bounds__(kT) fire4_kernel(const float4* __restrict__ po
 // (32-bit index math inside a plane).
 __global__ void __launch_bounds__(kT) pool_kernel(const uint8_t* __restrict__ lat, long long BC, int ppy, int H, int W,
                                                   int T, spk_pool_geom g, int Ho, int Wo, uint8_t* __restrict__ out) {
+    spk_pdl_wait();
     // blockIdx.y selects a slice of ppy planes; inside it all index math is 32-bit
     const int plane_out = Ho * Wo;
     const int q = blockIdx.x * kT + threadIdx.x;  // < ppy * plane_out <= 2^30
@@ -98,6 +101,7 @@ template <int L>
 __global__ void __launch_bounds__(kT) pool_fixed_kernel(const uint8_t* __restrict__ lat, long long BC, int ppy, int H,
                                                         int W, int T, int S, int Ho, int Wo,
                                                         uint8_t* __restrict__ out) {
+    spk_pdl_wait();
     const int plane_out = Ho * Wo;
     const int q = blockIdx.x * kT + threadIdx.x;
     const long long bc = (long long)blockIdx.y * ppy + q / plane_out;
@@ -139,6 +143,7 @@ template <bool BULK>
 __global__ void __launch_bounds__(kT) pool_smem_kernel(const uint8_t* __restrict__ lat, long long BC, int ppc, int H,
                                                        int W, int T, spk_pool_geom g, int Ho, int Wo,
                                                        uint8_t* __restrict__ out) {
+    spk_pdl_wait();
     extern __shared__ __align__(128) uint8_t psm[];
     __shared__ __align__(8) unsigned long long bar;
     const int HW = H * W, HWo = Ho * Wo;
@@ -248,6 +253,7 @@ constexpr int kInhPix = 256;
 
 __global__ void __launch_bounds__(kT) inhibit_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar, int C,
                                                      int HW, int T, int pc) {
+    spk_pdl_wait();
     __shared__ unsigned long long best[kInhPix];
     const int b = blockIdx.y, p0 = blockIdx.x * pc;  // pc <= kInhPix pixels per CTA
     const int np = min(pc, HW - p0);
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(kT) inhibit_kernel(uint8_t* __restrict__ lat, 
 // potentials once where alive.
 __global__ void __launch_bounds__(kT) inhibit_wide_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar,
                                                           int C, int HW, int T) {
+    spk_pdl_wait();
     const int b = blockIdx.y;
     const int p = 4 * (blockIdx.x * kT + threadIdx.x);
     if (p >= HW) return;
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(kT) inhibit_wide_kernel(uint8_t* __restrict__ 
 // memory — no 200-way atomics on one pixel's slot.
 __global__ void __launch_bounds__(kT) inhibit_small_kernel(uint8_t* __restrict__ lat, float* __restrict__ pstar,
                                                            int C, int HW, int T) {
+    spk_pdl_wait();
     __shared__ unsigned long long part[kT];
     __shared__ uint32_t win_c[32];
     const int b = blockIdx.x;
@@ -403,6 +411,7 @@ __global__ void __launch_bounds__(kT) inhibit_small_kernel(uint8_t* __restrict__
 
 // ---------------------------------------------------------------- gather
 __global__ void gather_kernel(const uint8_t* __restrict__ lat, size_t n, int T, float* __restrict__ f) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
     const int l = min((int)lat[q], T);
@@ -415,6 +424,7 @@ __global__ void gather_kernel(const uint8_t* __restrict__ lat, size_t n, int T, 
 // T+1 possible features come from a shared table of the same IEEE divisions (R-GATHER)
 __global__ void __launch_bounds__(kT) gather4_kernel(const uint32_t* __restrict__ lat, size_t n4, int T,
                                                      float4* __restrict__ f) {
+    spk_pdl_wait();
     __shared__ float tab[256];
     tab[threadIdx.x] = __fdiv_rn((float)(T - min((int)threadIdx.x, T)), (float)T);
     __syncthreads();
@@ -445,6 +455,7 @@ __global__ void __launch_bounds__(kT) gather4_kernel(const uint32_t* __restrict_
 // every input byte is read once and the loads stream straight from HBM.
 __global__ void __launch_bounds__(kT) pool2_vec_kernel(const uint4* __restrict__ lat, long long n_items, int cw,
                                                        int W16, int T, uint2* __restrict__ out) {
+    spk_pdl_wait();
     // item i: chunk c = i % cw of output row r = i / cw (rows of all planes concatenated:
     // output row r reads input rows 2r, 2r + 1 because H is even)
     const uint32_t tt = 0x01010101u * (uint32_t)T;
@@ -478,6 +489,7 @@ __global__ void __launch_bounds__(kT) pool2_vec_kernel(const uint4* __restrict__
 // ---------------------------------------------------------------- boundary conversions
 __global__ void lat_to_dense_kernel(const uint8_t* __restrict__ lat, int B, int T, size_t N,
                                     uint8_t* __restrict__ dense) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t total = (size_t)B * T * N;
     if (q >= total) return;
@@ -487,6 +499,7 @@ __global__ void lat_to_dense_kernel(const uint8_t* __restrict__ lat, int B, int 
 
 __global__ void dense_to_lat_kernel(const uint8_t* __restrict__ dense, int B, int T, size_t N,
                                     uint8_t* __restrict__ lat, unsigned int* __restrict__ bad) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (size_t)B * N) return;
     const size_t b = q / N, i = q % N;
@@ -505,6 +518,7 @@ __global__ void dense_to_lat_kernel(const uint8_t* __restrict__ dense, int B, in
 // ---------------------------------------------------------------- R-STDP routing
 __global__ void rstdp_route_kernel(spk_winner* __restrict__ win, const int32_t* __restrict__ nwin, int B,
                                    int k, const int32_t* __restrict__ labels, int mpc) {
+    spk_pdl_wait();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= B * k) return;
     const int b = q / k, s = q % k;
@@ -516,6 +530,7 @@ __global__ void rstdp_route_kernel(spk_winner* __restrict__ win, const int32_t* 
 // ---------------------------------------------------------------- data-parallel STDP
 __global__ void winners_rebase_kernel(spk_winner* __restrict__ win, const int32_t* __restrict__ nwin, int B, int k,
                                       int b0) {
+    spk_pdl_wait();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= B * k) return;
     const int b = q / k, s = q % k;
@@ -535,12 +550,12 @@ extern "C" spk_status spk_fire(const float* pot, int B, int T, int C, int H, int
     const bool vec = (N & 3) == 0 && (reinterpret_cast<uintptr_t>(pot) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && (reinterpret_cast<uintptr_t>(pstar) & 15) == 0;
     if (vec) {
-        fire4_kernel<<<spk::ceil_div((size_t)B * (N / 4), kT), kT, 0, spk::as_cuda(stream)>>>(
+        spk::launch(fire4_kernel, spk::ceil_div((size_t)B * (N / 4), kT), kT, 0, spk::as_cuda(stream),
             reinterpret_cast<const float4*>(pot), B, T, N / 4, theta, reinterpret_cast<uchar4*>(lat),
             reinterpret_cast<float4*>(pstar));
         return spk::launched("fire4_kernel");
     }
-    fire_kernel<<<spk::ceil_div((size_t)B * N, kT), kT, 0, spk::as_cuda(stream)>>>(pot, B, T, N, theta, lat,
+    spk::launch(fire_kernel, spk::ceil_div((size_t)B * N, kT), kT, 0, spk::as_cuda(stream), pot, B, T, N, theta, lat,
                                                                                  pstar);
     return spk::launched("fire_kernel");
 }
@@ -576,7 +591,7 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
         const int cw = W / 16;
         const long long n_items = BC * Ho * cw;
         const unsigned blocks = (unsigned)std::min<long long>((n_items + 2 * kT - 1) / (2 * kT), (long long)spk::sm_count() * 8);
-        pool2_vec_kernel<<<blocks, kT, 0, spk::as_cuda(stream)>>>(reinterpret_cast<const uint4*>(lat), n_items, cw,
+        spk::launch(pool2_vec_kernel, blocks, kT, 0, spk::as_cuda(stream), reinterpret_cast<const uint4*>(lat), n_items, cw,
                                                                   cw, T, reinterpret_cast<uint2*>(out));
         return spk::launched("pool2_vec_kernel");
     }
@@ -593,10 +608,10 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
             cudaFuncSetAttribute(pool_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPoolSmem);
         }
         if (bulk) {
-            pool_smem_kernel<true><<<(unsigned)nblk, kT, smem, spk::as_cuda(stream)>>>(lat, BC, ppc, H, W, T, *p, Ho, Wo, out);
+            spk::launch(pool_smem_kernel<true>, (unsigned)nblk, kT, smem, spk::as_cuda(stream), lat, BC, ppc, H, W, T, *p, Ho, Wo, out);
             return spk::launched("pool_smem_kernel<bulk>");
         }
-        pool_smem_kernel<false><<<(unsigned)nblk, kT, smem, spk::as_cuda(stream)>>>(lat, BC, ppc, H, W, T, *p, Ho, Wo, out);
+        spk::launch(pool_smem_kernel<false>, (unsigned)nblk, kT, smem, spk::as_cuda(stream), lat, BC, ppc, H, W, T, *p, Ho, Wo, out);
         return spk::launched("pool_smem_kernel");
     }
     const long long ppy = std::min<long long>(BC, std::max(1, (1 << 30) / plane_out));
@@ -609,12 +624,12 @@ extern "C" spk_status spk_pool(const uint8_t* lat, int B, int C, int H, int W, i
     }();
     if (fixed_ok && p->Ph == 0 && p->Pw == 0 && p->Lh == p->Lw && p->Sh == p->Sw && (p->Lh == 2 || p->Lh == 3)) {
         if (p->Lh == 2)
-            pool_fixed_kernel<2><<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, p->Sh, Ho, Wo, out);
+            spk::launch(pool_fixed_kernel<2>, grid, kT, 0, spk::as_cuda(stream), lat, BC, (int)ppy, H, W, T, p->Sh, Ho, Wo, out);
         else
-            pool_fixed_kernel<3><<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, p->Sh, Ho, Wo, out);
+            spk::launch(pool_fixed_kernel<3>, grid, kT, 0, spk::as_cuda(stream), lat, BC, (int)ppy, H, W, T, p->Sh, Ho, Wo, out);
         return spk::launched("pool_fixed_kernel");
     }
-    pool_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, BC, (int)ppy, H, W, T, *p, Ho, Wo, out);
+    spk::launch(pool_kernel, grid, kT, 0, spk::as_cuda(stream), lat, BC, (int)ppy, H, W, T, *p, Ho, Wo, out);
     return spk::launched("pool_kernel");
 }
 
@@ -630,12 +645,12 @@ extern "C" spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int 
     SPK_CHECK(B <= 65535, SPK_ERR_SHAPE, "B=%d > 65535", B);
     const int HW = H * W;
     if (HW <= 32) {
-        inhibit_small_kernel<<<(unsigned)B, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
+        spk::launch(inhibit_small_kernel, (unsigned)B, kT, 0, spk::as_cuda(stream), lat, pstar, C, HW, T);
         return spk::launched("inhibit_small_kernel");
     }
     if (HW >= 4096 && (HW & 3) == 0 && ((reinterpret_cast<uintptr_t>(lat) | reinterpret_cast<uintptr_t>(pstar)) & 15) == 0) {
         const dim3 grid(spk::ceil_div((size_t)HW / 4, kT), (unsigned)B);
-        inhibit_wide_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T);
+        spk::launch(inhibit_wide_kernel, grid, kT, 0, spk::as_cuda(stream), lat, pstar, C, HW, T);
         return spk::launched("inhibit_wide_kernel");
     }
     // fewer pixels per CTA when the grid would not cover the SMs (C1: one 28x28 sample),
@@ -646,7 +661,7 @@ extern "C" spk_status spk_inhibit(uint8_t* lat, float* pstar, int B, int C, int 
         pc = std::max(1, std::min(kInhPix, (HW + want - 1) / want));
     }
     const dim3 grid(spk::ceil_div((size_t)HW, pc), (unsigned)B);
-    inhibit_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(lat, pstar, C, HW, T, pc);
+    spk::launch(inhibit_kernel, grid, kT, 0, spk::as_cuda(stream), lat, pstar, C, HW, T, pc);
     return spk::launched("inhibit_kernel");
 }
 
@@ -659,11 +674,11 @@ extern "C" spk_status spk_gather(const uint8_t* lat, size_t n, int T, float* fea
     if (n % 4 == 0 && (reinterpret_cast<uintptr_t>(lat) & 3) == 0 && (reinterpret_cast<uintptr_t>(feat) & 15) == 0) {
         const size_t n4 = n / 4;
         const unsigned blocks = (unsigned)std::min<size_t>(spk::ceil_div(n4, (size_t)kT * 4), (size_t)spk::sm_count() * 8);
-        gather4_kernel<<<blocks, kT, 0, spk::as_cuda(stream)>>>(reinterpret_cast<const uint32_t*>(lat), n4, T,
+        spk::launch(gather4_kernel, blocks, kT, 0, spk::as_cuda(stream), reinterpret_cast<const uint32_t*>(lat), n4, T,
                                                                 reinterpret_cast<float4*>(feat));
         return spk::launched("gather4_kernel");
     }
-    gather_kernel<<<spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream)>>>(lat, n, T, feat);
+    spk::launch(gather_kernel, spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream), lat, n, T, feat);
     return spk::launched("gather_kernel");
 }
 
@@ -675,7 +690,7 @@ extern "C" spk_status spk_lat_to_dense(const uint8_t* lat, int B, int T, size_t 
     SPK_CHECK(B >= 1 && N >= 1, SPK_ERR_SHAPE, "non-positive size");
     SPK_CHECK(T >= 1 && T <= 254, SPK_ERR_UNSUPPORTED, "T=%d outside 1..254", T);
     const size_t n = (size_t)B * T * N;
-    lat_to_dense_kernel<<<spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream)>>>(lat, B, T, N, dense);
+    spk::launch(lat_to_dense_kernel, spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream), lat, B, T, N, dense);
     return spk::launched("lat_to_dense_kernel");
 }
 
@@ -692,7 +707,7 @@ extern "C" spk_status spk_dense_to_lat(const uint8_t* dense, int B, int T, size_
     if (cudaMemsetAsync(bad_index, 0xff, sizeof(int32_t), s) != cudaSuccess)
         return spk::launched("memset(bad_index)");
     const size_t n = (size_t)B * N;
-    dense_to_lat_kernel<<<spk::ceil_div(n, kT), kT, 0, s>>>(dense, B, T, N, lat,
+    spk::launch(dense_to_lat_kernel, spk::ceil_div(n, kT), kT, 0, s, dense, B, T, N, lat,
                                                             reinterpret_cast<unsigned int*>(bad_index));
     return spk::launched("dense_to_lat_kernel");
 }
@@ -705,7 +720,7 @@ extern "C" spk_status spk_rstdp_route(spk_winner* win, const int32_t* nwin, int 
     SPK_CHECK_PTR(labels);
     SPK_CHECK(B >= 1 && k >= 1, SPK_ERR_ARG, "B=%d k=%d", B, k);
     SPK_CHECK(maps_per_class >= 1, SPK_ERR_ARG, "maps_per_class < 1");
-    rstdp_route_kernel<<<spk::ceil_div((size_t)B * k, kT), kT, 0, spk::as_cuda(stream)>>>(win, nwin, B, k, labels,
+    spk::launch(rstdp_route_kernel, spk::ceil_div((size_t)B * k, kT), kT, 0, spk::as_cuda(stream), win, nwin, B, k, labels,
                                                                                         maps_per_class);
     return spk::launched("rstdp_route_kernel");
 }
@@ -717,6 +732,6 @@ extern "C" spk_status spk_winners_rebase(spk_winner* win, const int32_t* nwin, i
     SPK_CHECK_PTR(nwin);
     SPK_CHECK(B >= 1 && k >= 1 && b0 >= 0, SPK_ERR_ARG, "B=%d k=%d b0=%d", B, k, b0);
     SPK_CHECK((long long)B * k < (1ll << 31), SPK_ERR_ARG, "B*k too large");
-    winners_rebase_kernel<<<spk::ceil_div((size_t)B * k, kT), kT, 0, spk::as_cuda(stream)>>>(win, nwin, B, k, b0);
+    spk::launch(winners_rebase_kernel, spk::ceil_div((size_t)B * k, kT), kT, 0, spk::as_cuda(stream), win, nwin, B, k, b0);
     return spk::launched("winners_rebase_kernel");
 }

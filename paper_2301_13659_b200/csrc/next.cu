@@ -22,6 +22,7 @@ constexpr int kT = 256;
 // bits, so an integer atomicMax on the bit pattern is exact and order-independent)
 __global__ void __launch_bounds__(kT) rate_max_kernel(const float* __restrict__ y, int N, float thresh,
                                                       unsigned* __restrict__ vmax_bits) {
+    spk_pdl_wait();
     const int b = blockIdx.y;
     const float* v = y + (size_t)b * N;
     unsigned m = 0u;
@@ -54,6 +55,7 @@ __device__ __forceinline__ uint64_t mix_state(uint64_t z) {
 __global__ void __launch_bounds__(kT) rate_emit_kernel(const float* __restrict__ y, int N, int T, float thresh,
                                                        uint64_t seed, uint64_t b0, const unsigned* __restrict__ vmax_bits,
                                                        uint8_t* __restrict__ out) {
+    spk_pdl_wait();
     const int b = blockIdx.y;
     const int i0 = (blockIdx.x * kT + threadIdx.x) * 4;
     if (i0 >= N) return;
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(kT) rate_emit_kernel(const float* __restrict__
 // rate[b][i] = (#t with step[b][t][i] == 0) / T (R-GATHER on a non-cumulative train)
 __global__ void __launch_bounds__(kT) rate_gather_kernel(const uint8_t* __restrict__ step, int B, int T, size_t N,
                                                          float* __restrict__ rate) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * kT + threadIdx.x;
     if (q >= (size_t)B * N) return;
     const size_t b = q / N, i = q % N;
@@ -112,6 +115,7 @@ __global__ void __launch_bounds__(kT) rate_gather_kernel(const uint8_t* __restri
 __global__ void __launch_bounds__(kT) pool_rates_kernel(const uint8_t* __restrict__ step, const float* __restrict__ rate,
                                                         int B, int T, int C, int H, int W, spk_pool_geom g, int Ho,
                                                         int Wo, uint8_t* __restrict__ out) {
+    spk_pdl_wait();
     const size_t q = (size_t)blockIdx.x * kT + threadIdx.x;
     const size_t plane = (size_t)Ho * Wo;
     if (q >= (size_t)B * C * plane) return;
@@ -145,6 +149,7 @@ __global__ void __launch_bounds__(kT) pool_rates_kernel(const uint8_t* __restric
 // ------------------------------------------------------------ quantize
 __global__ void __launch_bounds__(kT) quantize_kernel(float* __restrict__ w, size_t n, float lower, float mid,
                                                       float upper) {
+    spk_pdl_wait();
     for (size_t i = (size_t)blockIdx.x * kT + threadIdx.x; i < n; i += (size_t)gridDim.x * kT)
         w[i] = (w[i] < mid) ? lower : upper;
 }
@@ -173,6 +178,7 @@ __device__ __forceinline__ uint64_t block_min_u64(uint64_t v, uint64_t* red) {
 __global__ void __launch_bounds__(kT) fcwta_kernel(const uint8_t* __restrict__ lat, const float* __restrict__ pstar,
                                                    int O, int T, int k, int radius, int use_smem,
                                                    spk_winner* __restrict__ win, int32_t* __restrict__ nwin) {
+    spk_pdl_wait();
     extern __shared__ uint64_t keys[];  // [O] when use_smem
     __shared__ uint64_t red[kT / 32];
     const int b = blockIdx.x;
@@ -252,11 +258,11 @@ extern "C" spk_status spk_rate_code(const float* y, int B, int N, int T, float t
     unsigned* vmax = static_cast<unsigned*>(ws);
     if (cudaMemsetAsync(vmax, 0, (size_t)B * sizeof(unsigned), s) != cudaSuccess) return spk::launched("memset(vmax)");
     const int chunks = std::min(64, (N + kT - 1) / kT);
-    rate_max_kernel<<<dim3(chunks, B), kT, 0, s>>>(y, N, thresh, vmax);
+    spk::launch(rate_max_kernel, dim3(chunks, B), kT, 0, s, y, N, thresh, vmax);
     spk_status st = spk::launched("rate_max_kernel");
     if (st != SPK_OK) return st;
     const unsigned gx = spk::ceil_div((size_t)(N + 3) / 4, kT);
-    rate_emit_kernel<<<dim3(gx, B), kT, 0, s>>>(y, N, T, thresh, seed, b0, vmax, step);
+    spk::launch(rate_emit_kernel, dim3(gx, B), kT, 0, s, y, N, T, thresh, seed, b0, vmax, step);
     return spk::launched("rate_emit_kernel");
 }
 
@@ -265,7 +271,7 @@ extern "C" spk_status spk_rate_gather(const uint8_t* step, int B, int T, size_t 
     SPK_CHECK_PTR(step);
     SPK_CHECK_PTR(rate);
     SPK_CHECK(B >= 1 && T >= 1 && N >= 1, SPK_ERR_SHAPE, "B, T, N must be >= 1");
-    rate_gather_kernel<<<spk::ceil_div((size_t)B * N, kT), kT, 0, spk::as_cuda(stream)>>>(step, B, T, N, rate);
+    spk::launch(rate_gather_kernel, spk::ceil_div((size_t)B * N, kT), kT, 0, spk::as_cuda(stream), step, B, T, N, rate);
     return spk::launched("rate_gather_kernel");
 }
 
@@ -282,7 +288,7 @@ extern "C" spk_status spk_pool_rates(const uint8_t* step, const float* rate, int
     SPK_CHECK(H + 2 * p->Ph >= p->Lh && W + 2 * p->Pw >= p->Lw, SPK_ERR_SHAPE, "window larger than padded input (Eq. 3)");
     const int Ho = (H + 2 * p->Ph - p->Lh) / p->Sh + 1, Wo = (W + 2 * p->Pw - p->Lw) / p->Sw + 1;
     const size_t n = (size_t)B * C * Ho * Wo;
-    pool_rates_kernel<<<spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream)>>>(step, rate, B, T, C, H, W, *p, Ho, Wo,
+    spk::launch(pool_rates_kernel, spk::ceil_div(n, kT), kT, 0, spk::as_cuda(stream), step, rate, B, T, C, H, W, *p, Ho, Wo,
                                                                               out);
     return spk::launched("pool_rates_kernel");
 }
@@ -295,7 +301,7 @@ extern "C" spk_status spk_quantize(float* w, size_t n, float lower, float mid, f
     SPK_CHECK(lower <= mid && mid <= upper, SPK_ERR_ARG, "quantize needs lower <= mid <= upper");
     if (n == 0) return SPK_OK;
     const unsigned grid = std::min<size_t>(spk::ceil_div(n, kT), 148u * 16u);
-    quantize_kernel<<<grid, kT, 0, spk::as_cuda(stream)>>>(w, n, lower, mid, upper);
+    spk::launch(quantize_kernel, grid, kT, 0, spk::as_cuda(stream), w, n, lower, mid, upper);
     return spk::launched("quantize_kernel");
 }
 
@@ -316,6 +322,6 @@ extern "C" spk_status spk_fcwta(const uint8_t* lat, const float* pstar, int B, i
     cudaStream_t s = spk::as_cuda(stream);
     if (use_smem && smem > 48 * 1024)
         cudaFuncSetAttribute(fcwta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fcwta_kernel<<<B, kT, use_smem ? smem : 0, s>>>(lat, pstar, O, T, k, radius, use_smem, win, nwin);
+    spk::launch(fcwta_kernel, B, kT, use_smem ? smem : 0, s, lat, pstar, O, T, k, radius, use_smem, win, nwin);
     return spk::launched("fcwta_kernel");
 }

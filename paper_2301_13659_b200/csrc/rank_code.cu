@@ -208,6 +208,7 @@ template <bool STAGED, int kThreads>
 __global__ void __launch_bounds__(kThreads) rank_code_kernel(const float* __restrict__ y, int N, int T,
                                                             float thresh, int sort,
                                                             uint8_t* __restrict__ lat) {
+    spk_pdl_wait();
     extern __shared__ __align__(16) unsigned char dyn[];
     __shared__ RankSmem sm;
     rank_code_body<STAGED, kThreads>(y + (size_t)blockIdx.x * N, N, T, thresh, sort, lat + (size_t)blockIdx.x * N, sm,
@@ -222,6 +223,7 @@ constexpr int kSortMax = 8192, kSortThreads = 512;
 
 __global__ void __launch_bounds__(kSortThreads) rank_code_sort_kernel(const float* __restrict__ y, int N, int T,
                                                                       float thresh, uint8_t* __restrict__ lat) {
+    spk_pdl_wait();
     extern __shared__ unsigned long long keys[];  // capacity: next power of two >= N
     __shared__ unsigned int s_n;
     const float* ys = y + (size_t)blockIdx.x * N;
@@ -296,6 +298,7 @@ struct HistCfg {
 template <int SHIFT, int kHT, int kCand, bool STAGE>
 __global__ void __launch_bounds__(kHT) rank_code_hist_kernel(const float* __restrict__ y, int N, int T, float thresh,
                                                             uint8_t* __restrict__ lat) {
+    spk_pdl_wait();
     constexpr int kBkt = HistCfg<SHIFT, kHT, kCand, STAGE>::kBkt, kNW = kHT / 32;
     static_assert(kBkt / 2 >= kCand, "the bucket table is reused for the grouped candidates");
     extern __shared__ __align__(16) unsigned char dyn[];
@@ -540,7 +543,7 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
             cudaFuncSetAttribute(rank_code_hist_kernel<SH, TH, 1024, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(kSortMax));
         }
-        rank_code_hist_kernel<SH, TH, 1024, true><<<B, TH, Cfg::smem(N), s>>>(y, N, T, thresh, lat);
+        spk::launch(rank_code_hist_kernel<SH, TH, 1024, true>, B, TH, Cfg::smem(N), s, y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel<small>");
     }
     if (sort && N <= kSortMax) {
@@ -552,7 +555,7 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
             cudaFuncSetAttribute(rank_code_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned long long) * kSortMax));
         }
-        rank_code_sort_kernel<<<B, kSortThreads, smem, s>>>(y, N, T, thresh, lat);
+        spk::launch(rank_code_sort_kernel, B, kSortThreads, smem, s, y, N, T, thresh, lat);
         return spk::launched("rank_code_sort_kernel");
     }
     if (sort) {  // larger samples: bucket histogram + boundary-bucket sort
@@ -564,7 +567,7 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
             cudaFuncSetAttribute(rank_code_hist_kernel<17, 1024, 4096, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem(0));
         }
-        rank_code_hist_kernel<17, 1024, 4096, false><<<B, 1024, Cfg::smem(0), s>>>(y, N, T, thresh, lat);
+        spk::launch(rank_code_hist_kernel<17, 1024, 4096, false>, B, 1024, Cfg::smem(0), s, y, N, T, thresh, lat);
         return spk::launched("rank_code_hist_kernel");
     }
     if (N <= 8192) {  // small samples: 256-thread CTAs, several resident per SM
@@ -574,7 +577,7 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
             cudaFuncSetAttribute(rank_code_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned int) * 8192));
         }
-        rank_code_kernel<true, 256><<<B, 256, smem, s>>>(y, N, T, thresh, sort, lat);
+        spk::launch(rank_code_kernel<true, 256>, B, 256, smem, s, y, N, T, thresh, sort, lat);
         return spk::launched("rank_code_kernel<staged,256>");
     }
     if (N <= kStageMax) {
@@ -584,9 +587,9 @@ extern "C" spk_status spk_rank_code(const float* y, int B, int N, int T, float t
             cudaFuncSetAttribute(rank_code_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(unsigned int) * kStageMax));
         }
-        rank_code_kernel<true, 1024><<<B, 1024, smem, s>>>(y, N, T, thresh, sort, lat);
+        spk::launch(rank_code_kernel<true, 1024>, B, 1024, smem, s, y, N, T, thresh, sort, lat);
         return spk::launched("rank_code_kernel<staged,1024>");
     }
-    rank_code_kernel<false, 1024><<<B, 1024, 0, s>>>(y, N, T, thresh, sort, lat);
+    spk::launch(rank_code_kernel<false, 1024>, B, 1024, 0, s, y, N, T, thresh, sort, lat);
     return spk::launched("rank_code_kernel<global,1024>");
 }

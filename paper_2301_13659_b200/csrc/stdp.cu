@@ -29,6 +29,7 @@ __device__ __forceinline__ bool winner_valid(const spk_winner& w, int B, int ncf
 __global__ void stdp_slotmap_kernel(const spk_winner* __restrict__ win, const int32_t* __restrict__ nwin, int B,
                                     int k, int ncfg, int Ho, int Wo, int Co, int32_t* __restrict__ slotmap,
                                     int32_t* __restrict__ invalid) {
+    spk_pdl_wait();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= B * k) return;
     const int b = s / k, q = s - b * k;
@@ -47,6 +48,7 @@ __global__ void __launch_bounds__(kBucketThreads) stdp_bucket_kernel(const int32
                                                                     int cap, int32_t* __restrict__ list,
                                                                     int32_t* __restrict__ start,
                                                                     int32_t* __restrict__ cnt) {
+    spk_pdl_wait();
     constexpr int kWarps = kBucketThreads / 32;
     __shared__ int wsum[kWarps];
     const int o = blockIdx.x;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restr
                                                                   const int32_t* __restrict__ start,
                                                                   const int32_t* __restrict__ cnt,
                                                                   const Cfgs cfgs, int ncfg) {
+    spk_pdl_wait();
     __shared__ long long s_ofs[kWinChunk];  // lat_in offset of (b, channel 0, y0, x0)
     __shared__ int s_y0[kWinChunk], s_x0[kWinChunk], s_t[kWinChunk];
     __shared__ float s_ap[kWinChunk], s_am[kWinChunk], s_lo[kWinChunk], s_hi[kWinChunk];  // winner's config
@@ -238,11 +241,11 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     cudaStream_t s = spk::as_cuda(stream);
     int32_t* invalid = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + need - 256);  // spk_stdp_status
     if (cudaMemsetAsync(invalid, 0, sizeof(int32_t), s) != cudaSuccess) return spk::launched("memset(invalid)");
-    stdp_slotmap_kernel<<<spk::ceil_div((size_t)cap, 256), 256, 0, s>>>(win, nwin, g->B, k, ncfg, Ho, Wo, g->Co,
+    spk::launch(stdp_slotmap_kernel, spk::ceil_div((size_t)cap, 256), 256, 0, s, win, nwin, g->B, k, ncfg, Ho, Wo, g->Co,
                                                                       slotmap, invalid);
     spk_status st = spk::launched("stdp_slotmap_kernel");
     if (st != SPK_OK) return st;
-    stdp_bucket_kernel<<<g->Co, kBucketThreads, 0, s>>>(slotmap, cap, cap, list, start, cnt);
+    spk::launch(stdp_bucket_kernel, g->Co, kBucketThreads, 0, s, slotmap, cap, cap, list, start, cnt);
     st = spk::launched("stdp_bucket_kernel");
     if (st != SPK_OK) return st;
     const size_t K = (size_t)g->Ci * g->Kh * g->Kw;
@@ -250,10 +253,10 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     // average winners per map (upper bound: every slot a winner) picks the tile width
     if ((long long)g->B * k >= 16ll * g->Co) {
         const dim3 grid(spk::ceil_div(K, 32), (unsigned)g->Co);
-        stdp_update_kernel<32, SPK_STDP_T32><<<grid, SPK_STDP_T32, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+        spk::launch(stdp_update_kernel<32, SPK_STDP_T32>, grid, SPK_STDP_T32, 0, s, w, *g, lat_in, win, list, start, cnt, cc, ncfg);
     } else {
         const dim3 grid(spk::ceil_div(K, 128), (unsigned)g->Co);
-        stdp_update_kernel<128, 256><<<grid, 256, 0, s>>>(w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+        spk::launch(stdp_update_kernel<128, 256>, grid, 256, 0, s, w, *g, lat_in, win, list, start, cnt, cc, ncfg);
     }
     return spk::launched("stdp_update_kernel");
 }

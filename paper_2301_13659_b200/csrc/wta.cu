@@ -62,6 +62,7 @@ struct WtaArgs {
 // KK = per-pixel keep count (>= min(k, C)) for mode 1
 template <int KK>
 __global__ void __launch_bounds__(kThreads) wta_cluster_kernel(const WtaArgs a) {
+    spk_pdl_wait();
     constexpr int kChan = KK >= 4 ? 16 : 8;  // channels read per batch in the per-pixel pre-reduction
     extern __shared__ unsigned long long keys[];  // [kCapKeys]
     __shared__ unsigned long long red[kThreads / 32];
@@ -335,13 +336,15 @@ spk_status launch_wta(const WtaArgs& a, int B, size_t cap, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = (unsigned)a.cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see spk::launch
+    at[1].val.programmaticStreamSerializationAllowed = spk::pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, kern, a);
     return spk::launched("wta_cluster_kernel");
 }
