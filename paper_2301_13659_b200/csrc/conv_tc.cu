@@ -480,7 +480,6 @@ __device__ __forceinline__ uint32_t live_planes(const TcArgs& a) {
 template <int EPI, bool PSTAR, int TP>
 // 20 warps: 5 per scheduler, whose 16K-register file then allows 96 registers per thread
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
-    spk_pdl_wait();
     constexpr int LOGTP = TP == 1 ? 0 : TP == 16 ? 4 : 5;
     constexpr int PPT = 128 / TP;  // pixels per M tile (TP = 1: one time step, rows = 128 pixels)
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -554,6 +553,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // the setup above (synapse table, barriers, TMEM allocation) reads only kernel parameters and
+    // shared memory, so under programmatic dependent launch it overlaps the previous kernel's tail;
+    // every role reads the previous kernels' outputs only after this wait
+    spk_pdl_wait();
 #ifndef SPK_TMEM0
 #define SPK_TMEM0 1
 #endif
