@@ -1448,30 +1448,40 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 __global__ void pack_weights_kernel(const float* __restrict__ w, int Co, int K, int Nt, int n_ntiles, int nks,
                                     float inv_scale23, uint8_t* __restrict__ wpk, int* __restrict__ flag) {
     spk_pdl_wait();
-    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // over (nt, ks, c, n, e)
-    const size_t per_plane = (size_t)Nt * KS;
-    if (q >= (size_t)n_ntiles * nks * per_plane) return;
-    const size_t blk = q / per_plane, r = q % per_plane;
+    // one thread per (nt, ks, c, n, 4 consecutive synapses e0..e0+3): one 4-byte store per digit
+    // plane instead of four byte stores
+    const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // over (nt, ks, c, n, e4)
+    const size_t per_plane4 = (size_t)Nt * (KS / 4);
+    if (q >= (size_t)n_ntiles * nks * per_plane4) return;
+    const size_t blk = q / per_plane4, r = q % per_plane4;
     const int nt = (int)(blk / nks), ks = (int)(blk % nks);
-    const int c = (int)(r / ((size_t)Nt * 16)), r2 = (int)(r % ((size_t)Nt * 16));
-    const int n = r2 / 16, e = r2 % 16;
-    const int k = ks * KS + c * 16 + e, o = nt * Nt + n;
-    float v = 0.0f;
-    if (o < Co && k < K) v = w[(size_t)o * K + k];
-    float x = __fmul_rn(v, inv_scale23);  // exact: inv_scale23 is a power of two
-    if (!(x >= 0.0f) || x > 8388608.0f) {  // negative, NaN or above the scale: clamp and flag
-        atomicOr(flag, 1);
-        x = (x > 8388608.0f) ? 8388608.0f : 0.0f;
-    }
-    const uint32_t qv = (uint32_t)__float2int_rn(x);  // 0 .. 2^23
-    uint8_t* base = wpk + blk * 3 * per_plane + (size_t)c * 3 * Nt * 16;
+    const int c = (int)(r / ((size_t)Nt * 4)), r2 = (int)(r % ((size_t)Nt * 4));
+    const int n = r2 / 4, e0 = (r2 % 4) * 4;
+    const int k0 = ks * KS + c * 16 + e0, o = nt * Nt + n;
+    uint32_t pk[3] = {0u, 0u, 0u};
     uint32_t live = 0;  // bit 1 + d: digit d non-zero
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float v = 0.0f;
+        if (o < Co && k0 + i < K) v = w[(size_t)o * K + k0 + i];
+        float x = __fmul_rn(v, inv_scale23);  // exact: inv_scale23 is a power of two
+        if (!(x >= 0.0f) || x > 8388608.0f) {  // negative, NaN or above the scale: clamp and flag
+            atomicOr(flag, 1);
+            x = (x > 8388608.0f) ? 8388608.0f : 0.0f;
+        }
+        const uint32_t qv = (uint32_t)__float2int_rn(x);  // 0 .. 2^23
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const uint32_t digit = (qv >> (8 * d)) & 255u;
+            pk[d] |= digit << (8 * i);
+            live |= digit ? 2u << d : 0u;
+        }
+    }
+    uint8_t* base = wpk + blk * 3 * ((size_t)Nt * KS) + (size_t)c * 3 * Nt * 16;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         const int row = d * Nt + n;
-        const uint32_t digit = (qv >> (8 * d)) & 255u;
-        base[(size_t)(row >> 3) * 128 + (row & 7) * 16 + e] = (uint8_t)digit;
-        live |= digit ? 2u << d : 0u;
+        *reinterpret_cast<uint32_t*>(base + (size_t)(row >> 3) * 128 + (row & 7) * 16 + e0) = pk[d];
     }
     live = __reduce_or_sync(__activemask(), live);
     // one atomic per warp, and only while it still adds a bit (the flag fills up at once)
@@ -1621,7 +1631,7 @@ spk_status spk_conv_tc(const uint8_t* lat_in, const float* w, const spk_conv_geo
     uint8_t* wpk = static_cast<uint8_t*>(ws) + 256;
     if (w) {  // w == nullptr: the workspace already holds this layer's packed weights (spk_conv_prepack)
         if (cudaMemsetAsync(flag, 0, sizeof(int), s) != cudaSuccess) return spk::launched("memset(flag)");
-        const size_t nthreads = (size_t)p.n_ntiles * p.nks * p.Nt * KS;
+        const size_t nthreads = (size_t)p.n_ntiles * p.nks * p.Nt * (KS / 4);
         spk::launch(pack_weights_kernel, spk::ceil_div(nthreads, 256), 256, 0, s, w, g.Co, p.K, p.Nt, p.n_ntiles, p.nks,
                                                                         inv_scale23, wpk, flag);
         spk_status st = spk::launched("pack_weights_kernel");
