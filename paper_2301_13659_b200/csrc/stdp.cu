@@ -9,6 +9,8 @@
 //   (2) one thread per weight element walking its map's winners in order.
 // The per-weight arithmetic is fp32 in the order of Eq. 4-6 with explicit
 // round-to-nearest intrinsics (no contraction): bit-identical to the oracle.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -201,6 +203,89 @@ __global__ void __launch_bounds__(kUpdThreads) stdp_update_kernel(float* __restr
     if (valid2) w[(size_t)o * K + kk2] = W;
 }
 
+// Per-weight form: one thread per weight runs ITS gathers and ITS ordered chain together — no
+// shared [winner][weight] table and no phase barrier, so a CTA covers 256 weights with 256 chains
+// (the 32-weight tile leaves 7 of 8 warps idle during the chain) and the gathers of the next
+// winners are issued while the chain of the current ones runs.  Same fp32 chain, same order.
+template <int kThr>
+__global__ void __launch_bounds__(kThr) stdp_update_pw_kernel(float* __restrict__ w, spk_conv_geom g,
+                                                              const uint8_t* __restrict__ lat_in,
+                                                              const spk_winner* __restrict__ win,
+                                                              const int32_t* __restrict__ list,
+                                                              const int32_t* __restrict__ start,
+                                                              const int32_t* __restrict__ cnt, const Cfgs cfgs,
+                                                              int ncfg) {
+    spk_pdl_wait();
+    __shared__ long long s_ofs[kWinChunk];  // lat_in offset of (b, channel 0, y0, x0)
+    __shared__ int s_y0[kWinChunk], s_x0[kWinChunk], s_t[kWinChunk];
+    __shared__ float s_ap[kWinChunk], s_am[kWinChunk], s_lo[kWinChunk], s_hi[kWinChunk];  // winner's config
+    __shared__ uint8_t s_st[kWinChunk];
+    __shared__ spk_stdp_config s_cf[kMaxCfg];
+    const int o = blockIdx.y;
+    const int n = cnt[o];
+    if (n == 0) return;
+    const int K = g.Ci * g.Kh * g.Kw;
+    const int KhKw = g.Kh * g.Kw;
+    const long long HW = (long long)g.Hi * g.Wi;
+    const int kk = blockIdx.x * kThr + threadIdx.x;
+    const bool valid = kk < K;
+    const int c1 = kk / KhKw, r1 = kk - c1 * KhKw, i1 = r1 / g.Kw, j1 = r1 - i1 * g.Kw;
+    const long long own = c1 * HW + (long long)i1 * g.Wi + j1;
+#pragma unroll
+    for (int q = 0; q < kMaxCfg; ++q)  // static indices: the parameter block stays in constant space
+        if (threadIdx.x == q && q < ncfg) s_cf[q] = cfgs.c[q];
+    float W = valid ? w[(size_t)o * K + kk] : 0.0f;
+    for (int e0 = 0; e0 < n; e0 += kWinChunk) {
+        const int m = min(kWinChunk, n - e0);
+        __syncthreads();
+        for (int q = threadIdx.x; q < m; q += kThr) {
+            const spk_winner wn = win[list[(size_t)start[o] + e0 + q]];
+            const int y0 = wn.y * g.Sh - g.Ph, x0 = wn.x * g.Sw - g.Pw;
+            s_ofs[q] = (long long)wn.b * g.Ci * HW + (long long)y0 * g.Wi + x0;
+            s_y0[q] = y0;
+            s_x0[q] = x0;
+            s_t[q] = wn.t;
+            const spk_stdp_config cf = s_cf[wn.cfg];
+            s_ap[q] = cf.a_plus;
+            s_am[q] = cf.a_minus;
+            s_lo[q] = cf.lower;
+            s_hi[q] = cf.upper;
+            s_st[q] = cf.stabilize != 0;
+        }
+        __syncthreads();
+        if (valid) {
+            constexpr int kB = 8;  // gathers issued ahead of the chain
+            for (int eb = 0; eb < m; eb += kB) {
+                int tj[kB];
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int e = eb + u;
+                    tj[u] = 0x7fffffff;  // padded input: never fires (R-NEVER)
+                    if (e < m) {
+                        const int iy = s_y0[e] + i1, ix = s_x0[e] + j1;
+                        if ((unsigned)iy < (unsigned)g.Hi && (unsigned)ix < (unsigned)g.Wi)
+                            tj[u] = __ldg(lat_in + s_ofs[e] + own);  // == T: never
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kB; ++u) {
+                    const int e = eb + u;
+                    if (e >= m) break;
+                    const float A = tj[u] <= s_t[e] ? s_ap[e] : s_am[e];  // R-EQ4-TIE
+                    const float lo = s_lo[e], hi = s_hi[e];
+                    // (W-L)(U-W) soft bound, Eq. 4; plain A, Eq. 5
+                    const float d = s_st[e] ? __fmul_rn(A, __fmul_rn(__fsub_rn(W, lo), __fsub_rn(hi, W))) : A;
+                    float nw = __fadd_rn(W, d);
+                    if (nw > hi) nw = hi;  // Eq. 6 on W + dW (R-EQ6-CLAMP)
+                    if (nw < lo) nw = lo;
+                    W = nw;
+                }
+            }
+        }
+    }
+    if (valid) w[(size_t)o * K + kk] = W;
+}
+
 }  // namespace
 
 extern "C" size_t spk_stdp_workspace(const spk_conv_geom* g, int k) {
@@ -250,6 +335,19 @@ extern "C" spk_status spk_stdp(float* w, const spk_conv_geom* g, const uint8_t* 
     if (st != SPK_OK) return st;
     const size_t K = (size_t)g->Ci * g->Kh * g->Kw;
     SPK_CHECK(g->Co <= 65535, SPK_ERR_SHAPE, "Co=%d > 65535", g->Co);
+    static const int pw = [] {  // A/B knob: SPK_STDP_PW=0 keeps the two-phase tiles, 2 forces the per-weight form
+        const char* e = std::getenv("SPK_STDP_PW");
+        return e ? std::atoi(e) : 1;
+    }();
+    // per-weight form for few winners per map on short rows (C1: K 50, FC: K 3200; FC 57 -> 24 us);
+    // maps with many winners (C2 layer 3: ~41, the chain dominates) keep the 32-weight tiles and
+    // few winners on long rows (C3 decision layer, K 6250) the 128-weight ones —
+    // profiles/r02_ab_stdp_pw.txt
+    if (pw == 2 || (pw == 1 && (long long)g->B * k < 16ll * g->Co && K < 4096)) {
+        const dim3 grid(spk::ceil_div(K, 256), (unsigned)g->Co);
+        spk::launch(stdp_update_pw_kernel<256>, grid, 256, 0, s, w, *g, lat_in, win, list, start, cnt, cc, ncfg);
+        return spk::launched("stdp_update_pw_kernel");
+    }
     // average winners per map (upper bound: every slot a winner) picks the tile width
     if ((long long)g->B * k >= 16ll * g->Co) {
         const dim3 grid(spk::ceil_div(K, 32), (unsigned)g->Co);
